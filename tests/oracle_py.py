@@ -1,0 +1,169 @@
+"""ctypes binding of the C oracle (oracle/swedg_oracle.c -> oracle/liboracle.so).
+
+TEST INFRASTRUCTURE: the checker the CUDA path is compared against.  Only
+tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg use it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(REPO, "oracle", "liboracle.so")
+GOLDEN = os.path.join(REPO, "tests", "golden")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+class OracleOps(C.Structure):
+    _fields_ = [
+        ("N", C.c_int), ("Np", C.c_int), ("nq", C.c_int), ("nf", C.c_int), ("npf", C.c_int),
+        ("K", C.c_int), ("scheme", C.c_int), ("penalty_lf", C.c_int), ("g", C.c_double),
+        ("Vq", _dp), ("Vf", _dp), ("Pq", _dp), ("Qr", _dp), ("Qs", _dp), ("wf", _dp),
+        ("face_index", _ip), ("gf", _dp), ("sJ", _dp), ("nx", _dp), ("ny", _dp),
+        ("Mh_inv", _dp), ("J_vol", _dp), ("M_diag", _dp), ("nbr", _ip), ("perm", _ip),
+        ("b_stacked", _dp), ("src_x", _dp), ("src_y", _dp),
+    ]
+
+
+def _build_lib() -> None:
+    src = os.path.join(REPO, "oracle", "swedg_oracle.c")
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(src):
+        subprocess.run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                        "-shared", src, "-o", LIB, "-lm"], check=True)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _build_lib()
+        _lib = C.CDLL(LIB)
+        _lib.oracle_set_bathymetry.argtypes = [C.POINTER(OracleOps), _dp, _dp, _dp, _dp]
+        _lib.oracle_entropy_projection.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip]
+        _lib.oracle_rhs_from_proj.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
+        _lib.oracle_rhs.argtypes = [C.POINTER(OracleOps), _dp, _dp, _dp, _ip]
+        _lib.oracle_rhs_sbp.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
+        _lib.oracle_step_lsrk45.argtypes = [C.POINTER(OracleOps), _dp, _dp, C.c_double, C.c_int, _ip]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _pi(a):
+    return None if a is None else a.ctypes.data_as(_ip)
+
+
+def load_golden(name: str) -> dict:
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    return {k: z[k] for k in z.files}
+
+
+class Oracle:
+    """The C restatement driven from a case dictionary (golden fixture layout)."""
+
+    def __init__(self, case: dict, penalty_lf: bool = True):
+        c = {k: np.ascontiguousarray(v) for k, v in case.items()}
+        self.c = c
+        self.scheme = int(c["scheme"][0])
+        sc = self.scheme
+        op = OracleOps()
+        op.N = int(c["N"][0])
+        op.Np = int(c["Np"][0])
+        op.nq = int(c["nq"][0])
+        op.nf = int(c["nf"][0])
+        op.npf = int(c["npf"][0])
+        op.K = int(c["K"][0])
+        op.scheme = sc
+        op.penalty_lf = 1 if penalty_lf else 0
+        op.g = float(c["g"][0])
+        # reference operators stored [cols][rows] == column-major
+        self._keep = []
+
+        def keep(a, dt=np.float64):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a
+
+        op.Vq = _p(keep(c["ref_Vq"]))
+        op.Vf = _p(keep(c["ref_Vf"]))
+        op.Pq = _p(keep(c["ref_Pq"]))
+        if sc == 1:
+            op.Qr = _p(keep(c["sbp_Qx"]))
+            op.Qs = _p(keep(c["sbp_Qy"]))
+            op.face_index = _pi(keep(c["sbp_face_index"], np.int32))
+            op.M_diag = _p(keep(c["sbp_M_diag"]))
+            op.J_vol = _p(keep(c["J_vol"]))
+        else:
+            op.Qr = _p(keep(c["ref_Qh_x"]))
+            op.Qs = _p(keep(c["ref_Qh_y"]))
+            op.Mh_inv = _p(keep(c["Mh_inv"]))
+        op.wf = _p(keep(c["surfq_w"]))
+        op.gf = _p(keep(c["gf"]))
+        op.sJ = _p(keep(c["sJ"]))
+        op.nx = _p(keep(c["nx"]))
+        op.ny = _p(keep(c["ny"]))
+        op.nbr = _pi(keep(c["nbr"], np.int32))
+        op.perm = _pi(keep(c["perm"], np.int32))
+        self.op = op
+        self.K, self.nq, self.nf, self.Np = op.K, op.nq, op.nf, op.Np
+        self.nh = op.nq + op.nf
+        self.set_bathymetry(c["b"])
+
+    def set_bathymetry(self, b):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        K = self.K
+        if self.scheme == 1:
+            self.b_stacked = np.zeros((K, self.nq))
+            self.src_x = np.zeros((K, self.nq))
+            self.src_y = np.zeros((K, self.nq))
+        else:
+            self.b_stacked = np.zeros((K, self.nh))
+            self.src_x = np.zeros((K, self.nh))
+            self.src_y = np.zeros((K, self.nh))
+        lib().oracle_set_bathymetry(C.byref(self.op), _p(b), _p(self.b_stacked), _p(self.src_x),
+                                    _p(self.src_y))
+        self.op.b_stacked = _p(self.b_stacked)
+        self.op.src_x = _p(self.src_x)
+        self.op.src_y = _p(self.src_y)
+
+    def entropy_projection(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        proj = np.zeros((self.K, 3, self.nh))
+        bad = C.c_int(-1)
+        err = lib().oracle_entropy_projection(C.byref(self.op), _p(u), _p(proj), C.byref(bad))
+        return proj, err, bad.value
+
+    def rhs(self, u, elems=None):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        bad = C.c_int(-1)
+        if self.scheme == 1:
+            du = np.zeros((self.K, 3, self.nq))
+            ei = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
+            err = lib().oracle_rhs_sbp(C.byref(self.op), _p(u), _p(du), _pi(ei),
+                                       0 if ei is None else len(ei), C.byref(bad))
+            return du, err, bad.value
+        proj, err, b = self.entropy_projection(u)
+        du = np.zeros((self.K, 3, self.Np))
+        if err:
+            return du, err, b
+        ei = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
+        err = lib().oracle_rhs_from_proj(C.byref(self.op), _p(proj), _p(du), _pi(ei),
+                                         0 if ei is None else len(ei), C.byref(bad))
+        return du, err, bad.value
+
+    def step_lsrk45(self, u, res, dt, nsteps):
+        u = np.array(u, dtype=np.float64, copy=True)
+        res = np.array(res, dtype=np.float64, copy=True)
+        bad = C.c_int(-1)
+        err = lib().oracle_step_lsrk45(C.byref(self.op), _p(u), _p(res), float(dt), int(nsteps),
+                                       C.byref(bad))
+        return u, res, err
