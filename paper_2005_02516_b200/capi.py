@@ -1,0 +1,319 @@
+"""ctypes binding of the C ABI (include/swedg_b200.h) — the host side of the drop-in.
+
+This is a thin, fail-loud layer: if libswedg_b200.so is missing or no CUDA
+device is present, every entry point raises; there is no CPU fallback.
+The C++ adapter for reference users is include/swedg_b200.hpp; this module
+serves the Python tests, bench.py and __graft_entry__.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+SWEDG_OK = 0
+SWEDG_ERR_INVALID = -1
+SWEDG_ERR_POSITIVITY = -2
+SWEDG_ERR_NONFINITE = -3
+SWEDG_ERR_CUDA = -4
+SWEDG_ERR_UNSUPPORTED = -5
+
+SCHEME_HYBRIDIZED = 0
+SCHEME_SBP = 1
+PENALTY_EC = 0
+PENALTY_LF = 1
+MODE_FAST = 0
+MODE_PARITY = 1
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+class SwedgError(RuntimeError):
+    """Reference: std::runtime_error thrown by rhs()/entropy_projection() (solver.hpp:176-180,288-290)."""
+
+    def __init__(self, code: int, msg: str, elem: int = -1, t: float = 0.0):
+        super().__init__(msg)
+        self.code, self.elem, self.t = code, elem, t
+
+
+class PositivityError(SwedgError):
+    """Nonpositive water height (swe.hpp:25-32 PositivityError, wrapped at solver.hpp:176-180)."""
+
+
+class NonFiniteError(SwedgError):
+    """Non-finite RHS (solver.hpp:288-290, :429-431)."""
+
+
+class InvalidArgument(SwedgError, ValueError):
+    """std::invalid_argument (e.g. dt <= 0, solver.hpp:468)."""
+
+
+class _Desc(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_int), ("scheme", C.c_int), ("penalty", C.c_int), ("mode", C.c_int),
+        ("N", C.c_int), ("Np", C.c_int), ("nq", C.c_int), ("nf", C.c_int), ("npf", C.c_int),
+        ("K", C.c_int), ("g", C.c_double), ("device", C.c_int),
+        ("Vq", _dp), ("Vf", _dp), ("Pq", _dp), ("Qr", _dp), ("Qs", _dp), ("wf", _dp),
+        ("face_index", _ip), ("M_diag", _dp),
+        ("gf", _dp), ("sJ", _dp), ("nx", _dp), ("ny", _dp), ("J_vol", _dp), ("Mh_inv", _dp),
+        ("nbr", _ip), ("perm", _ip),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree extension (building it first if sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if _build.needs_build():
+        _build.build()
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA extension missing: {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
+    vp = C.c_void_p
+    L.swedg_create.argtypes = [C.POINTER(_Desc), C.POINTER(vp)]
+    L.swedg_destroy.argtypes = [vp]
+    L.swedg_set_stream.argtypes = [vp, vp]
+    L.swedg_get_stream.argtypes = [vp]
+    L.swedg_get_stream.restype = vp
+    L.swedg_set_penalty.argtypes = [vp, C.c_int]
+    L.swedg_set_mode.argtypes = [vp, C.c_int]
+    L.swedg_set_bathymetry.argtypes = [vp, _dp]
+    L.swedg_entropy_projection.argtypes = [vp, _dp, C.c_double, _dp]
+    L.swedg_rhs.argtypes = [vp, _dp, C.c_double, _dp]
+    L.swedg_set_state.argtypes = [vp, _dp, _dp, C.c_double]
+    L.swedg_get_state.argtypes = [vp, _dp, _dp, _dp]
+    L.swedg_step_lsrk45.argtypes = [vp, C.c_double, C.c_int, C.c_int]
+    L.swedg_state_device_ptr.argtypes = [vp, C.POINTER(vp), C.POINTER(vp)]
+    L.swedg_rhs_device.argtypes = [vp, vp, vp, C.c_double]
+    L.swedg_check.argtypes = [vp]
+    L.swedg_last_error.argtypes = [vp, _ip, C.POINTER(C.c_long), _dp, C.c_char_p, C.c_size_t]
+    L.swedg_create_error.restype = C.c_char_p
+    L.swedg_launch_count.argtypes = [vp]
+    L.swedg_launch_count.restype = C.c_longlong
+    L.swedg_device_bytes.argtypes = [vp]
+    L.swedg_device_bytes.restype = C.c_size_t
+    L.swedg_debug_bathymetry.argtypes = [vp, _dp, _dp]
+    _lib = L
+    return L
+
+
+EXPORTED = [
+    "swedg_create", "swedg_destroy", "swedg_set_stream", "swedg_get_stream", "swedg_set_penalty",
+    "swedg_set_mode", "swedg_set_bathymetry", "swedg_entropy_projection", "swedg_rhs",
+    "swedg_set_state", "swedg_get_state", "swedg_step_lsrk45", "swedg_state_device_ptr",
+    "swedg_rhs_device", "swedg_check", "swedg_last_error", "swedg_create_error",
+    "swedg_launch_count", "swedg_device_bytes", "swedg_abi_version", "swedg_debug_bathymetry",
+]
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _pi(a):
+    return None if a is None else a.ctypes.data_as(_ip)
+
+
+@dataclass
+class Sizes:
+    N: int
+    Np: int
+    nq: int
+    nf: int
+    npf: int
+    K: int
+
+    @property
+    def nh(self) -> int:
+        return self.nq + self.nf
+
+
+class Handle:
+    """One device-resident solver instance (one rank's element block)."""
+
+    def __init__(self, *, scheme: int, N: int, Np: int, nq: int, nf: int, npf: int, K: int,
+                 g: float, Qr, Qs, wf, gf, sJ, nx, ny, nbr, perm, Vq=None, Vf=None, Pq=None,
+                 Mh_inv=None, face_index=None, M_diag=None, J_vol=None,
+                 penalty: int = PENALTY_LF, mode: int = MODE_FAST, device: int = 0):
+        L = lib()
+        self.sizes = Sizes(N, Np, nq, nf, npf, K)
+        self.scheme = scheme
+        keep = []
+
+        def f(a):
+            if a is None:
+                return None
+            a = _f64(a)
+            keep.append(a)
+            return _p(a)
+
+        def i(a):
+            if a is None:
+                return None
+            a = _i32(a)
+            keep.append(a)
+            return _pi(a)
+
+        d = _Desc()
+        d.abi_version = 1
+        d.scheme, d.penalty, d.mode = scheme, penalty, mode
+        d.N, d.Np, d.nq, d.nf, d.npf, d.K = N, Np, nq, nf, npf, K
+        d.g = float(g)
+        d.device = device
+        d.Vq, d.Vf, d.Pq, d.Qr, d.Qs, d.wf = f(Vq), f(Vf), f(Pq), f(Qr), f(Qs), f(wf)
+        d.face_index, d.M_diag = i(face_index), f(M_diag)
+        d.gf, d.sJ, d.nx, d.ny, d.J_vol, d.Mh_inv = f(gf), f(sJ), f(nx), f(ny), f(J_vol), f(Mh_inv)
+        d.nbr, d.perm = i(nbr), i(perm)
+        h = C.c_void_p()
+        rc = L.swedg_create(C.byref(d), C.byref(h))
+        if rc != SWEDG_OK:
+            raise _err_class(rc)(rc, "swedg_create: " + L.swedg_create_error().decode())
+        self._h = h
+        self._lib = L
+        self.nstate = nq if scheme == SCHEME_SBP else Np
+
+    # -- lifecycle -------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.swedg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc == SWEDG_OK:
+            return
+        code = C.c_int()
+        elem = C.c_long()
+        t = C.c_double()
+        buf = C.create_string_buffer(512)
+        self._lib.swedg_last_error(self._h, C.byref(code), C.byref(elem), C.byref(t), buf, 512)
+        raise _err_class(rc)(rc, buf.value.decode(), elem.value, t.value)
+
+    # -- API ------------------------------------------------------------------
+    def set_stream(self, stream_ptr: int | None):
+        self._check(self._lib.swedg_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    @property
+    def stream(self) -> int:
+        return self._lib.swedg_get_stream(self._h) or 0
+
+    def set_penalty(self, penalty: int):
+        self._check(self._lib.swedg_set_penalty(self._h, penalty))
+
+    def set_mode(self, mode: int):
+        self._check(self._lib.swedg_set_mode(self._h, mode))
+
+    def set_bathymetry(self, b):
+        b = _f64(b)
+        self._check(self._lib.swedg_set_bathymetry(self._h, _p(b)))
+
+    def bathymetry_products(self):
+        s = self.sizes
+        if self.scheme == SCHEME_SBP:
+            src = np.zeros((s.K, 2, s.nq))
+            self._check(self._lib.swedg_debug_bathymetry(self._h, None, _p(src)))
+            return None, src
+        bs = np.zeros((s.K, s.nh))
+        src = np.zeros((s.K, 2, s.nh))
+        self._check(self._lib.swedg_debug_bathymetry(self._h, _p(bs), _p(src)))
+        return bs, src
+
+    def entropy_projection(self, u, t: float = 0.0) -> np.ndarray:
+        s = self.sizes
+        u = _f64(u)
+        proj = np.zeros((s.K, 3, s.nh))
+        self._check(self._lib.swedg_entropy_projection(self._h, _p(u), float(t), _p(proj)))
+        return proj
+
+    def rhs(self, u, t: float = 0.0) -> np.ndarray:
+        s = self.sizes
+        u = _f64(u)
+        du = np.zeros((s.K, 3, self.nstate))
+        self._check(self._lib.swedg_rhs(self._h, _p(u), float(t), _p(du)))
+        return du
+
+    def set_state(self, u, res=None, t: float = 0.0):
+        u = _f64(u)
+        r = None if res is None else _f64(res)
+        self._check(self._lib.swedg_set_state(self._h, _p(u), _p(r), float(t)))
+
+    def get_state(self):
+        s = self.sizes
+        u = np.zeros((s.K, 3, self.nstate))
+        r = np.zeros_like(u)
+        t = C.c_double()
+        self._check(self._lib.swedg_get_state(self._h, _p(u), _p(r), C.byref(t)))
+        return u, r, t.value
+
+    def step(self, dt: float, nsteps: int = 1, sync: bool = True):
+        self._check(self._lib.swedg_step_lsrk45(self._h, float(dt), int(nsteps), 1 if sync else 0))
+
+    def check(self):
+        self._check(self._lib.swedg_check(self._h))
+
+    def state_device_ptrs(self):
+        u = C.c_void_p()
+        r = C.c_void_p()
+        self._check(self._lib.swedg_state_device_ptr(self._h, C.byref(u), C.byref(r)))
+        return u.value, r.value
+
+    def rhs_device(self, u_ptr: int, du_ptr: int, t: float = 0.0):
+        self._check(self._lib.swedg_rhs_device(self._h, C.c_void_p(u_ptr), C.c_void_p(du_ptr), float(t)))
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.swedg_launch_count(self._h))
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self._lib.swedg_device_bytes(self._h))
+
+
+def _err_class(rc: int):
+    return {SWEDG_ERR_POSITIVITY: PositivityError, SWEDG_ERR_NONFINITE: NonFiniteError,
+            SWEDG_ERR_INVALID: InvalidArgument}.get(rc, SwedgError)
+
+
+def handle_from_case(c: dict, *, penalty: int = PENALTY_LF, mode: int = MODE_FAST,
+                     device: int = 0, set_bathymetry: bool = True) -> Handle:
+    """Create a handle from a case dictionary in the golden-fixture layout
+    (tests/golden/*.npz: reference operators [cols][rows], per-element arrays)."""
+    scheme = int(c["scheme"][0]) if np.ndim(c["scheme"]) else int(c["scheme"])
+    sc = lambda k: int(np.asarray(c[k]).reshape(-1)[0])  # noqa: E731
+    kw = dict(scheme=scheme, N=sc("N"), Np=sc("Np"), nq=sc("nq"), nf=sc("nf"), npf=sc("npf"),
+              K=sc("K"), g=float(np.asarray(c["g"]).reshape(-1)[0]), wf=c["surfq_w"], gf=c["gf"],
+              sJ=c["sJ"], nx=c["nx"], ny=c["ny"], nbr=c["nbr"], perm=c["perm"],
+              penalty=penalty, mode=mode, device=device)
+    if scheme == SCHEME_SBP:
+        kw.update(Qr=c["sbp_Qx"], Qs=c["sbp_Qy"], face_index=c["sbp_face_index"],
+                  M_diag=c["sbp_M_diag"], J_vol=c["J_vol"])
+    else:
+        kw.update(Qr=c["ref_Qh_x"], Qs=c["ref_Qh_y"], Vq=c["ref_Vq"], Vf=c["ref_Vf"], Pq=c["ref_Pq"],
+                  Mh_inv=c["Mh_inv"])
+    h = Handle(**kw)
+    if set_bathymetry:
+        h.set_bathymetry(c["b"])
+    return h

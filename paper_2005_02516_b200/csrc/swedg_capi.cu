@@ -1,0 +1,734 @@
+// C ABI of the B200-native ESDG shallow-water RHS (include/swedg_b200.h).
+//
+// A handle owns every device buffer of one rank's element block: the
+// reference operators, per-element geometry, connectivity, bathymetry
+// source, the resident state and LSRK register, and the stage scratch
+// (face traces, surface-row accumulator, lifted volume part).  All work is
+// stream-ordered on the handle's stream; host-pointer entry points copy in,
+// launch, copy out and check the device error record.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/swedg_b200.h"
+#include "modal_kernels.cuh"
+#include "sbp_kernels.cuh"
+
+using namespace swedg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct swedg_handle_s {
+    int scheme, penalty, mode, N, Np, nq, nf, npf, nh, K;
+    double g;
+    int device;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // device buffers
+    double* ops = nullptr;   // packed reference operators
+    double* gf = nullptr;    // [K][4][nrow]
+    double* surf = nullptr;  // [K][3][nf]  w*sJ, nx, ny
+    double* Minv = nullptr;  // modal: [K][Np][Np]; SBP: [K][nq] diagonal
+    int* nbr = nullptr;      // [K][3]
+    int* perm = nullptr;     // [K][nf]
+    int* fidx = nullptr;     // SBP face_index [nf]
+    double* bs = nullptr;    // [K][nh] (modal)
+    double* src = nullptr;   // [K][2][nh] (SBP: [K][2][nq])
+    double* u = nullptr;     // resident state
+    double* res = nullptr;   // LSRK register
+    double* utmp = nullptr;  // host-API scratch state
+    double* du = nullptr;    // host-API scratch rhs
+    double* proj = nullptr;  // host-API scratch projection
+    double* trace = nullptr; // [K][3][nf]
+    double* accf = nullptr;  // [K][3][nf]
+    double* T1 = nullptr;    // [K][3][Np]
+    ErrRec* err = nullptr;
+    size_t dev_bytes = 0;
+    bool bathy_set = false;
+    unsigned next_stage = 1;
+    long long launches = 0;
+    double t = 0.0;
+    // error state
+    int last_code = SWEDG_OK;
+    long last_elem = -1;
+    double last_t = 0.0;
+    std::string last_msg;
+    // stage bookkeeping for error decoding (current call)
+    unsigned call_stage0 = 0;
+    std::vector<double> call_stage_t;
+    int nstate() const { return scheme == SWEDG_SCHEME_SBP ? nq : Np; }
+};
+
+namespace {
+
+int fail(swedg_handle h, int code, const std::string& msg, long elem = -1, double t = 0.0) {
+    if (h) {
+        h->last_code = code;
+        h->last_msg = msg;
+        h->last_elem = elem;
+        h->last_t = t;
+    } else {
+        g_create_error = msg;
+    }
+    return code;
+}
+
+#define CUDA_TRY(h, expr)                                                                  \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(h, SWEDG_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+int dalloc(swedg_handle h, T** p, size_t n) {
+    size_t bytes = n * sizeof(T);
+    if (bytes == 0) bytes = sizeof(T);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    if (e != cudaSuccess)
+        return fail(h, SWEDG_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    h->dev_bytes += bytes;
+    return SWEDG_OK;
+}
+
+template <class T>
+int upload(swedg_handle h, T* dst, const T* src, size_t n) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess)
+        return fail(h, SWEDG_ERR_CUDA, std::string("upload: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+// ---- kernel dispatch -------------------------------------------------------
+
+// Opt a kernel into its dynamic shared memory once per (kernel, device) and
+// return its occupancy (resident CTAs per SM) for persistent grids.
+int kernel_occupancy(const void* kern, int device, int threads, size_t smem) {
+    struct Entry {
+        const void* k;
+        int dev;
+        int occ;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& e : cache)
+        if (e.k == kern && e.dev == device) return e.occ;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    if (occ < 1) occ = 1;
+    cache.push_back({kern, device, occ});
+    return occ;
+}
+
+struct StageArgs {
+    const double* u_in;
+    double* proj;       // optional
+    bool rk;            // fused RK update on (h->u, h->res)
+    double a, b, dt;
+    double* du_out;     // rhs mode
+    unsigned stage_id;
+    bool early_exit;
+};
+
+template <int N>
+int run_modal_stage(swedg_handle h, const StageArgs& sa) {
+    ModalVolParams vp;
+    vp.K = h->K;
+    vp.g = h->g;
+    vp.ops = h->ops;
+    vp.u = sa.u_in;
+    vp.gf = h->gf;
+    vp.bs = h->bs;
+    vp.src = h->src;
+    vp.trace = h->trace;
+    vp.accf = h->accf;
+    vp.T1 = h->T1;
+    vp.proj = sa.proj;
+    vp.err = h->err;
+    vp.stage_id = sa.stage_id;
+    vp.early_exit = sa.early_exit ? 1 : 0;
+    using VC = VolCfg<N>;
+    const size_t smem = VolSmem<N>::bytes(VC::E);
+    const int nblk_needed = (h->K + VC::E - 1) / VC::E;
+    auto launch_vol = [&](void (*kern)(ModalVolParams)) -> int {
+        int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, VC::T, smem);
+        int grid = std::min(nblk_needed, occ * h->nsm);
+        if (grid < 1) grid = 1;
+        kern<<<grid, VC::T, smem, h->stream>>>(vp);
+        return SWEDG_OK;
+    };
+    if (h->mode == SWEDG_MODE_PARITY)
+        launch_vol(modal_volume_kernel<N, true>);
+    else
+        launch_vol(modal_volume_kernel<N, false>);
+    h->launches++;
+
+    ModalSurfParams sp;
+    sp.K = h->K;
+    sp.g = h->g;
+    sp.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
+    sp.ops = h->ops;
+    sp.trace = h->trace;
+    sp.accf = h->accf;
+    sp.T1 = h->T1;
+    sp.surf = h->surf;
+    sp.src = h->src;
+    sp.nbr = h->nbr;
+    sp.perm = h->perm;
+    sp.Minv = h->Minv;
+    sp.du = sa.du_out;
+    sp.u = h->u;
+    sp.res = h->res;
+    sp.rk_a = sa.a;
+    sp.rk_b = sa.b;
+    sp.dt = sa.dt;
+    sp.rk_mode = sa.rk ? 1 : 0;
+    sp.err = h->err;
+    sp.stage_id = sa.stage_id;
+    sp.early_exit = sa.early_exit ? 1 : 0;
+    using SC = SurfCfg<N>;
+    const int grid = (h->K + SC::E - 1) / SC::E;
+    if (h->mode == SWEDG_MODE_PARITY)
+        modal_surface_kernel<N, true><<<grid, SC::T, 0, h->stream>>>(sp);
+    else
+        modal_surface_kernel<N, false><<<grid, SC::T, 0, h->stream>>>(sp);
+    h->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+template <int N>
+int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
+    SbpParams sp;
+    sp.K = h->K;
+    sp.g = h->g;
+    sp.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
+    sp.ops = h->ops;
+    sp.fidx = h->fidx;
+    sp.u = sa.u_in;
+    sp.gf = h->gf;
+    sp.surf = h->surf;
+    sp.src = h->src;
+    sp.minv = h->Minv;
+    sp.nbr = h->nbr;
+    sp.perm = h->perm;
+    sp.du = sa.du_out;
+    sp.uo = h->u;
+    sp.res = h->res;
+    sp.rk_a = sa.a;
+    sp.rk_b = sa.b;
+    sp.dt = sa.dt;
+    sp.rk_mode = sa.rk ? 1 : 0;
+    sp.err = h->err;
+    sp.stage_id = sa.stage_id;
+    sp.early_exit = sa.early_exit ? 1 : 0;
+    sp.du_scratch = h->du;
+    using C = SbpCfg<N>;
+    const size_t smem = SbpSmem<N>::bytes(C::E);
+    const int grid = (h->K + C::E - 1) / C::E;
+    auto go = [&](void (*kern)(SbpParams)) {
+        kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, C::T, smem);
+        kern<<<grid, C::T, smem, h->stream>>>(sp);
+    };
+    if (h->mode == SWEDG_MODE_PARITY)
+        go(sbp_rhs_kernel<N, true>);
+    else
+        go(sbp_rhs_kernel<N, false>);
+    h->launches++;
+    if (sa.rk) {
+        // the SBP RHS reads neighbour states: the RK update runs after all du are known
+        SbpUpdateParams up;
+        up.n = (size_t)h->K * 3 * h->nq;
+        up.du = h->du;
+        up.u = h->u;
+        up.res = h->res;
+        up.a = sa.a;
+        up.b = sa.b;
+        up.dt = sa.dt;
+        up.err = h->err;
+        up.early_exit = sa.early_exit ? 1 : 0;
+        const int tb = 256;
+        const int gr = (int)std::min<size_t>((up.n + tb - 1) / tb, (size_t)h->nsm * 16);
+        if (h->mode == SWEDG_MODE_PARITY)
+            sbp_update_kernel<true><<<gr, tb, 0, h->stream>>>(up);
+        else
+            sbp_update_kernel<false><<<gr, tb, 0, h->stream>>>(up);
+        h->launches++;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+int run_stage(swedg_handle h, const StageArgs& sa) {
+    if (h->scheme == SWEDG_SCHEME_SBP) {
+        switch (h->N) {
+            case 1: return run_sbp_stage<1>(h, sa);
+            case 2: return run_sbp_stage<2>(h, sa);
+            case 3: return run_sbp_stage<3>(h, sa);
+            case 4: return run_sbp_stage<4>(h, sa);
+        }
+    } else {
+        switch (h->N) {
+            case 1: return run_modal_stage<1>(h, sa);
+            case 2: return run_modal_stage<2>(h, sa);
+            case 3: return run_modal_stage<3>(h, sa);
+            case 4: return run_modal_stage<4>(h, sa);
+        }
+    }
+    return fail(h, SWEDG_ERR_UNSUPPORTED, "degree not compiled in");
+}
+
+template <int N>
+void launch_modal_bathy(swedg_handle h, const double* db) {
+    ModalBathyParams bp;
+    bp.K = h->K;
+    bp.ops = h->ops;
+    bp.b = db;
+    bp.gf = h->gf;
+    bp.surf = h->surf;
+    bp.bs = h->bs;
+    bp.src = h->src;
+    int threads = ((ModalDims<N>::nh + 31) / 32) * 32;
+    modal_bathymetry_kernel<N><<<h->K, threads, 0, h->stream>>>(bp);
+    h->launches++;
+}
+
+template <int N>
+void launch_sbp_bathy(swedg_handle h, const double* db) {
+    SbpBathyParams bp;
+    bp.K = h->K;
+    bp.ops = h->ops;
+    bp.b = db;
+    bp.gf = h->gf;
+    bp.src = h->src;
+    int threads = ((SbpDims<N>::nq + 31) / 32) * 32;
+    sbp_bathymetry_kernel<N><<<h->K, threads, 0, h->stream>>>(bp);
+    h->launches++;
+}
+
+// Decode the device error record (syncs the stream).
+int check_errors(swedg_handle h, bool projection_wrapped = true) {
+    ErrRec rec;
+    CUDA_TRY(h, cudaMemcpyAsync(&rec, h->err, sizeof(rec), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (rec.key == kNoError) return SWEDG_OK;
+    unsigned stage = (unsigned)(rec.key >> 33);
+    int kern = (int)((rec.key >> 32) & 1);
+    long elem = (long)(rec.key & 0xffffffffull);
+    double t = h->t;
+    if (stage >= h->call_stage0 && stage - h->call_stage0 < h->call_stage_t.size())
+        t = h->call_stage_t[stage - h->call_stage0];
+    // reset for the next call
+    unsigned long long none = kNoError;
+    CUDA_TRY(h, cudaMemcpyAsync(h->err, &none, sizeof(none), cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (kern == 0) {
+        std::string msg = (projection_wrapped && h->scheme == SWEDG_SCHEME_HYBRIDIZED)
+                              ? "entropy projection failed in element " + std::to_string(elem) +
+                                    " at t = " + std::to_string(t) + ": nonpositive water height"
+                              : "nonpositive water height in element " + std::to_string(elem) +
+                                    " at t = " + std::to_string(t);
+        return fail(h, SWEDG_ERR_POSITIVITY, msg, elem, t);
+    }
+    std::string msg = std::string(h->scheme == SWEDG_SCHEME_SBP ? "non-finite SBP RHS" : "non-finite RHS") +
+                      " in element " + std::to_string(elem) + " at t = " + std::to_string(t);
+    return fail(h, SWEDG_ERR_NONFINITE, msg, elem, t);
+}
+
+int ensure_scratch(swedg_handle h) {
+    size_t ns = (size_t)h->K * 3 * h->nstate();
+    if (!h->utmp && dalloc(h, &h->utmp, ns)) return h->last_code;
+    if (!h->du && dalloc(h, &h->du, ns)) return h->last_code;
+    return SWEDG_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int swedg_abi_version(void) { return SWEDG_ABI_VERSION; }
+
+const char* swedg_create_error(void) { return g_create_error.c_str(); }
+
+int swedg_create(const swedg_desc* d, swedg_handle* out) {
+    if (!d || !out) return fail(nullptr, SWEDG_ERR_INVALID, "null descriptor");
+    *out = nullptr;
+    if (d->abi_version != SWEDG_ABI_VERSION) return fail(nullptr, SWEDG_ERR_INVALID, "ABI version mismatch");
+    if (d->scheme != SWEDG_SCHEME_HYBRIDIZED && d->scheme != SWEDG_SCHEME_SBP)
+        return fail(nullptr, SWEDG_ERR_INVALID, "unknown scheme");
+    if (d->N < 1 || d->N > 4) return fail(nullptr, SWEDG_ERR_UNSUPPORTED, "degree must be 1..4");
+    if (d->K < 1) return fail(nullptr, SWEDG_ERR_INVALID, "K must be >= 1");
+    const int N = d->N;
+    const int Np = (N + 1) * (N + 2) / 2, npf = N + 1, nf = 3 * npf;
+    int nq_expect = d->scheme == SWEDG_SCHEME_SBP ? (N == 1 ? 6 : N == 2 ? 12 : N == 3 ? 21 : 37) : (N + 1) * (N + 1);
+    if (d->Np != Np || d->npf != npf || d->nf != nf || d->nq != nq_expect)
+        return fail(nullptr, SWEDG_ERR_UNSUPPORTED,
+                    "operator sizes do not match the compiled degree-" + std::to_string(N) + " kernels");
+    if (!d->Qr || !d->Qs || !d->wf || !d->gf || !d->sJ || !d->nx || !d->ny || !d->nbr || !d->perm)
+        return fail(nullptr, SWEDG_ERR_INVALID, "missing descriptor array");
+    if (d->scheme == SWEDG_SCHEME_HYBRIDIZED && (!d->Vq || !d->Vf || !d->Pq || !d->Mh_inv))
+        return fail(nullptr, SWEDG_ERR_INVALID, "missing hybridized operator array");
+    if (d->scheme == SWEDG_SCHEME_SBP && (!d->face_index || !d->M_diag || !d->J_vol))
+        return fail(nullptr, SWEDG_ERR_INVALID, "missing SBP operator array");
+
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(nullptr, SWEDG_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(ce));
+    if (d->device < 0 || d->device >= ndev) return fail(nullptr, SWEDG_ERR_INVALID, "bad device ordinal");
+
+    auto* h = new swedg_handle_s();
+    h->scheme = d->scheme;
+    h->penalty = d->penalty;
+    h->mode = d->mode;
+    h->N = N;
+    h->Np = Np;
+    h->nq = d->nq;
+    h->nf = nf;
+    h->npf = npf;
+    h->nh = d->nq + nf;
+    h->K = d->K;
+    h->g = d->g;
+    h->device = d->device;
+    cudaSetDevice(h->device);
+    cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete h;
+        return fail(nullptr, SWEDG_ERR_CUDA, "stream creation failed");
+    }
+    h->own_stream = true;
+    auto bail = [&](int code) {
+        g_create_error = h->last_msg;
+        swedg_destroy(h);
+        return code;
+    };
+    const size_t K = (size_t)h->K;
+    const int nq = h->nq, nh = h->nh, nrow = nq + nf;
+
+    // ---- validate connectivity on the host (fail loudly, never silently)
+    for (size_t k = 0; k < K; ++k)
+        for (int f = 0; f < 3; ++f) {
+            int nb = d->nbr[k * 3 + f];
+            if (nb < -1 || nb >= h->K) {
+                fail(h, SWEDG_ERR_INVALID, "neighbour index out of range in element " + std::to_string(k));
+                return bail(SWEDG_ERR_INVALID);
+            }
+            if (nb >= 0)
+                for (int s = 0; s < npf; ++s) {
+                    int p = d->perm[k * nf + f * npf + s];
+                    if (p < 0 || p >= nf) {
+                        fail(h, SWEDG_ERR_INVALID, "face permutation out of range in element " + std::to_string(k));
+                        return bail(SWEDG_ERR_INVALID);
+                    }
+                }
+        }
+
+    // ---- reference operators
+    std::vector<double> ops;
+    if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
+        ops.reserve((size_t)nq * Np * 2 + (size_t)nf * Np + 4 * (size_t)nh * nh);
+        ops.insert(ops.end(), d->Vq, d->Vq + (size_t)nq * Np);
+        ops.insert(ops.end(), d->Vf, d->Vf + (size_t)nf * Np);
+        ops.insert(ops.end(), d->Pq, d->Pq + (size_t)Np * nq);
+        std::vector<double> qa((size_t)nh * nh), qb((size_t)nh * nh);
+        for (int j = 0; j < nh; ++j)
+            for (int i = 0; i < nh; ++i) {
+                qa[i + (size_t)j * nh] = 0.125 * (d->Qr[i + (size_t)j * nh] - d->Qr[j + (size_t)i * nh]);
+                qb[i + (size_t)j * nh] = 0.125 * (d->Qs[i + (size_t)j * nh] - d->Qs[j + (size_t)i * nh]);
+            }
+        ops.insert(ops.end(), qa.begin(), qa.end());
+        ops.insert(ops.end(), qb.begin(), qb.end());
+        ops.insert(ops.end(), d->Qr, d->Qr + (size_t)nh * nh);
+        ops.insert(ops.end(), d->Qs, d->Qs + (size_t)nh * nh);
+    } else {
+        // SBP: [Qr nq*nq][Qs nq*nq][QA][QB] with QA/QB = Q_SBP_x/4, Q_SBP_y/4 (FAST)
+        ops.insert(ops.end(), d->Qr, d->Qr + (size_t)nq * nq);
+        ops.insert(ops.end(), d->Qs, d->Qs + (size_t)nq * nq);
+        for (size_t x = 0; x < (size_t)nq * nq; ++x) ops.push_back(0.25 * d->Qr[x]);
+        for (size_t x = 0; x < (size_t)nq * nq; ++x) ops.push_back(0.25 * d->Qs[x]);
+    }
+    if (dalloc(h, &h->ops, ops.size()) || upload(h, h->ops, ops.data(), ops.size())) return bail(h->last_code);
+
+    // ---- geometry and connectivity
+    std::vector<double> surf(K * 3 * nf);
+    for (size_t k = 0; k < K; ++k)
+        for (int i = 0; i < nf; ++i) {
+            surf[(k * 3 + 0) * nf + i] = d->wf[i] * d->sJ[k * nf + i];  // m = w * sJ (solver.hpp:113)
+            surf[(k * 3 + 1) * nf + i] = d->nx[k * nf + i];
+            surf[(k * 3 + 2) * nf + i] = d->ny[k * nf + i];
+        }
+    if (dalloc(h, &h->gf, K * 4 * nrow) || upload(h, h->gf, d->gf, K * 4 * nrow)) return bail(h->last_code);
+    if (dalloc(h, &h->surf, surf.size()) || upload(h, h->surf, surf.data(), surf.size())) return bail(h->last_code);
+    if (dalloc(h, &h->nbr, K * 3) || upload(h, h->nbr, d->nbr, K * 3)) return bail(h->last_code);
+    {
+        std::vector<int> perm(d->perm, d->perm + K * nf);
+        for (size_t k = 0; k < K; ++k)
+            for (int f = 0; f < 3; ++f)
+                if (d->nbr[k * 3 + f] < 0)
+                    for (int s = 0; s < npf; ++s) perm[k * nf + f * npf + s] = 0;
+        if (dalloc(h, &h->perm, K * nf) || upload(h, h->perm, perm.data(), K * nf)) return bail(h->last_code);
+    }
+    if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
+        if (dalloc(h, &h->Minv, K * Np * Np) || upload(h, h->Minv, d->Mh_inv, K * Np * Np)) return bail(h->last_code);
+        if (dalloc(h, &h->bs, K * nh) || dalloc(h, &h->src, K * 2 * nh)) return bail(h->last_code);
+        if (dalloc(h, &h->trace, K * 3 * nf) || dalloc(h, &h->accf, K * 3 * nf) || dalloc(h, &h->T1, K * 3 * Np))
+            return bail(h->last_code);
+    } else {
+        std::vector<double> minv(K * nq);
+        for (size_t k = 0; k < K; ++k)
+            for (int i = 0; i < nq; ++i) minv[k * nq + i] = 1.0 / (d->M_diag[i] * d->J_vol[k * nq + i]);  // :357
+        if (dalloc(h, &h->Minv, K * nq) || upload(h, h->Minv, minv.data(), K * nq)) return bail(h->last_code);
+        if (dalloc(h, &h->fidx, nf) || upload(h, h->fidx, d->face_index, nf)) return bail(h->last_code);
+        if (dalloc(h, &h->src, K * 2 * nq)) return bail(h->last_code);
+    }
+    const size_t ns = K * 3 * h->nstate();
+    if (dalloc(h, &h->u, ns) || dalloc(h, &h->res, ns)) return bail(h->last_code);
+    if (h->scheme == SWEDG_SCHEME_SBP && dalloc(h, &h->du, ns)) return bail(h->last_code);
+    if (dalloc(h, &h->err, 1)) return bail(h->last_code);
+    unsigned long long none = kNoError;
+    if (cudaMemcpyAsync(h->err, &none, sizeof(none), cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+        cudaMemsetAsync(h->u, 0, ns * sizeof(double), h->stream) != cudaSuccess ||
+        cudaMemsetAsync(h->res, 0, ns * sizeof(double), h->stream) != cudaSuccess ||
+        cudaMemsetAsync(h->src, 0, K * 2 * (h->scheme == SWEDG_SCHEME_SBP ? nq : nh) * sizeof(double), h->stream) != cudaSuccess)
+        return bail(fail(h, SWEDG_ERR_CUDA, "initialisation failed"));
+    if (h->bs && cudaMemsetAsync(h->bs, 0, K * nh * sizeof(double), h->stream) != cudaSuccess)
+        return bail(fail(h, SWEDG_ERR_CUDA, "initialisation failed"));
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) return bail(fail(h, SWEDG_ERR_CUDA, "sync failed"));
+    *out = h;
+    return SWEDG_OK;
+}
+
+int swedg_destroy(swedg_handle h) {
+    if (!h) return SWEDG_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    void* ptrs[] = {h->ops, h->gf, h->surf, h->Minv, h->nbr, h->perm, h->fidx, h->bs, h->src, h->u,
+                    h->res, h->utmp, h->du, h->proj, h->trace, h->accf, h->T1, h->err};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return SWEDG_OK;
+}
+
+int swedg_set_stream(swedg_handle h, void* stream) {
+    if (!h) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    if (stream) {
+        h->stream = static_cast<cudaStream_t>(stream);
+        h->own_stream = false;
+    } else {
+        cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        h->own_stream = true;
+    }
+    return SWEDG_OK;
+}
+
+void* swedg_get_stream(swedg_handle h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int swedg_set_penalty(swedg_handle h, int penalty) {
+    if (!h || (penalty != SWEDG_PENALTY_EC && penalty != SWEDG_PENALTY_LF)) return SWEDG_ERR_INVALID;
+    h->penalty = penalty;
+    return SWEDG_OK;
+}
+
+int swedg_set_mode(swedg_handle h, int mode) {
+    if (!h || (mode != SWEDG_MODE_FAST && mode != SWEDG_MODE_PARITY)) return SWEDG_ERR_INVALID;
+    h->mode = mode;
+    return SWEDG_OK;
+}
+
+int swedg_set_bathymetry(swedg_handle h, const double* b) {
+    if (!h || !b) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    const size_t nb = (size_t)h->K * (h->scheme == SWEDG_SCHEME_SBP ? h->nq : h->Np);
+    double* db = nullptr;
+    if (dalloc(h, &db, nb)) return h->last_code;
+    h->dev_bytes -= nb * sizeof(double);
+    if (upload(h, db, b, nb)) {
+        cudaFree(db);
+        return h->last_code;
+    }
+    if (h->scheme == SWEDG_SCHEME_SBP) {
+        switch (h->N) {
+            case 1: launch_sbp_bathy<1>(h, db); break;
+            case 2: launch_sbp_bathy<2>(h, db); break;
+            case 3: launch_sbp_bathy<3>(h, db); break;
+            case 4: launch_sbp_bathy<4>(h, db); break;
+        }
+    } else {
+        switch (h->N) {
+            case 1: launch_modal_bathy<1>(h, db); break;
+            case 2: launch_modal_bathy<2>(h, db); break;
+            case 3: launch_modal_bathy<3>(h, db); break;
+            case 4: launch_modal_bathy<4>(h, db); break;
+        }
+    }
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    cudaFree(db);
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("set_bathymetry: ") + cudaGetErrorString(e));
+    h->bathy_set = true;
+    return SWEDG_OK;
+}
+
+// Device pointers of the bathymetry products (for tests): b_stacked, src
+int swedg_debug_bathymetry(swedg_handle h, double* bs, double* src) {
+    if (!h) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    const size_t K = h->K;
+    if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
+        if (bs) CUDA_TRY(h, cudaMemcpyAsync(bs, h->bs, K * h->nh * 8, cudaMemcpyDeviceToHost, h->stream));
+        if (src) CUDA_TRY(h, cudaMemcpyAsync(src, h->src, K * 2 * h->nh * 8, cudaMemcpyDeviceToHost, h->stream));
+    } else if (src) {
+        CUDA_TRY(h, cudaMemcpyAsync(src, h->src, K * 2 * h->nq * 8, cudaMemcpyDeviceToHost, h->stream));
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return SWEDG_OK;
+}
+
+int swedg_entropy_projection(swedg_handle h, const double* u, double t, double* proj) {
+    if (!h || !u || !proj) return SWEDG_ERR_INVALID;
+    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED) return fail(h, SWEDG_ERR_INVALID, "entropy projection is hybridized-only");
+    cudaSetDevice(h->device);
+    if (ensure_scratch(h)) return h->last_code;
+    const size_t K = h->K;
+    if (!h->proj && dalloc(h, &h->proj, K * 3 * h->nh)) return h->last_code;
+    if (upload(h, h->utmp, u, K * 3 * h->Np)) return h->last_code;
+    h->call_stage0 = h->next_stage;
+    h->call_stage_t.assign(1, t);
+    StageArgs sa{h->utmp, h->proj, false, 0, 0, 0, h->du, h->next_stage++, false};
+    if (run_stage(h, sa)) return h->last_code;
+    CUDA_TRY(h, cudaMemcpyAsync(proj, h->proj, K * 3 * h->nh * 8, cudaMemcpyDeviceToHost, h->stream));
+    int rc = check_errors(h);
+    if (rc && h->last_code == SWEDG_ERR_NONFINITE) return SWEDG_OK;  // projection itself succeeded
+    return rc;
+}
+
+int swedg_rhs(swedg_handle h, const double* u, double t, double* du) {
+    if (!h || !u || !du) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    if (ensure_scratch(h)) return h->last_code;
+    const size_t n = (size_t)h->K * 3 * h->nstate();
+    if (upload(h, h->utmp, u, n)) return h->last_code;
+    h->call_stage0 = h->next_stage;
+    h->call_stage_t.assign(1, t);
+    StageArgs sa{h->utmp, nullptr, false, 0, 0, 0, h->du, h->next_stage++, false};
+    if (run_stage(h, sa)) return h->last_code;
+    CUDA_TRY(h, cudaMemcpyAsync(du, h->du, n * 8, cudaMemcpyDeviceToHost, h->stream));
+    return check_errors(h);
+}
+
+int swedg_rhs_device(swedg_handle h, const double* u_dev, double* du_dev, double t) {
+    if (!h || !u_dev || !du_dev) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    if (h->scheme == SWEDG_SCHEME_SBP && ensure_scratch(h)) return h->last_code;
+    h->call_stage0 = h->next_stage;
+    h->call_stage_t.assign(1, t);
+    StageArgs sa{u_dev, nullptr, false, 0, 0, 0, du_dev, h->next_stage++, false};
+    return run_stage(h, sa);
+}
+
+int swedg_set_state(swedg_handle h, const double* u, const double* res, double t) {
+    if (!h || !u) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    const size_t n = (size_t)h->K * 3 * h->nstate();
+    if (upload(h, h->u, u, n)) return h->last_code;
+    if (res) {
+        if (upload(h, h->res, res, n)) return h->last_code;
+    } else {
+        CUDA_TRY(h, cudaMemsetAsync(h->res, 0, n * 8, h->stream));
+    }
+    h->t = t;
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return SWEDG_OK;
+}
+
+int swedg_get_state(swedg_handle h, double* u, double* res, double* t) {
+    if (!h) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    const size_t n = (size_t)h->K * 3 * h->nstate();
+    if (u) CUDA_TRY(h, cudaMemcpyAsync(u, h->u, n * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (res) CUDA_TRY(h, cudaMemcpyAsync(res, h->res, n * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (t) *t = h->t;
+    return SWEDG_OK;
+}
+
+int swedg_state_device_ptr(swedg_handle h, double** u, double** res) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (u) *u = h->u;
+    if (res) *res = h->res;
+    return SWEDG_OK;
+}
+
+int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    if (nsteps < 0) return fail(h, SWEDG_ERR_INVALID, "nsteps must be >= 0");
+    cudaSetDevice(h->device);
+    h->call_stage0 = h->next_stage;
+    h->call_stage_t.clear();
+    for (int n = 0; n < nsteps; ++n) {
+        const double t0 = h->t;
+        for (int s = 0; s < 5; ++s) {
+            h->call_stage_t.push_back(t0 + Lsrk45::c[s] * dt);
+            StageArgs sa{h->u, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, h->next_stage++, true};
+            if (run_stage(h, sa)) return h->last_code;
+        }
+        h->t = t0 + dt;
+    }
+    if (sync) return check_errors(h);
+    return SWEDG_OK;
+}
+
+int swedg_check(swedg_handle h) {
+    if (!h) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    return check_errors(h);
+}
+
+int swedg_last_error(swedg_handle h, int* code, long* elem, double* t, char* msg, size_t len) {
+    if (!h) {
+        if (msg && len) {
+            std::strncpy(msg, g_create_error.c_str(), len - 1);
+            msg[len - 1] = 0;
+        }
+        return SWEDG_OK;
+    }
+    if (code) *code = h->last_code;
+    if (elem) *elem = h->last_elem;
+    if (t) *t = h->last_t;
+    if (msg && len) {
+        std::strncpy(msg, h->last_msg.c_str(), len - 1);
+        msg[len - 1] = 0;
+    }
+    return SWEDG_OK;
+}
+
+long long swedg_launch_count(swedg_handle h) { return h ? h->launches : 0; }
+
+size_t swedg_device_bytes(swedg_handle h) { return h ? h->dev_bytes : 0; }
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+"""GPU parity of the CUDA path against the reference (golden fixtures) and the C oracle.
+
+Every call goes through the C ABI (include/swedg_b200.h) via
+paper_2005_02516_b200.capi.  Two arithmetic modes are tested:
+
+  PARITY  reference evaluation order, no FMA contraction: asserted BIT-FOR-BIT
+          equal to the reference's outputs (tests/golden, produced by the
+          unmodified reference headers) — projection, bathymetry source, RHS
+          with LF and EC penalties, LSRK45 steps and whole runs.
+  FAST    the production kernels (FMA, reassociated flux differencing):
+          asserted within the north-star tolerance
+              max|du - du_ref| / (1 + max|du_ref|) <= 1e-12   per RHS
+              max|u  - u_ref|  / (1 + max|u_ref|)  <= 1e-10   after the config horizon
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle_py import Oracle, load_golden
+
+pytestmark = pytest.mark.gpu
+
+capi = pytest.importorskip("paper_2005_02516_b200.capi")
+
+MODAL = ["modal_n1_affine", "modal_n2_walls", "modal_n3_warp", "modal_n4_warp", "modal_n4_affine"]
+SBP = ["sbp_dam_n4", "sbp_lake_n3", "sbp_vortex_n2"]
+RHS_TOL = 1e-12
+RUN_TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / (1.0 + np.abs(b).max()))
+
+
+def make(c, mode, penalty=capi.PENALTY_LF):
+    return capi.handle_from_case(c, mode=mode, penalty=penalty)
+
+
+def run_like_reference(h, u0, dt, tfinal):
+    """run.hpp:230-262 step sequence on the device-resident state."""
+    nsteps = int(math.ceil(tfinal / dt - 1e-12)) if tfinal > 0 else 0
+    h.set_state(u0, None, 0.0)
+    t = 0.0
+    steps = 0
+    for _ in range(nsteps):
+        step_dt = min(dt, tfinal - t)
+        if step_dt <= 0.0:
+            break
+        h.step(step_dt, 1, sync=False)
+        t = t + step_dt
+        steps += 1
+    h.check()
+    u, _, _ = h.get_state()
+    return u, steps
+
+
+@pytest.mark.parametrize("name", MODAL)
+def test_modal_parity_bitwise(name):
+    c = load_golden(name)
+    h = make(c, capi.MODE_PARITY)
+    bs, src = h.bathymetry_products()
+    np.testing.assert_array_equal(bs, c["b_stacked"])
+    np.testing.assert_array_equal(src[:, 0], c["src_x"])
+    np.testing.assert_array_equal(src[:, 1], c["src_y"])
+    np.testing.assert_array_equal(h.entropy_projection(c["u"]), c["proj"])
+    np.testing.assert_array_equal(h.rhs(c["u"]), c["du_lf"])
+    h.set_penalty(capi.PENALTY_EC)
+    np.testing.assert_array_equal(h.rhs(c["u"]), c["du_ec"])
+    h.set_penalty(capi.PENALTY_LF)
+    h.set_state(c["u"])
+    h.step(float(c["dt"][0]), int(c["nsteps"][0]))
+    u, res, _ = h.get_state()
+    np.testing.assert_array_equal(u, c["u_steps"])
+    np.testing.assert_array_equal(res, c["res_steps"])
+
+
+@pytest.mark.parametrize("name", MODAL)
+def test_modal_fast_within_tolerance(name):
+    c = load_golden(name)
+    h = make(c, capi.MODE_FAST)
+    assert rel(h.entropy_projection(c["u"]), c["proj"]) <= 1e-13
+    assert rel(h.rhs(c["u"]), c["du_lf"]) <= RHS_TOL
+    h.set_penalty(capi.PENALTY_EC)
+    assert rel(h.rhs(c["u"]), c["du_ec"]) <= RHS_TOL
+
+
+@pytest.mark.parametrize("name", ["c1_vortex", "c2_lake", "dam_n3"])
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_problem_runs(name, mode):
+    c = load_golden(name)
+    h = make(c, capi.MODE_PARITY if mode == "parity" else capi.MODE_FAST)
+    du = h.rhs(c["u"])
+    u, steps = run_like_reference(h, c["u"], float(c["dt"][0]), float(c["tfinal"][0]))
+    assert steps == int(c["run_steps"][0])
+    if mode == "parity":
+        np.testing.assert_array_equal(du, c["du_lf"])
+        np.testing.assert_array_equal(u, c["u_final"])
+    else:
+        assert rel(du, c["du_lf"]) <= RHS_TOL
+        assert rel(u, c["u_final"]) <= RUN_TOL
+
+
+def test_lake_at_rest_preserved_to_roundoff():
+    c = load_golden("c2_lake")
+    for mode in (capi.MODE_PARITY, capi.MODE_FAST):
+        h = make(c, mode)
+        assert np.abs(h.rhs(c["u"])).max() < 1e-10
+        u, _ = run_like_reference(h, c["u"], float(c["dt"][0]), float(c["tfinal"][0]))
+        assert np.abs(u - c["u"]).max() < 1e-10
+
+
+@pytest.mark.parametrize("name", SBP)
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_sbp(name, mode):
+    c = load_golden(name)
+    h = make(c, capi.MODE_PARITY if mode == "parity" else capi.MODE_FAST)
+    _, src = h.bathymetry_products()
+    du = h.rhs(c["u"])
+    h.set_penalty(capi.PENALTY_EC)
+    du_ec = h.rhs(c["u"])
+    h.set_penalty(capi.PENALTY_LF)
+    u, steps = run_like_reference(h, c["u"], float(c["dt"][0]), float(c["tfinal"][0]))
+    assert steps == int(c["run_steps"][0])
+    if mode == "parity":
+        np.testing.assert_array_equal(src[:, 0], c["src_x"])
+        np.testing.assert_array_equal(src[:, 1], c["src_y"])
+        np.testing.assert_array_equal(du, c["du_lf"])
+        np.testing.assert_array_equal(du_ec, c["du_ec"])
+        np.testing.assert_array_equal(u, c["u_final"])
+    else:
+        assert rel(du, c["du_lf"]) <= RHS_TOL
+        assert rel(du_ec, c["du_ec"]) <= RHS_TOL
+        assert rel(u, c["u_final"]) <= RUN_TOL
+
+
+def test_positivity_error_names_element_1():
+    c = load_golden("positivity")
+    h = make(c, capi.MODE_FAST)
+    with pytest.raises(capi.PositivityError) as ei:
+        h.rhs(c["u"])
+    assert "element 1" in str(ei.value)
+    assert ei.value.elem == 1
+
+
+def test_dt_must_be_positive():
+    c = load_golden("modal_n1_affine")
+    h = make(c, capi.MODE_FAST)
+    h.set_state(c["u"])
+    with pytest.raises(capi.InvalidArgument):
+        h.step(-1.0, 1)
+
+
+def test_oracle_agrees_with_gpu_on_perturbed_state():
+    """Random admissible perturbation (not in any fixture): GPU vs C oracle."""
+    c = load_golden("modal_n4_warp")
+    rng = np.random.default_rng(7)
+    u = c["u"] + 0.01 * rng.standard_normal(c["u"].shape)
+    orc = Oracle(c)
+    ref, err, _ = orc.rhs(u)
+    assert err == 0
+    h = make(c, capi.MODE_PARITY)
+    np.testing.assert_array_equal(h.rhs(u), ref)
+    h.set_mode(capi.MODE_FAST)
+    assert rel(h.rhs(u), ref) <= RHS_TOL
