@@ -1,0 +1,59 @@
+/*
+ * swedg_setup.h — native case setup (host C++, multithreaded) that produces
+ * every input of swedg_create for the reference's problems, without the
+ * reference.  It restates, for a standalone user:
+ *   quadrature.hpp  surface/volume/SBP rules        refelem.hpp  Dubiner basis, RefOperators,
+ *   mesh.hpp        uniform mesh, warp, dam snap/fit, connect (O(K log K)), geometry, match_faces
+ *   solver.hpp      precompute_element_ops (M_h^{-1}), compute_dt
+ *   diagnostics.hpp / run.hpp   make_state, make_nodal_state, lake / vortex / dam-break builders
+ *   tests/test_solver.cpp:14-25 smooth_state (the C4/C5 "smooth wave" workload)
+ * Arrays are owned by the case; swedg_case_fill_desc points a swedg_desc at them.
+ */
+#ifndef SWEDG_SETUP_H
+#define SWEDG_SETUP_H
+
+#include <stddef.h>
+
+#include "swedg_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWEDG_PROBLEM_LAKE 0     /* run.hpp:116-137  lake at rest, [-1,1]^2 periodic, g = 9.81 */
+#define SWEDG_PROBLEM_VORTEX 1   /* run.hpp:139-154  translating vortex, [-10,10]x[-5,5], g = 2 */
+#define SWEDG_PROBLEM_DAMBREAK 2 /* run.hpp:159-209  curved dam x = y^2/25, walls, g = 9.81 */
+#define SWEDG_PROBLEM_SMOOTH 3   /* smooth_state(seed) on [-1,1]^2 periodic + lake bathymetry */
+
+typedef struct swedg_case_s* swedg_case;
+
+typedef struct {
+    int problem;     /* SWEDG_PROBLEM_* */
+    int scheme;      /* SWEDG_SCHEME_* */
+    int N;           /* degree */
+    int nx, ny;      /* quads per direction (K = 2 nx ny) */
+    double warp;     /* mesh warp amplitude (mesh.hpp:111-130), 0 = affine */
+    double cfl;      /* dt = cfl * h_min / ((N+1)(N+2)/2) */
+    double g;        /* <= 0: the problem's default */
+    unsigned seed;   /* SMOOTH: mt19937 seed of smooth_state */
+    int threads;     /* host threads, <= 0: hardware concurrency */
+} swedg_case_config;
+
+int swedg_case_build(const swedg_case_config* cfg, swedg_case* out);
+int swedg_case_destroy(swedg_case c);
+const char* swedg_case_error(void);
+/* Fill every operator/geometry/connectivity pointer and size of *d (penalty,
+ * mode and device are left for the caller). */
+int swedg_case_fill_desc(swedg_case c, swedg_desc* d);
+/* Named host arrays: "u0" [K][3][n], "b" [K][n], "xy_vol" [K][2][nq], "map_coeffs" [K][2][Np],
+ * "J_vol" [K][nq], "volq_w" [nq], "Vq" ... ; returns element count via *n. */
+const double* swedg_case_array(swedg_case c, const char* name, size_t* n);
+const int* swedg_case_iarray(swedg_case c, const char* name, size_t* n);
+double swedg_case_dt(swedg_case c);
+double swedg_case_min_edge(swedg_case c);
+int swedg_case_K(swedg_case c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWEDG_SETUP_H */

@@ -317,3 +317,124 @@ def handle_from_case(c: dict, *, penalty: int = PENALTY_LF, mode: int = MODE_FAS
     if set_bathymetry:
         h.set_bathymetry(c["b"])
     return h
+
+
+# ---------------------------------------------------------------------------
+# native case setup (include/swedg_setup.h)
+PROBLEM_LAKE = 0
+PROBLEM_VORTEX = 1
+PROBLEM_DAMBREAK = 2
+PROBLEM_SMOOTH = 3
+PROBLEMS = {"lake": PROBLEM_LAKE, "vortex": PROBLEM_VORTEX, "dambreak": PROBLEM_DAMBREAK,
+            "smooth": PROBLEM_SMOOTH}
+
+
+class _CaseCfg(C.Structure):
+    _fields_ = [("problem", C.c_int), ("scheme", C.c_int), ("N", C.c_int), ("nx", C.c_int),
+                ("ny", C.c_int), ("warp", C.c_double), ("cfl", C.c_double), ("g", C.c_double),
+                ("seed", C.c_uint), ("threads", C.c_int)]
+
+
+def _setup_lib():
+    L = lib()
+    if not getattr(L, "_setup_bound", False):
+        vp = C.c_void_p
+        L.swedg_case_build.argtypes = [C.POINTER(_CaseCfg), C.POINTER(vp)]
+        L.swedg_case_destroy.argtypes = [vp]
+        L.swedg_case_error.restype = C.c_char_p
+        L.swedg_case_fill_desc.argtypes = [vp, C.POINTER(_Desc)]
+        L.swedg_case_array.argtypes = [vp, C.c_char_p, C.POINTER(C.c_size_t)]
+        L.swedg_case_array.restype = _dp
+        L.swedg_case_iarray.argtypes = [vp, C.c_char_p, C.POINTER(C.c_size_t)]
+        L.swedg_case_iarray.restype = _ip
+        L.swedg_case_dt.argtypes = [vp]
+        L.swedg_case_dt.restype = C.c_double
+        L.swedg_case_min_edge.argtypes = [vp]
+        L.swedg_case_min_edge.restype = C.c_double
+        L.swedg_case_K.argtypes = [vp]
+        L._setup_bound = True
+    return L
+
+
+class Case:
+    """A problem built by the native setup (lake / vortex / dambreak / smooth)."""
+
+    def __init__(self, problem="smooth", *, scheme=SCHEME_HYBRIDIZED, N=4, nx=16, ny=None,
+                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0):
+        L = _setup_lib()
+        cfg = _CaseCfg()
+        cfg.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
+        cfg.scheme, cfg.N, cfg.nx, cfg.ny = scheme, N, nx, ny if ny is not None else nx
+        cfg.warp, cfg.cfl, cfg.g, cfg.seed, cfg.threads = warp, cfl, g, seed, threads
+        h = C.c_void_p()
+        rc = L.swedg_case_build(C.byref(cfg), C.byref(h))
+        if rc != SWEDG_OK:
+            raise _err_class(rc)(rc, "swedg_case_build: " + L.swedg_case_error().decode())
+        self._c, self._lib = h, L
+        self.scheme, self.N = scheme, N
+        self.desc = _Desc()
+        L.swedg_case_fill_desc(self._c, C.byref(self.desc))
+        d = self.desc
+        self.K, self.Np, self.nq, self.nf, self.npf = d.K, d.Np, d.nq, d.nf, d.npf
+        self.g = d.g
+        self.dt = L.swedg_case_dt(self._c)
+        self.min_edge = L.swedg_case_min_edge(self._c)
+        self.nstate = self.nq if scheme == SCHEME_SBP else self.Np
+
+    def array(self, name: str) -> np.ndarray:
+        n = C.c_size_t()
+        p = self._lib.swedg_case_array(self._c, name.encode(), C.byref(n))
+        if not p:
+            raise KeyError(name)
+        return np.ctypeslib.as_array(p, shape=(n.value,)).copy() if n.value else np.zeros(0)
+
+    def iarray(self, name: str) -> np.ndarray:
+        n = C.c_size_t()
+        p = self._lib.swedg_case_iarray(self._c, name.encode(), C.byref(n))
+        if not p:
+            raise KeyError(name)
+        return np.ctypeslib.as_array(p, shape=(n.value,)).copy() if n.value else np.zeros(0, np.int32)
+
+    def u0(self) -> np.ndarray:
+        return self.array("u0").reshape(self.K, 3, self.nstate)
+
+    def b(self) -> np.ndarray:
+        return self.array("b").reshape(self.K, self.nstate)
+
+    def handle(self, *, penalty=PENALTY_LF, mode=MODE_FAST, device=0, set_bathymetry=True) -> "Handle":
+        return Handle.from_desc(self.desc, self, penalty=penalty, mode=mode, device=device,
+                                b=self.b() if set_bathymetry else None)
+
+    def close(self):
+        if getattr(self, "_c", None):
+            self._lib.swedg_case_destroy(self._c)
+            self._c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _handle_from_desc(cls, desc, owner, *, penalty=PENALTY_LF, mode=MODE_FAST, device=0, b=None):
+    L = lib()
+    d = _Desc()
+    C.pointer(d)[0] = desc
+    d.penalty, d.mode, d.device = penalty, mode, device
+    h = C.c_void_p()
+    rc = L.swedg_create(C.byref(d), C.byref(h))
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, "swedg_create: " + L.swedg_create_error().decode())
+    self = cls.__new__(cls)
+    self._h, self._lib = h, L
+    self.sizes = Sizes(d.N, d.Np, d.nq, d.nf, d.npf, d.K)
+    self.scheme = d.scheme
+    self.nstate = d.nq if d.scheme == SCHEME_SBP else d.Np
+    self._owner = owner
+    if b is not None:
+        self.set_bathymetry(b)
+    return self
+
+
+Handle.from_desc = classmethod(_handle_from_desc)
