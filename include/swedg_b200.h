@@ -151,6 +151,16 @@ int swedg_last_error(swedg_handle h, int* code, long* elem, double* t, char* msg
 const char* swedg_create_error(void);
 
 /* ---- introspection ---------------------------------------------------------- */
+/* Per-kernel CUDA-event timers on the handle's stream (off by default).  Kernel
+ * classes: 0 = volume kernel (modal projection+volume / SBP rhs), 1 = surface +
+ * update kernel (modal) / RK update (SBP).  swedg_read_timers syncs, returns the
+ * summed milliseconds and launch counts since the last read, and resets them. */
+int swedg_enable_timers(swedg_handle h, int on);
+int swedg_read_timers(swedg_handle h, double* ms, long long* launches, int nclass);
+/* Measured FP64 (DFMA) throughput of the device in TFLOP/s (FMA = 2 flops):
+ * a register-resident DFMA chain kernel, best of `reps` timed launches. */
+int swedg_probe_fp64_peak(int device, int reps, double* tflops);
+
 /* Number of kernels launched by this handle since creation (evidence counter). */
 long long swedg_launch_count(swedg_handle h);
 /* Device memory held by the handle, bytes. */

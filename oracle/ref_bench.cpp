@@ -1,0 +1,68 @@
+// swedg_refbench — times the UNMODIFIED reference CPU hot path (built against
+// oracle/shim into oracle/_ref/) on the bench workload — TEST / BASELINE
+// INFRASTRUCTURE ONLY (bench.py --impl reference and bench.py's cpu_baseline).
+//
+// Workload = bench.py's: modal ESDG (hybridized) degree N, smooth_state field
+// (tests/test_solver.cpp:14-25 generator, seed 23) with lake bathymetry on the
+// warped periodic [-1,1]^2 mesh, LSRK45 steps of the reference's own
+// step_lsrk45 (solver.hpp:466-484) over rhs (solver.hpp:295) with
+// ops.threads = T (parallel_for, parallel.hpp:14).  A bench "step" is one
+// LSRK45 step (5 RHS stages).  Prints one JSON line.
+//
+//   swedg_refbench N K1D warmup steps threads [warp]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <thread>
+
+#include "swedg/run.hpp"
+#include "swedg/solver.hpp"
+
+using namespace swedg;
+
+int main(int argc, char** argv) {
+    if (argc < 6) {
+        std::fprintf(stderr, "usage: swedg_refbench N K1D warmup steps threads [warp]\n");
+        return 2;
+    }
+    int N = std::atoi(argv[1]), n = std::atoi(argv[2]), warm = std::atoi(argv[3]),
+        steps = std::atoi(argv[4]), threads = std::atoi(argv[5]);
+    double warp = argc > 6 ? std::atof(argv[6]) : 0.1;
+    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+    auto t0 = std::chrono::steady_clock::now();
+    RefOperators ref = build_ref_operators(N);
+    Mesh mesh = uniform_tri_mesh(n, n, {0, 0, 2, 2});
+    set_mapping_degree(mesh, N);
+    if (warp != 0.0) warp_mesh(mesh, warp);
+    Connectivity conn = connect(mesh, true, true);
+    Geometry geo = build_geometry(mesh, ref);
+    FaceMatch fm = match_faces(mesh, conn, geo, ref);
+    SolverOps ops = precompute_element_ops(ref, mesh, geo, conn, fm, 9.81, Penalty::LaxFriedrichs, threads);
+    std::mt19937 rng(23);
+    std::uniform_real_distribution<double> amp(-0.1, 0.1);
+    double a1 = amp(rng), a2 = amp(rng), a3 = amp(rng);
+    ExactFn fn = [=](double x, double y, double) -> ConsState {
+        double h = 1.5 + a1 * std::sin(M_PI * x) * std::cos(M_PI * y);
+        double u = a2 * std::cos(M_PI * x);
+        double v = a3 * std::sin(M_PI * y);
+        return {h, h * u, h * v};
+    };
+    State st = make_state(mesh, N, fn, lake_bathymetry);
+    set_bathymetry(ops, st.b);
+    double setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double dt = compute_dt(mesh, N, 0.125);
+    std::vector<Mat> res;
+    auto rhs_fn = [&](const State& s) { return rhs(ops, s); };
+    for (int i = 0; i < warm; ++i) step_lsrk45(st, rhs_fn, dt, res);
+    auto t1 = std::chrono::steady_clock::now();
+    for (int i = 0; i < steps; ++i) step_lsrk45(st, rhs_fn, dt, res);
+    double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    long K = mesh.num_elements();
+    double dof = (double)K * ref.Np * 3;
+    double gdofs = steps > 0 ? dof * 5.0 * steps / sec / 1e9 : 0.0;
+    std::printf("{\"value\": %.6g, \"unit\": \"GDOF*stages/s\", \"ms_per_step\": %.6g, \"K\": %ld, \"N\": %d, "
+                "\"K1D\": %d, \"threads\": %d, \"steps\": %d, \"warmup\": %d, \"setup_s\": %.3f, \"dt\": %.17g}\n",
+                gdofs, steps > 0 ? sec * 1e3 / steps : 0.0, K, N, n, threads, steps, warm, setup_s, dt);
+    return 0;
+}

@@ -103,6 +103,9 @@ def lib() -> C.CDLL:
     L.swedg_device_bytes.argtypes = [vp]
     L.swedg_device_bytes.restype = C.c_size_t
     L.swedg_debug_bathymetry.argtypes = [vp, _dp, _dp]
+    L.swedg_enable_timers.argtypes = [vp, C.c_int]
+    L.swedg_read_timers.argtypes = [vp, _dp, C.POINTER(C.c_longlong), C.c_int]
+    L.swedg_probe_fp64_peak.argtypes = [C.c_int, C.c_int, _dp]
     _lib = L
     return L
 
@@ -113,6 +116,7 @@ EXPORTED = [
     "swedg_set_state", "swedg_get_state", "swedg_step_lsrk45", "swedg_state_device_ptr",
     "swedg_rhs_device", "swedg_check", "swedg_last_error", "swedg_create_error",
     "swedg_launch_count", "swedg_device_bytes", "swedg_abi_version", "swedg_debug_bathymetry",
+    "swedg_enable_timers", "swedg_read_timers", "swedg_probe_fp64_peak",
 ]
 
 
@@ -260,13 +264,22 @@ class Handle:
         r = None if res is None else _f64(res)
         self._check(self._lib.swedg_set_state(self._h, _p(u), _p(r), float(t)))
 
-    def get_state(self):
+    def get_state(self, u_out=None, with_res: bool = True):
         s = self.sizes
-        u = np.zeros((s.K, 3, self.nstate))
-        r = np.zeros_like(u)
+        u = np.zeros((s.K, 3, self.nstate)) if u_out is None else u_out
+        r = np.zeros_like(u) if with_res else None
         t = C.c_double()
         self._check(self._lib.swedg_get_state(self._h, _p(u), _p(r), C.byref(t)))
         return u, r, t.value
+
+    def enable_timers(self, on: bool = True):
+        self._check(self._lib.swedg_enable_timers(self._h, 1 if on else 0))
+
+    def read_timers(self):
+        ms = np.zeros(2)
+        n = (C.c_longlong * 2)()
+        self._check(self._lib.swedg_read_timers(self._h, _p(ms), n, 2))
+        return ms, [int(n[0]), int(n[1])]
 
     def step(self, dt: float, nsteps: int = 1, sync: bool = True):
         self._check(self._lib.swedg_step_lsrk45(self._h, float(dt), int(nsteps), 1 if sync else 0))
@@ -290,6 +303,15 @@ class Handle:
     @property
     def device_bytes(self) -> int:
         return int(self._lib.swedg_device_bytes(self._h))
+
+
+def probe_fp64_peak(device: int = 0, reps: int = 5) -> float:
+    """Measured DFMA throughput of the device, TFLOP/s (FMA = 2 flops)."""
+    t = C.c_double()
+    rc = lib().swedg_probe_fp64_peak(device, reps, C.byref(t))
+    if rc != SWEDG_OK:
+        raise SwedgError(rc, "fp64 peak probe failed")
+    return t.value
 
 
 def _err_class(rc: int):

@@ -68,6 +68,12 @@ struct swedg_handle_s {
     long last_elem = -1;
     double last_t = 0.0;
     std::string last_msg;
+    // per-kernel-class event timers
+    bool timers = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+    double timer_ms[2] = {0.0, 0.0};
+    long long timer_n[2] = {0, 0};
     // stage bookkeeping for error decoding (current call)
     unsigned call_stage0 = 0;
     std::vector<double> call_stage_t;
@@ -113,6 +119,49 @@ int upload(swedg_handle h, T* dst, const T* src, size_t n) {
         return fail(h, SWEDG_ERR_CUDA, std::string("upload: ") + cudaGetErrorString(e));
     return SWEDG_OK;
 }
+
+// ---- per-kernel event timers ------------------------------------------------
+cudaEvent_t take_event(swedg_handle h) {
+    if (!h->ev_pool.empty()) {
+        cudaEvent_t e = h->ev_pool.back();
+        h->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct KTimer {
+    swedg_handle h;
+    int cls;
+    cudaEvent_t a = nullptr;
+    KTimer(swedg_handle h_, int c) : h(h_), cls(c) {
+        if (h->timers) {
+            a = take_event(h);
+            cudaEventRecord(a, h->stream);
+        }
+    }
+    ~KTimer() {
+        if (a) {
+            cudaEvent_t b = take_event(h);
+            cudaEventRecord(b, h->stream);
+            h->ev_pending.push_back({cls, {a, b}});
+            if (h->ev_pending.size() > 4096) {  // bound the pending list
+                cudaEventSynchronize(b);
+                for (auto& p : h->ev_pending) {
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+                    h->timer_ms[p.first] += ms;
+                    h->timer_n[p.first] += 1;
+                    h->ev_pool.push_back(p.second.first);
+                    h->ev_pool.push_back(p.second.second);
+                }
+                h->ev_pending.clear();
+            }
+        }
+    }
+};
 
 // ---- kernel dispatch -------------------------------------------------------
 
@@ -174,10 +223,13 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         kern<<<grid, VC::T, smem, h->stream>>>(vp);
         return SWEDG_OK;
     };
-    if (h->mode == SWEDG_MODE_PARITY)
-        launch_vol(modal_volume_kernel<N, true>);
-    else
-        launch_vol(modal_volume_kernel<N, false>);
+    {
+        KTimer kt(h, 0);
+        if (h->mode == SWEDG_MODE_PARITY)
+            launch_vol(modal_volume_kernel<N, true>);
+        else
+            launch_vol(modal_volume_kernel<N, false>);
+    }
     h->launches++;
 
     ModalSurfParams sp;
@@ -205,10 +257,13 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     sp.early_exit = sa.early_exit ? 1 : 0;
     using SC = SurfCfg<N>;
     const int grid = (h->K + SC::E - 1) / SC::E;
-    if (h->mode == SWEDG_MODE_PARITY)
-        modal_surface_kernel<N, true><<<grid, SC::T, 0, h->stream>>>(sp);
-    else
-        modal_surface_kernel<N, false><<<grid, SC::T, 0, h->stream>>>(sp);
+    {
+        KTimer kt(h, 1);
+        if (h->mode == SWEDG_MODE_PARITY)
+            modal_surface_kernel<N, true><<<grid, SC::T, 0, h->stream>>>(sp);
+        else
+            modal_surface_kernel<N, false><<<grid, SC::T, 0, h->stream>>>(sp);
+    }
     h->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
@@ -248,10 +303,13 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
         kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, C::T, smem);
         kern<<<grid, C::T, smem, h->stream>>>(sp);
     };
-    if (h->mode == SWEDG_MODE_PARITY)
-        go(sbp_rhs_kernel<N, true>);
-    else
-        go(sbp_rhs_kernel<N, false>);
+    {
+        KTimer kt(h, 0);
+        if (h->mode == SWEDG_MODE_PARITY)
+            go(sbp_rhs_kernel<N, true>);
+        else
+            go(sbp_rhs_kernel<N, false>);
+    }
     h->launches++;
     if (sa.rk) {
         // the SBP RHS reads neighbour states: the RK update runs after all du are known
@@ -267,10 +325,13 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
         up.early_exit = sa.early_exit ? 1 : 0;
         const int tb = 256;
         const int gr = (int)std::min<size_t>((up.n + tb - 1) / tb, (size_t)h->nsm * 16);
-        if (h->mode == SWEDG_MODE_PARITY)
-            sbp_update_kernel<true><<<gr, tb, 0, h->stream>>>(up);
-        else
-            sbp_update_kernel<false><<<gr, tb, 0, h->stream>>>(up);
+        {
+            KTimer kt(h, 1);
+            if (h->mode == SWEDG_MODE_PARITY)
+                sbp_update_kernel<true><<<gr, tb, 0, h->stream>>>(up);
+            else
+                sbp_update_kernel<false><<<gr, tb, 0, h->stream>>>(up);
+        }
         h->launches++;
     }
     cudaError_t e = cudaGetLastError();
@@ -526,8 +587,90 @@ int swedg_destroy(swedg_handle h) {
                     h->res, h->utmp, h->du, h->proj, h->trace, h->accf, h->T1, h->err};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (auto& p : h->ev_pending) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
+    return SWEDG_OK;
+}
+
+int swedg_enable_timers(swedg_handle h, int on) {
+    if (!h) return SWEDG_ERR_INVALID;
+    h->timers = on != 0;
+    return SWEDG_OK;
+}
+
+int swedg_read_timers(swedg_handle h, double* ms, long long* launches, int nclass) {
+    if (!h) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    for (auto& p : h->ev_pending) {
+        float m = 0.f;
+        cudaEventElapsedTime(&m, p.second.first, p.second.second);
+        h->timer_ms[p.first] += m;
+        h->timer_n[p.first] += 1;
+        h->ev_pool.push_back(p.second.first);
+        h->ev_pool.push_back(p.second.second);
+    }
+    h->ev_pending.clear();
+    for (int c = 0; c < nclass && c < 2; ++c) {
+        if (ms) ms[c] = h->timer_ms[c];
+        if (launches) launches[c] = h->timer_n[c];
+        h->timer_ms[c] = 0.0;
+        h->timer_n[c] = 0;
+    }
+    return SWEDG_OK;
+}
+
+namespace {
+__global__ void fp64_peak_kernel(double* out, int iters, double s) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double m = 0.999999999, c = s;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0 = __fma_rn(a0, m, c); a1 = __fma_rn(a1, m, c); a2 = __fma_rn(a2, m, c); a3 = __fma_rn(a3, m, c);
+            a4 = __fma_rn(a4, m, c); a5 = __fma_rn(a5, m, c); a6 = __fma_rn(a6, m, c); a7 = __fma_rn(a7, m, c);
+        }
+    }
+    double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == 12345.678) out[0] = r;  // keep the chain live
+}
+}  // namespace
+
+int swedg_probe_fp64_peak(int device, int reps, double* tflops) {
+    if (!tflops) return SWEDG_ERR_INVALID;
+    if (cudaSetDevice(device) != cudaSuccess) return SWEDG_ERR_CUDA;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    double* d = nullptr;
+    cudaMalloc(&d, 8);
+    const int threads = 256, blocks = nsm * 8, iters = 4096;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    fp64_peak_kernel<<<blocks, threads>>>(d, 64, 1e-12);
+    double best = 0.0;
+    for (int r = 0; r < (reps > 0 ? reps : 5); ++r) {
+        cudaEventRecord(a);
+        fp64_peak_kernel<<<blocks, threads>>>(d, iters, 1e-12);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        double fl = 2.0 * 64.0 * iters * (double)threads * blocks;
+        if (ms > 0) best = std::max(best, fl / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return SWEDG_ERR_CUDA;
+    *tflops = best;
     return SWEDG_OK;
 }
 
