@@ -311,12 +311,17 @@ def run_ours(args, rank, world, local):
     vol_tflops = fb["vol_flops"] * K / (vol_avg_ms * 1e-3) / 1e12
     surf_gbs = fb["surf_bytes"] * K / (surf_avg_ms * 1e-3) / 1e9
     traffic = load_traffic()
-    vol_traffic = traffic.get("modal_volume_kernel", {}).get("dram_bytes_per_launch")
-    surf_traffic = traffic.get("modal_surface_kernel", {}).get("dram_bytes_per_launch")
+    def _tr(name):
+        t = traffic.get(name)
+        return None if not t else round(t["dram_bytes_per_element"] * K)
+
+    vol_traffic = _tr("modal_volume_kernel")
+    surf_traffic = _tr("modal_surface_kernel")
     roofline = {
         "kernel": "modal_volume_kernel<4,fast> (entropy projection + flux differencing + volume lift)",
         "bound": "fp64", "achieved": round(vol_tflops, 4), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
         "frac": round(vol_tflops / fp64_peak, 4), "traffic": vol_traffic,
+        "traffic_note": "ncu --set full dram__bytes_read+write per element (profiles/ncu_traffic.json) x K",
         "peak_source": "measured in-run: DFMA chain probe (swedg_probe_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
         "algorithmic_flops_per_launch": fb["vol_flops"] * K, "avg_launch_ms": round(vol_avg_ms, 4),
         "share_of_step": round(kms[0] / ms if ms > 0 else 0.0, 4),

@@ -17,6 +17,7 @@
 
 #include "../../include/swedg_b200.h"
 #include "modal_kernels.cuh"
+#include "modal_fast.cuh"
 #include "sbp_kernels.cuh"
 
 using namespace swedg;
@@ -225,10 +226,16 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     };
     {
         KTimer kt(h, 0);
-        if (h->mode == SWEDG_MODE_PARITY)
+        if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
-        else
-            launch_vol(modal_volume_kernel<N, false>);
+        } else {
+            using FC = VolFastCfg<N>;
+            auto kern = modal_volume_fast_kernel<N>;
+            const size_t fsm = FC::bytes();
+            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, FC::T, fsm);
+            int grid = std::min((h->K + FC::E - 1) / FC::E, occ * h->nsm);
+            kern<<<std::max(grid, 1), FC::T, fsm, h->stream>>>(vp);
+        }
     }
     h->launches++;
 
