@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,6 +19,7 @@
 #include "../../include/swedg_b200.h"
 #include "modal_kernels.cuh"
 #include "modal_fast.cuh"
+#include "modal_warp_n4.cuh"
 #include "sbp_kernels.cuh"
 
 using namespace swedg;
@@ -38,6 +40,7 @@ struct swedg_handle_s {
     double g;
     int device;
     int nsm = 148;
+    int vol_variant = 0;  // FAST volume kernel: 0 = best for N (warp/TMEM at N=4), 1 = two-row, 2 = row
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // device buffers
@@ -228,6 +231,14 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
+        } else if (N == 4 && h->vol_variant == 0) {
+            auto kern = modal_volume_warp_n4_kernel;
+            const size_t wsm = WarpN4::bytes();
+            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, WarpN4::T, wsm);
+            int grid = std::min((h->K + WarpN4::WARPS - 1) / WarpN4::WARPS, occ * h->nsm);
+            kern<<<std::max(grid, 1), WarpN4::T, wsm, h->stream>>>(vp);
+        } else if (h->vol_variant == 2) {
+            launch_vol(modal_volume_kernel<N, false>);
         } else {
             using FC = VolFastCfg<N>;
             auto kern = modal_volume_fast_kernel<N>;
@@ -478,6 +489,10 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->K = d->K;
     h->g = d->g;
     h->device = d->device;
+    if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
+        std::string sv(v);
+        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : 0);
+    }
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
     if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -653,6 +668,7 @@ int swedg_probe_fp64_peak(int device, int reps, double* tflops) {
     if (!tflops) return SWEDG_ERR_INVALID;
     if (cudaSetDevice(device) != cudaSuccess) return SWEDG_ERR_CUDA;
     int nsm = 148;
+    int vol_variant = 0;  // FAST volume kernel: 0 = best for N (warp/TMEM at N=4), 1 = two-row, 2 = row
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double* d = nullptr;
     cudaMalloc(&d, 8);
