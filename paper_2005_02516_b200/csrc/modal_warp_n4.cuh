@@ -35,6 +35,10 @@ struct WarpN4 {
     static constexpr int tA = 0;                // row l, columns j = 0..39      -> 160 cols
     static constexpr int tB = 160;              // row 32+(l&7), 7 column slots   ->  28 cols
     static constexpr int tD = 188;              // 3 pair slots of loop D         ->  12 cols
+    static constexpr int tV = 208;              // V row l (Vq row l, or Vf row l-25) 15 dbl -> 30 cols
+    static constexpr int tV2 = 240;             // lanes < 24: Vf row 7 + l/3             -> 30 cols
+    static constexpr int tP = 272;              // Pq(l&15, i), i in lane half (<= 13)    -> 26 cols
+    static constexpr int tT = 304;              // Vq(i, l&15), i in lane half (<= 13)    -> 26 cols
     static constexpr int tcols = 512;
     // per-warp shared block (doubles)
     static constexpr int oA = 0;                // double2[40] (hu, hv)
@@ -75,6 +79,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, double2 (&q)[4]) {
 #pragma unroll
     for (int p = 0; p < 4; ++p)
         q[p] = make_double2(__hiloint2double(r[4 * p + 1], r[4 * p]), __hiloint2double(r[4 * p + 3], r[4 * p + 2]));
+}
+
+// 32 columns -> 16 doubles
+__device__ __forceinline__ void tmem_ld32d(uint32_t taddr, double (&d)[16]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int p = 0; p < 16; ++p) d[p] = __hiloint2double(r[2 * p + 1], r[2 * p]);
+}
+
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, double a) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__double2loint(a)),
+                 "r"(__double2hiint(a))
+                 : "memory");
 }
 
 __device__ __forceinline__ double2 tmem_ld4(uint32_t taddr) {
@@ -159,6 +186,23 @@ modal_volume_warp_n4_kernel(ModalVolParams prm) {
             const int row = p % 25, j = nq + 12 + p / 25;
             tmem_st4(tbase + W::tD + 4 * s, ok ? QA[row + j * nh] : 0.0, ok ? QB[row + j * nh] : 0.0);
         }
+        const double* gVq = prm.ops + O::Vq;  // 25 x 15
+        const double* gVf = prm.ops + O::Vf;  // 15 x 15
+        const double* gPq = prm.ops + O::Pq;  // 15 x 25
+        for (int m = 0; m < 16; ++m) {
+            const double vrow = m < Np ? (lane < nq ? gVq[lane + m * nq] : gVf[(lane - nq) + m * nf]) : 0.0;
+            tmem_st2(tbase + W::tV + 2 * m, vrow);
+            const double v2 = (m < Np && lane < 24) ? gVf[(7 + lane / 3) + m * nf] : 0.0;
+            tmem_st2(tbase + W::tV2 + 2 * m, v2);
+        }
+        {
+            const int mm = lane & 15, half = lane >> 4, i0 = half ? 13 : 0, cnt = half ? 12 : 13;
+            for (int ii = 0; ii < 16; ++ii) {
+                const bool ok = mm < Np && ii < cnt;
+                tmem_st2(tbase + W::tP + 2 * ii, ok ? gPq[mm + (i0 + ii) * Np] : 0.0);
+                tmem_st2(tbase + W::tT + 2 * ii, ok ? gVq[(i0 + ii) + mm * nq] : 0.0);
+            }
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -200,35 +244,40 @@ modal_volume_warp_n4_kernel(ModalVolParams prm) {
         __syncwarp();
         prefetch(k + nwarps);
 
-        // ---- entropy variables at the 25 volume points (lanes 0..24)
-        if (lane < nq) {
-            double uq0 = 0.0, uq1 = 0.0, uq2 = 0.0;
+        // ---- entropy variables at the 25 volume points (lanes 0..24); V row from TMEM
+        const double ig = 1.0 / g;
+        {
+            double Vr[16];
+            tmem_ld32d(tbase + W::tV, Vr);
+            if (lane < nq) {
+                double uq0 = 0.0, uq1 = 0.0, uq2 = 0.0;
 #pragma unroll
-            for (int m = 0; m < Np; ++m) {
-                const double v = sVq[lane + m * nq];
-                uq0 = __fma_rn(v, el[W::oU + m], uq0);
-                uq1 = __fma_rn(v, el[W::oU + Np + m], uq1);
-                uq2 = __fma_rn(v, el[W::oU + 2 * Np + m], uq2);
+                for (int m = 0; m < Np; ++m) {
+                    uq0 = __fma_rn(Vr[m], el[W::oU + m], uq0);
+                    uq1 = __fma_rn(Vr[m], el[W::oU + Np + m], uq1);
+                    uq2 = __fma_rn(Vr[m], el[W::oU + 2 * Np + m], uq2);
+                }
+                if (!(uq0 > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                const double inv = 1.0 / uq0;
+                const double vx = uq1 * inv, vy = uq2 * inv;
+                el[W::oV + lane] = g * (uq0 + el[W::oBs + lane]) - 0.5 * (vx * vx + vy * vy);
+                el[W::oV + nq + lane] = vx;
+                el[W::oV + 2 * nq + lane] = vy;
             }
-            if (!(uq0 > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
-            const double vx = uq1 / uq0, vy = uq2 / uq0;
-            el[W::oV + lane] = g * (uq0 + el[W::oBs + lane]) - 0.5 * (vx * vx + vy * vy);
-            el[W::oV + nq + lane] = vx;
-            el[W::oV + 2 * nq + lane] = vy;
         }
         __syncwarp();
-        // ---- vh = Pq v: lanes m and m+16 each take half of the 25-term dots
+        // ---- vh = Pq v: lanes m and m+16 each take half of the 25-term dots (Pq from TMEM)
         {
-            const int m = lane & 15, half = lane >> 4;
-            const int i0 = half ? 13 : 0, i1 = half ? nq : 13;
+            double Pr[16];
+            tmem_ld32d(tbase + W::tP, Pr);
+            const int half = lane >> 4, i0 = half ? 13 : 0;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-            if (m < Np) {
-                for (int i = i0; i < i1; ++i) {
-                    const double p = sPq[m + i * Np];
-                    s0 = __fma_rn(p, el[W::oV + i], s0);
-                    s1 = __fma_rn(p, el[W::oV + nq + i], s1);
-                    s2 = __fma_rn(p, el[W::oV + 2 * nq + i], s2);
-                }
+#pragma unroll
+            for (int ii = 0; ii < 13; ++ii) {
+                const int i = min(i0 + ii, nq - 1);  // padded operator entries are zero
+                s0 = __fma_rn(Pr[ii], el[W::oV + i], s0);
+                s1 = __fma_rn(Pr[ii], el[W::oV + nq + i], s1);
+                s2 = __fma_rn(Pr[ii], el[W::oV + 2 * nq + i], s2);
             }
             s0 += __shfl_down_sync(0xffffffffu, s0, 16);
             s1 += __shfl_down_sync(0xffffffffu, s1, 16);
@@ -240,44 +289,62 @@ modal_volume_warp_n4_kernel(ModalVolParams prm) {
             }
         }
         __syncwarp();
-        // ---- u tilde at rows l (all lanes) and 32+l (lanes 0..7)
+        // ---- u tilde: row l on every lane; rows 32..39 as 24 (row, component) dots
         double hi, Ui, Vi, ui, vi;
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const int row = w == 0 ? lane : 32 + lane;
-            if (w == 1 && lane >= 8) break;
+        {
+            double Vr[16];
+            tmem_ld32d(tbase + W::tV, Vr);
             double vt0 = 0.0, vt1 = 0.0, vt2 = 0.0;
 #pragma unroll
             for (int m = 0; m < Np; ++m) {
-                const double v = row < nq ? sVq[row + m * nq] : sVf[(row - nq) + m * nf];
-                vt0 = __fma_rn(v, el[W::oVh + m], vt0);
-                vt1 = __fma_rn(v, el[W::oVh + Np + m], vt1);
-                vt2 = __fma_rn(v, el[W::oVh + 2 * Np + m], vt2);
+                vt0 = __fma_rn(Vr[m], el[W::oVh + m], vt0);
+                vt1 = __fma_rn(Vr[m], el[W::oVh + Np + m], vt1);
+                vt2 = __fma_rn(Vr[m], el[W::oVh + 2 * Np + m], vt2);
             }
-            const double h = (vt0 + 0.5 * (vt1 * vt1 + vt2 * vt2)) / g - el[W::oBs + row];
-            if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
-            const double U = h * vt1, V = h * vt2, u = U / h, v = V / h;
-            reinterpret_cast<double2*>(el + W::oA)[row] = make_double2(U, V);
-            reinterpret_cast<double2*>(el + W::oB)[row] = make_double2(u, v);
-            el[W::oH + row] = h;
-            if (row >= nq) {
-                double* tr = prm.trace + (size_t)k * 3 * nf + (row - nq);
-                tr[0] = h;
-                tr[nf] = U;
-                tr[2 * nf] = V;
+            double V2[16];
+            tmem_ld32d(tbase + W::tV2, V2);
+            const int c2 = lane % 3;
+            double s2 = 0.0;
+#pragma unroll
+            for (int m = 0; m < Np; ++m) s2 = __fma_rn(V2[m], el[W::oVh + c2 * Np + m], s2);
+            double* buf = el + W::oP;  // scratch (loop-D partials come later)
+            if (lane < 24) buf[lane] = s2;
+            hi = (vt0 + 0.5 * (vt1 * vt1 + vt2 * vt2)) * ig - el[W::oBs + lane];
+            Ui = hi * vt1;
+            Vi = hi * vt2;
+            ui = vt1;  // u = hu/h with hu = h v2 (FAST: no division)
+            vi = vt2;
+            __syncwarp();
+            double hB = 1.0, UB = 0.0, VB = 0.0, uB = 0.0, vB = 0.0;
+            if (lane < 8) {
+                const double w0 = buf[3 * lane], w1 = buf[3 * lane + 1], w2 = buf[3 * lane + 2];
+                hB = (w0 + 0.5 * (w1 * w1 + w2 * w2)) * ig - el[W::oBs + 32 + lane];
+                UB = hB * w1;
+                VB = hB * w2;
+                uB = w1;
+                vB = w2;
             }
-            if (prm.proj) {
-                double* pj = prm.proj + (size_t)k * 3 * nh + row;
-                pj[0] = h;
-                pj[nh] = U;
-                pj[2 * nh] = V;
-            }
-            if (w == 0) {
-                hi = h;
-                Ui = U;
-                Vi = V;
-                ui = u;
-                vi = v;
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+                if (w == 1 && lane >= 8) break;
+                const int row = w == 0 ? lane : 32 + lane;
+                const double h = w == 0 ? hi : hB, U = w == 0 ? Ui : UB, V = w == 0 ? Vi : VB;
+                if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                reinterpret_cast<double2*>(el + W::oA)[row] = make_double2(U, V);
+                reinterpret_cast<double2*>(el + W::oB)[row] = w == 0 ? make_double2(ui, vi) : make_double2(uB, vB);
+                el[W::oH + row] = h;
+                if (row >= nq) {
+                    double* tr = prm.trace + (size_t)k * 3 * nf + (row - nq);
+                    tr[0] = h;
+                    tr[nf] = U;
+                    tr[2 * nf] = V;
+                }
+                if (prm.proj) {
+                    double* pj = prm.proj + (size_t)k * 3 * nh + row;
+                    pj[0] = h;
+                    pj[nh] = U;
+                    pj[2 * nh] = V;
+                }
             }
         }
         __syncwarp();
@@ -399,16 +466,16 @@ modal_volume_warp_n4_kernel(ModalVolParams prm) {
         }
         __syncwarp();
         {
-            const int m = lane & 15, half = lane >> 4;
-            const int i0 = half ? 13 : 0, i1 = half ? nq : 13;
+            double Tr[16];
+            tmem_ld32d(tbase + W::tT, Tr);
+            const int half = lane >> 4, i0 = half ? 13 : 0;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-            if (m < Np) {
-                for (int i = i0; i < i1; ++i) {
-                    const double v = sVq[i + m * nq];
-                    s0 = __fma_rn(v, st[i], s0);
-                    s1 = __fma_rn(v, st[nq + i], s1);
-                    s2 = __fma_rn(v, st[2 * nq + i], s2);
-                }
+#pragma unroll
+            for (int ii = 0; ii < 13; ++ii) {
+                const int i = min(i0 + ii, nq - 1);
+                s0 = __fma_rn(Tr[ii], st[i], s0);
+                s1 = __fma_rn(Tr[ii], st[nq + i], s1);
+                s2 = __fma_rn(Tr[ii], st[2 * nq + i], s2);
             }
             s0 += __shfl_down_sync(0xffffffffu, s0, 16);
             s1 += __shfl_down_sync(0xffffffffu, s1, 16);
