@@ -35,6 +35,22 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Internal arithmetic type.  Built twice: real = double (the reference's own
+ * arithmetic, liboracle.so) and real = long double (-DORACLE_LONG_DOUBLE, x87 80-bit, liboracle_ld.so)
+ * — the latter is the accuracy yardstick for the FAST kernels: on
+ * cancellation-dominated states (the dam break at rest) two different FP64
+ * roundings of the same RHS differ by the reference's own rounding error, so
+ * FAST is required to be no less accurate than the reference there. */
+#ifdef ORACLE_LONG_DOUBLE
+typedef long double real;
+#define FABS(x) fabsl(x)
+#define SQRT(x) sqrtl(x)
+#else
+typedef double real;
+#define FABS(x) fabs(x)
+#define SQRT(x) sqrt(x)
+#endif
+
 #define ORACLE_OK 0
 #define ORACLE_ERR_POSITIVITY 1
 #define ORACLE_ERR_NONFINITE 2
@@ -59,13 +75,13 @@ typedef struct {
 
 /* ---- pointwise physics (swe.hpp) --------------------------------------- */
 
-static void ec_flux_xy(const double *a, const double *b, double g, double *fx, double *fy) {
-    double uxa = a[1] / a[0], uya = a[2] / a[0];
-    double uxb = b[1] / b[0], uyb = b[2] / b[0];
-    double h_avg = 0.5 * (a[0] + b[0]);
-    double p = g * h_avg * h_avg - 0.25 * g * (a[0] * a[0] + b[0] * b[0]);
-    double ux = 0.5 * (uxa + uxb), uy = 0.5 * (uya + uyb);
-    double hu = 0.5 * (a[1] + b[1]), hv = 0.5 * (a[2] + b[2]);
+static void ec_flux_xy(const real *a, const real *b, real g, real *fx, real *fy) {
+    real uxa = a[1] / a[0], uya = a[2] / a[0];
+    real uxb = b[1] / b[0], uyb = b[2] / b[0];
+    real h_avg = 0.5 * (a[0] + b[0]);
+    real p = g * h_avg * h_avg - 0.25 * g * (a[0] * a[0] + b[0] * b[0]);
+    real ux = 0.5 * (uxa + uxb), uy = 0.5 * (uya + uyb);
+    real hu = 0.5 * (a[1] + b[1]), hv = 0.5 * (a[2] + b[2]);
     fx[0] = hu;
     fx[1] = hu * ux + p;
     fx[2] = hu * uy;
@@ -74,9 +90,9 @@ static void ec_flux_xy(const double *a, const double *b, double g, double *fx, d
     fy[2] = hv * uy + p;
 }
 
-static void phys_flux(const double *u, double g, int dir, double *f) {
-    double vx = u[1] / u[0], vy = u[2] / u[0];
-    double p = 0.5 * g * u[0] * u[0];
+static void phys_flux(const real *u, real g, int dir, real *f) {
+    real vx = u[1] / u[0], vy = u[2] / u[0];
+    real p = 0.5 * g * u[0] * u[0];
     if (dir == 0) {
         f[0] = u[1];
         f[1] = u[1] * vx + p;
@@ -88,35 +104,35 @@ static void phys_flux(const double *u, double g, int dir, double *f) {
     }
 }
 
-static double wave_speed(const double *u, double g, double nx, double ny) {
-    double un = (u[1] * nx + u[2] * ny) / u[0];
-    return fabs(un) + sqrt(g * u[0]);
+static real wave_speed(const real *u, real g, real nx, real ny) {
+    real un = (u[1] * nx + u[2] * ny) / u[0];
+    return FABS(un) + SQRT(g * u[0]);
 }
 
-static void lf_penalty(const double *uL, const double *uR, double g, double nx, double ny,
-                       double *pen) {
-    double a = wave_speed(uL, g, nx, ny), b = wave_speed(uR, g, nx, ny);
-    double lam = (a < b) ? b : a; /* std::max */
+static void lf_penalty(const real *uL, const real *uR, real g, real nx, real ny,
+                       real *pen) {
+    real a = wave_speed(uL, g, nx, ny), b = wave_speed(uR, g, nx, ny);
+    real lam = (a < b) ? b : a; /* std::max */
     pen[0] = 0.5 * lam * (uR[0] - uL[0]);
     pen[1] = 0.5 * lam * (uR[1] - uL[1]);
     pen[2] = 0.5 * lam * (uR[2] - uL[2]);
 }
 
-static void wall_ghost(const double *u, double nx, double ny, double *out) {
-    double un = u[1] * nx + u[2] * ny;
+static void wall_ghost(const real *u, real nx, real ny, real *out) {
+    real un = u[1] * nx + u[2] * ny;
     out[0] = u[0];
     out[1] = u[1] - 2.0 * un * nx;
     out[2] = u[2] - 2.0 * un * ny;
 }
 
 /* physical split-form operator entry, solver.hpp:74-80 (Eigen coefficient order) */
-static double split_entry(const double *Qr, const double *Qs, int ld, const double *g1,
+static real split_entry(const double *Qr, const double *Qs, int ld, const double *g1,
                           const double *g2, int i, int j) {
-    double qr = Qr[i + (size_t)j * ld], qs = Qs[i + (size_t)j * ld];
+    real qr = Qr[i + (size_t)j * ld], qs = Qs[i + (size_t)j * ld];
     return 0.5 * (g1[i] * qr + qr * g1[j] + g2[i] * qs + qs * g2[j]);
 }
 /* skew part Qh - Qh^T, solver.hpp:107-108 */
-static double skew_entry(const double *Qr, const double *Qs, int ld, const double *g1,
+static real skew_entry(const double *Qr, const double *Qs, int ld, const double *g1,
                          const double *g2, int i, int j) {
     return split_entry(Qr, Qs, ld, g1, g2, i, j) - split_entry(Qr, Qs, ld, g1, g2, j, i);
 }
@@ -132,7 +148,7 @@ void oracle_set_bathymetry(const oracle_ops *op, const double *b, double *b_stac
             const double *gf = op->gf + (size_t)k * 4 * nrow;
             const double *bk = b + (size_t)k * nq;
             for (int i = 0; i < nq; ++i) {
-                double sx = 0.0, sy = 0.0;
+                real sx = 0.0, sy = 0.0;
                 for (int j = 0; j < nq; ++j) {
                     sx += split_entry(op->Qr, op->Qs, nq, gf, gf + nrow, i, j) * bk[j];
                     sy += split_entry(op->Qr, op->Qs, nq, gf + 2 * nrow, gf + 3 * nrow, i, j) * bk[j];
@@ -149,18 +165,18 @@ void oracle_set_bathymetry(const oracle_ops *op, const double *b, double *b_stac
         const double *bk = b + (size_t)k * Np;
         double *bs = b_stacked + (size_t)k * nh;
         for (int i = 0; i < nq; ++i) {
-            double s = 0.0;
+            real s = 0.0;
             for (int m = 0; m < Np; ++m) s += op->Vq[i + (size_t)m * nq] * bk[m];
             bs[i] = s;
         }
         for (int i = 0; i < nf; ++i) {
-            double s = 0.0;
+            real s = 0.0;
             for (int m = 0; m < Np; ++m) s += op->Vf[i + (size_t)m * nf] * bk[m];
             bs[nq + i] = s;
         }
         const double *gf = op->gf + (size_t)k * 4 * nh;
         for (int i = 0; i < nh; ++i) {
-            double sx = 0.0, sy = 0.0;
+            real sx = 0.0, sy = 0.0;
             for (int j = 0; j < nh; ++j) {
                 sx += skew_entry(op->Qr, op->Qs, nh, gf, gf + nh, i, j) * bs[j];
                 sy += skew_entry(op->Qr, op->Qs, nh, gf + 2 * nh, gf + 3 * nh, i, j) * bs[j];
@@ -169,8 +185,8 @@ void oracle_set_bathymetry(const oracle_ops *op, const double *b, double *b_stac
             src_y[(size_t)k * nh + i] = 0.5 * sy;
         }
         for (int i = 0; i < nf; ++i) {
-            double m = op->wf[i] * op->sJ[(size_t)k * nf + i];
-            double Bx = m * op->nx[(size_t)k * nf + i], By = m * op->ny[(size_t)k * nf + i];
+            real m = op->wf[i] * op->sJ[(size_t)k * nf + i];
+            real Bx = m * op->nx[(size_t)k * nf + i], By = m * op->ny[(size_t)k * nf + i];
             src_x[(size_t)k * nh + nq + i] += 0.5 * (Bx * bs[nq + i]);
             src_y[(size_t)k * nh + nq + i] += 0.5 * (By * bs[nq + i]);
         }
@@ -180,42 +196,42 @@ void oracle_set_bathymetry(const oracle_ops *op, const double *b, double *b_stac
 /* ---- entropy projection (solver.hpp:145-183) ----------------------------- */
 
 /* returns 0 or ORACLE_ERR_POSITIVITY; proj_k is [3][nh] */
-static int project_element(const oracle_ops *op, int k, const double *u, double *proj_k) {
+static int project_element(const oracle_ops *op, int k, const double *u, real *proj_k) {
     int Np = op->Np, nq = op->nq, nf = op->nf, nh = nq + nf;
     const double *uk = u + (size_t)k * 3 * Np;
     const double *bs = op->b_stacked + (size_t)k * nh;
-    double g = op->g;
-    double vq[3 * 64], vh[3 * 64];
+    real g = op->g;
+    real vq[3 * 64], vh[3 * 64];
     for (int i = 0; i < nq; ++i) {
-        double uq[3];
+        real uq[3];
         for (int c = 0; c < 3; ++c) {
-            double s = 0.0;
+            real s = 0.0;
             for (int m = 0; m < Np; ++m) s += op->Vq[i + (size_t)m * nq] * uk[c * Np + m];
             uq[c] = s;
         }
         if (!(uq[0] > 0.0)) return ORACLE_ERR_POSITIVITY;
-        double vx = uq[1] / uq[0], vy = uq[2] / uq[0];
+        real vx = uq[1] / uq[0], vy = uq[2] / uq[0];
         vq[0 * nq + i] = g * (uq[0] + bs[i]) - 0.5 * (vx * vx + vy * vy);
         vq[1 * nq + i] = vx;
         vq[2 * nq + i] = vy;
     }
     for (int m = 0; m < Np; ++m)
         for (int c = 0; c < 3; ++c) {
-            double s = 0.0;
+            real s = 0.0;
             for (int i = 0; i < nq; ++i) s += op->Pq[m + (size_t)i * Np] * vq[c * nq + i];
             vh[c * Np + m] = s;
         }
     for (int i = 0; i < nh; ++i) {
-        double vt[3];
+        real vt[3];
         for (int c = 0; c < 3; ++c) {
-            double s = 0.0;
+            real s = 0.0;
             if (i < nq)
                 for (int m = 0; m < Np; ++m) s += op->Vq[i + (size_t)m * nq] * vh[c * Np + m];
             else
                 for (int m = 0; m < Np; ++m) s += op->Vf[(i - nq) + (size_t)m * nf] * vh[c * Np + m];
             vt[c] = s;
         }
-        double h = (vt[0] + 0.5 * (vt[1] * vt[1] + vt[2] * vt[2])) / g - bs[i];
+        real h = (vt[0] + 0.5 * (vt[1] * vt[1] + vt[2] * vt[2])) / g - bs[i];
         if (!(h > 0.0)) return ORACLE_ERR_POSITIVITY;
         proj_k[0 * nh + i] = h;
         proj_k[1 * nh + i] = h * vt[1];
@@ -225,8 +241,7 @@ static int project_element(const oracle_ops *op, int k, const double *u, double 
 }
 
 /* proj: [K][3][nh].  Returns 0 or error code; *bad_elem = first failing element. */
-int oracle_entropy_projection(const oracle_ops *op, const double *u, double *proj,
-                              int *bad_elem) {
+static int entropy_projection_real(const oracle_ops *op, const double *u, real *proj, int *bad_elem) {
     int nh = op->nq + op->nf;
     for (int k = 0; k < op->K; ++k) {
         int e = project_element(op, k, u, proj + (size_t)k * 3 * nh);
@@ -238,28 +253,38 @@ int oracle_entropy_projection(const oracle_ops *op, const double *u, double *pro
     return ORACLE_OK;
 }
 
+int oracle_entropy_projection(const oracle_ops *op, const double *u, double *proj,
+                              int *bad_elem) {
+    size_t n = (size_t)op->K * 3 * (op->nq + op->nf);
+    real *p = (real *)malloc(sizeof(real) * n);
+    int e = entropy_projection_real(op, u, p, bad_elem);
+    for (size_t i = 0; i < n; ++i) proj[i] = (double)p[i];
+    free(p);
+    return e;
+}
+
 /* ---- modal RHS (solver.hpp:237-293) --------------------------------------
  * elems: optional subset (n_elems entries) — du is written only for those
  * elements; proj must hold every element (or at least the subset and its
  * neighbours). */
-int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
-                         const int *elems, int n_elems, int *bad_elem) {
+static int rhs_from_proj_real(const oracle_ops *op, const real *proj, double *du,
+                              const int *elems, int n_elems, int *bad_elem) {
     int Np = op->Np, nq = op->nq, nf = op->nf, nh = nq + nf, npf = op->npf;
-    double g = op->g;
+    real g = op->g;
     int n = elems ? n_elems : op->K;
-    double acc[3 * 128], stacked[3 * 128], modal[3 * 64];
+    real acc[3 * 128], stacked[3 * 128], modal[3 * 64];
     for (int ei = 0; ei < n; ++ei) {
         int k = elems ? elems[ei] : ei;
-        const double *ut = proj + (size_t)k * 3 * nh;
+        const real *ut = proj + (size_t)k * 3 * nh;
         const double *gf = op->gf + (size_t)k * 4 * nh;
-        memset(acc, 0, sizeof(double) * 3 * nh);
-        double fx[3], fy[3], ui[3], uj[3];
+        memset(acc, 0, sizeof(real) * 3 * nh);
+        real fx[3], fy[3], ui[3], uj[3];
         /* skew_volume_kernel pass 1: j < nq, all rows */
         for (int j = 0; j < nq; ++j) {
             uj[0] = ut[j]; uj[1] = ut[nh + j]; uj[2] = ut[2 * nh + j];
             for (int i = 0; i < nh; ++i) {
-                double qx = skew_entry(op->Qr, op->Qs, nh, gf, gf + nh, i, j);
-                double qy = skew_entry(op->Qr, op->Qs, nh, gf + 2 * nh, gf + 3 * nh, i, j);
+                real qx = skew_entry(op->Qr, op->Qs, nh, gf, gf + nh, i, j);
+                real qy = skew_entry(op->Qr, op->Qs, nh, gf + 2 * nh, gf + 3 * nh, i, j);
                 if (qx == 0.0 && qy == 0.0) continue;
                 ui[0] = ut[i]; ui[1] = ut[nh + i]; ui[2] = ut[2 * nh + i];
                 ec_flux_xy(ui, uj, g, fx, fy);
@@ -270,8 +295,8 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
         for (int j = nq; j < nh; ++j) {
             uj[0] = ut[j]; uj[1] = ut[nh + j]; uj[2] = ut[2 * nh + j];
             for (int i = 0; i < nq; ++i) {
-                double qx = skew_entry(op->Qr, op->Qs, nh, gf, gf + nh, i, j);
-                double qy = skew_entry(op->Qr, op->Qs, nh, gf + 2 * nh, gf + 3 * nh, i, j);
+                real qx = skew_entry(op->Qr, op->Qs, nh, gf, gf + nh, i, j);
+                real qy = skew_entry(op->Qr, op->Qs, nh, gf + 2 * nh, gf + 3 * nh, i, j);
                 if (qx == 0.0 && qy == 0.0) continue;
                 ui[0] = ut[i]; ui[1] = ut[nh + i]; ui[2] = ut[2 * nh + i];
                 ec_flux_xy(ui, uj, g, fx, fy);
@@ -283,22 +308,22 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
             int nb = op->nbr[(size_t)k * 3 + f];
             for (int s = 0; s < npf; ++s) {
                 int i = f * npf + s;
-                double nxi = op->nx[(size_t)k * nf + i], nyi = op->ny[(size_t)k * nf + i];
-                double m = op->wf[i] * op->sJ[(size_t)k * nf + i];
-                double Bx = m * nxi, By = m * nyi;
-                double up[3];
+                real nxi = op->nx[(size_t)k * nf + i], nyi = op->ny[(size_t)k * nf + i];
+                real m = op->wf[i] * op->sJ[(size_t)k * nf + i];
+                real Bx = m * nxi, By = m * nyi;
+                real up[3];
                 ui[0] = ut[nq + i]; ui[1] = ut[nh + nq + i]; ui[2] = ut[2 * nh + nq + i];
                 if (nb < 0) {
                     wall_ghost(ui, nxi, nyi, up);
                 } else {
                     int j = op->perm[(size_t)k * nf + i];
-                    const double *un = proj + (size_t)nb * 3 * nh;
+                    const real *un = proj + (size_t)nb * 3 * nh;
                     up[0] = un[nq + j]; up[1] = un[nh + nq + j]; up[2] = un[2 * nh + nq + j];
                 }
                 ec_flux_xy(up, ui, g, fx, fy);
                 for (int c = 0; c < 3; ++c) acc[c * nh + nq + i] += Bx * fx[c] + By * fy[c];
                 if (op->penalty_lf) {
-                    double pen[3];
+                    real pen[3];
                     lf_penalty(ui, up, g, nxi, nyi, pen);
                     for (int c = 0; c < 3; ++c) acc[c * nh + nq + i] -= m * pen[c];
                 }
@@ -307,7 +332,7 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
         /* bathymetry source; stacked = src - acc */
         const double *sx = op->src_x + (size_t)k * nh, *sy = op->src_y + (size_t)k * nh;
         for (int i = 0; i < nh; ++i) {
-            double h = ut[i];
+            real h = ut[i];
             stacked[0 * nh + i] = 0.0 - acc[0 * nh + i];
             stacked[1 * nh + i] = -g * h * sx[i] - acc[1 * nh + i];
             stacked[2 * nh + i] = -g * h * sy[i] - acc[2 * nh + i];
@@ -315,7 +340,7 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
         /* lift: Vq^T top + Vf^T bottom, then Mh_inv */
         for (int m = 0; m < Np; ++m)
             for (int c = 0; c < 3; ++c) {
-                double s1 = 0.0, s2 = 0.0;
+                real s1 = 0.0, s2 = 0.0;
                 for (int i = 0; i < nq; ++i) s1 += op->Vq[i + (size_t)m * nq] * stacked[c * nh + i];
                 for (int i = 0; i < nf; ++i) s2 += op->Vf[i + (size_t)m * nf] * stacked[c * nh + nq + i];
                 modal[c * Np + m] = s1 + s2;
@@ -325,7 +350,7 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
         int finite = 1;
         for (int c = 0; c < 3; ++c)
             for (int i = 0; i < Np; ++i) {
-                double s = 0.0;
+                real s = 0.0;
                 for (int m = 0; m < Np; ++m) s += Mi[i + (size_t)m * Np] * modal[c * Np + m];
                 duk[c * Np + i] = s;
                 if (!isfinite(s)) finite = 0;
@@ -338,11 +363,36 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
     return ORACLE_OK;
 }
 
+int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
+                         const int *elems, int n_elems, int *bad_elem) {
+    size_t n = (size_t)op->K * 3 * (op->nq + op->nf);
+    real *p = (real *)malloc(sizeof(real) * n);
+    for (size_t i = 0; i < n; ++i) p[i] = proj[i];
+    int e = rhs_from_proj_real(op, p, du, elems, n_elems, bad_elem);
+    free(p);
+    return e;
+}
+
+/* projection kept in REAL precision between the two phases */
 int oracle_rhs(const oracle_ops *op, const double *u, double *du, double *proj_scratch,
                int *bad_elem) {
-    int e = oracle_entropy_projection(op, u, proj_scratch, bad_elem);
-    if (e) return e;
-    return oracle_rhs_from_proj(op, proj_scratch, du, NULL, 0, bad_elem);
+    (void)proj_scratch;
+    size_t n = (size_t)op->K * 3 * (op->nq + op->nf);
+    real *p = (real *)malloc(sizeof(real) * n);
+    int e = entropy_projection_real(op, u, p, bad_elem);
+    if (!e) e = rhs_from_proj_real(op, p, du, NULL, 0, bad_elem);
+    free(p);
+    return e;
+}
+
+int oracle_rhs_subset(const oracle_ops *op, const double *u, double *du, const int *elems,
+                      int n_elems, int *bad_elem) {
+    size_t n = (size_t)op->K * 3 * (op->nq + op->nf);
+    real *p = (real *)malloc(sizeof(real) * n);
+    int e = entropy_projection_real(op, u, p, bad_elem);
+    if (!e) e = rhs_from_proj_real(op, p, du, elems, n_elems, bad_elem);
+    free(p);
+    return e;
 }
 
 /* ---- SBP RHS (solver.hpp:369-434) ---------------------------------------- */
@@ -350,9 +400,9 @@ int oracle_rhs(const oracle_ops *op, const double *u, double *du, double *proj_s
 int oracle_rhs_sbp(const oracle_ops *op, const double *u, double *du, const int *elems,
                    int n_elems, int *bad_elem) {
     int nq = op->nq, nf = op->nf, npf = op->npf, nrow = nq + nf;
-    double g = op->g;
+    real g = op->g;
     int n = elems ? n_elems : op->K;
-    double acc[3 * 128];
+    real acc[3 * 128];
     for (int ei = 0; ei < n; ++ei) {
         int k = elems ? elems[ei] : ei;
         const double *uk = u + (size_t)k * 3 * nq;
@@ -362,13 +412,13 @@ int oracle_rhs_sbp(const oracle_ops *op, const double *u, double *du, const int 
                 if (bad_elem) *bad_elem = k;
                 return ORACLE_ERR_POSITIVITY;
             }
-        memset(acc, 0, sizeof(double) * 3 * nq);
-        double fx[3], fy[3], ui[3], uj[3];
+        memset(acc, 0, sizeof(real) * 3 * nq);
+        real fx[3], fy[3], ui[3], uj[3];
         for (int j = 0; j < nq; ++j) {
             uj[0] = uk[j]; uj[1] = uk[nq + j]; uj[2] = uk[2 * nq + j];
             for (int i = 0; i < nq; ++i) {
-                double qx = split_entry(op->Qr, op->Qs, nq, gf, gf + nrow, i, j);
-                double qy = split_entry(op->Qr, op->Qs, nq, gf + 2 * nrow, gf + 3 * nrow, i, j);
+                real qx = split_entry(op->Qr, op->Qs, nq, gf, gf + nrow, i, j);
+                real qy = split_entry(op->Qr, op->Qs, nq, gf + 2 * nrow, gf + 3 * nrow, i, j);
                 if (qx == 0.0 && qy == 0.0) continue;
                 ui[0] = uk[i]; ui[1] = uk[nq + i]; ui[2] = uk[2 * nq + i];
                 ec_flux_xy(ui, uj, g, fx, fy);
@@ -380,10 +430,10 @@ int oracle_rhs_sbp(const oracle_ops *op, const double *u, double *du, const int 
             for (int s = 0; s < npf; ++s) {
                 int i = f * npf + s;
                 int vi = op->face_index[i];
-                double nxi = op->nx[(size_t)k * nf + i], nyi = op->ny[(size_t)k * nf + i];
-                double m = op->wf[i] * op->sJ[(size_t)k * nf + i];
-                double Bx = m * nxi, By = m * nyi;
-                double up[3], fxi[3], fyi[3];
+                real nxi = op->nx[(size_t)k * nf + i], nyi = op->ny[(size_t)k * nf + i];
+                real m = op->wf[i] * op->sJ[(size_t)k * nf + i];
+                real Bx = m * nxi, By = m * nyi;
+                real up[3], fxi[3], fyi[3];
                 ui[0] = uk[vi]; ui[1] = uk[nq + vi]; ui[2] = uk[2 * nq + vi];
                 if (nb < 0) {
                     wall_ghost(ui, nxi, nyi, up);
@@ -398,7 +448,7 @@ int oracle_rhs_sbp(const oracle_ops *op, const double *u, double *du, const int 
                 for (int c = 0; c < 3; ++c)
                     acc[c * nq + vi] += Bx * (fx[c] - fxi[c]) + By * (fy[c] - fyi[c]);
                 if (op->penalty_lf) {
-                    double pen[3];
+                    real pen[3];
                     lf_penalty(ui, up, g, nxi, nyi, pen);
                     for (int c = 0; c < 3; ++c) acc[c * nq + vi] -= m * pen[c];
                 }
@@ -409,11 +459,11 @@ int oracle_rhs_sbp(const oracle_ops *op, const double *u, double *du, const int 
         double *duk = du + (size_t)k * 3 * nq;
         int finite = 1;
         for (int i = 0; i < nq; ++i) {
-            double h = uk[i];
-            double minv = 1.0 / (op->M_diag[i] * J[i]);
-            double r0 = -acc[i];
-            double r1 = -acc[nq + i] - g * h * sx[i];
-            double r2 = -acc[2 * nq + i] - g * h * sy[i];
+            real h = uk[i];
+            real minv = 1.0 / (op->M_diag[i] * J[i]);
+            real r0 = -acc[i];
+            real r1 = -acc[nq + i] - g * h * sx[i];
+            real r2 = -acc[2 * nq + i] - g * h * sy[i];
             duk[i] = minv * r0;
             duk[nq + i] = minv * r1;
             duk[2 * nq + i] = minv * r2;
@@ -429,20 +479,20 @@ int oracle_rhs_sbp(const oracle_ops *op, const double *u, double *du, const int 
 
 /* ---- LSRK45 (solver.hpp:439-484) ------------------------------------------ */
 
-static const double LS_A[5] = {0.0, -0.41789047449985195, -1.192151694642677,
+static const real LS_A[5] = {0.0, -0.41789047449985195, -1.192151694642677,
                                -1.6977846924715279, -1.5141834442571558};
-static const double LS_B[5] = {0.14965902199922912, 0.37921031299962726, 0.8229550293869817,
+static const real LS_B[5] = {0.14965902199922912, 0.37921031299962726, 0.8229550293869817,
                                0.6994504559491221, 0.15305724796815198};
 
 /* n = K*3*(Np or nq) state entries; res must be zero-initialised on the first
  * call (the reference resizes/zeroes it on entry, solver.hpp:470-473). */
-int oracle_step_lsrk45(const oracle_ops *op, double *u, double *res, double dt, int nsteps,
+int oracle_step_lsrk45(const oracle_ops *op, double *u, double *res, real dt, int nsteps,
                        int *bad_elem) {
     int nloc = op->scheme == 1 ? op->nq : op->Np;
     size_t n = (size_t)op->K * 3 * nloc;
     size_t nproj = (size_t)op->K * 3 * (op->nq + op->nf);
-    double *du = (double *)malloc(sizeof(double) * n);
-    double *proj = op->scheme == 1 ? NULL : (double *)malloc(sizeof(double) * nproj);
+    double *du = (double *)malloc(sizeof(real) * n);
+    double *proj = op->scheme == 1 ? NULL : (double *)malloc(sizeof(real) * nproj);
     int err = 0;
     if (!(dt > 0.0)) err = -1;
     for (int st = 0; st < nsteps && !err; ++st)

@@ -13,6 +13,7 @@ import numpy as np
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(REPO, "oracle", "liboracle.so")
+LIB_LD = os.path.join(REPO, "oracle", "liboracle_ld.so")  # same code, long double arithmetic
 GOLDEN = os.path.join(REPO, "tests", "golden")
 
 _dp = C.POINTER(C.c_double)
@@ -30,28 +31,30 @@ class OracleOps(C.Structure):
     ]
 
 
-def _build_lib() -> None:
+def _build_lib(path, extra) -> None:
     src = os.path.join(REPO, "oracle", "swedg_oracle.c")
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(src):
+    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
         subprocess.run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                        "-shared", src, "-o", LIB, "-lm"], check=True)
+                        "-shared"] + extra + [src, "-o", path, "-lm"], check=True)
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        _build_lib()
-        _lib = C.CDLL(LIB)
+def lib(precision: str = "double"):
+    if precision not in _libs:
+        path, extra = (LIB, []) if precision == "double" else (LIB_LD, ["-DORACLE_LONG_DOUBLE"])
+        _build_lib(path, extra)
+        _lib = C.CDLL(path)
         _lib.oracle_set_bathymetry.argtypes = [C.POINTER(OracleOps), _dp, _dp, _dp, _dp]
         _lib.oracle_entropy_projection.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip]
         _lib.oracle_rhs_from_proj.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
         _lib.oracle_rhs.argtypes = [C.POINTER(OracleOps), _dp, _dp, _dp, _ip]
         _lib.oracle_rhs_sbp.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
         _lib.oracle_step_lsrk45.argtypes = [C.POINTER(OracleOps), _dp, _dp, C.c_double, C.c_int, _ip]
-    return _lib
+        _lib.oracle_rhs_subset.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
+        _libs[precision] = _lib
+    return _libs[precision]
 
 
 def _p(a):
@@ -70,7 +73,10 @@ def load_golden(name: str) -> dict:
 class Oracle:
     """The C restatement driven from a case dictionary (golden fixture layout)."""
 
-    def __init__(self, case: dict, penalty_lf: bool = True):
+    def __init__(self, case: dict, penalty_lf: bool = True, precision: str = "double"):
+        """precision "double" = the reference's arithmetic (bitwise); "ld" = the same
+        algorithm in x87 long double (an accuracy yardstick, not a parity target)."""
+        self.L = lib(precision)
         c = {k: np.ascontiguousarray(v) for k, v in case.items()}
         self.c = c
         self.scheme = int(c["scheme"][0])
@@ -129,7 +135,7 @@ class Oracle:
             self.b_stacked = np.zeros((K, self.nh))
             self.src_x = np.zeros((K, self.nh))
             self.src_y = np.zeros((K, self.nh))
-        lib().oracle_set_bathymetry(C.byref(self.op), _p(b), _p(self.b_stacked), _p(self.src_x),
+        self.L.oracle_set_bathymetry(C.byref(self.op), _p(b), _p(self.b_stacked), _p(self.src_x),
                                     _p(self.src_y))
         self.op.b_stacked = _p(self.b_stacked)
         self.op.src_x = _p(self.src_x)
@@ -139,7 +145,7 @@ class Oracle:
         u = np.ascontiguousarray(u, dtype=np.float64)
         proj = np.zeros((self.K, 3, self.nh))
         bad = C.c_int(-1)
-        err = lib().oracle_entropy_projection(C.byref(self.op), _p(u), _p(proj), C.byref(bad))
+        err = self.L.oracle_entropy_projection(C.byref(self.op), _p(u), _p(proj), C.byref(bad))
         return proj, err, bad.value
 
     def rhs(self, u, elems=None):
@@ -148,22 +154,19 @@ class Oracle:
         if self.scheme == 1:
             du = np.zeros((self.K, 3, self.nq))
             ei = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
-            err = lib().oracle_rhs_sbp(C.byref(self.op), _p(u), _p(du), _pi(ei),
+            err = self.L.oracle_rhs_sbp(C.byref(self.op), _p(u), _p(du), _pi(ei),
                                        0 if ei is None else len(ei), C.byref(bad))
             return du, err, bad.value
-        proj, err, b = self.entropy_projection(u)
         du = np.zeros((self.K, 3, self.Np))
-        if err:
-            return du, err, b
         ei = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
-        err = lib().oracle_rhs_from_proj(C.byref(self.op), _p(proj), _p(du), _pi(ei),
-                                         0 if ei is None else len(ei), C.byref(bad))
+        err = self.L.oracle_rhs_subset(C.byref(self.op), _p(u), _p(du), _pi(ei),
+                                       0 if ei is None else len(ei), C.byref(bad))
         return du, err, bad.value
 
     def step_lsrk45(self, u, res, dt, nsteps):
         u = np.array(u, dtype=np.float64, copy=True)
         res = np.array(res, dtype=np.float64, copy=True)
         bad = C.c_int(-1)
-        err = lib().oracle_step_lsrk45(C.byref(self.op), _p(u), _p(res), float(dt), int(nsteps),
+        err = self.L.oracle_step_lsrk45(C.byref(self.op), _p(u), _p(res), float(dt), int(nsteps),
                                        C.byref(bad))
         return u, res, err

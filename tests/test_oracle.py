@@ -122,3 +122,17 @@ def test_known_answer_ec_flux_and_entropy_vars():
     h_avg = 0.5 * (uL[0] + uR[0])
     p = g * h_avg * h_avg - 0.25 * g * (uL[0] ** 2 + uR[0] ** 2)
     assert (hu, hu * ux + p) == (1.0, 1.5)
+
+
+@pytest.mark.parametrize("name", MODAL + PROBLEMS_MODAL + PROBLEMS_SBP)
+def test_long_double_yardstick(name):
+    """The long-double build of the same algorithm agrees with the reference to its
+    rounding error; on states with du ~ 0 (lake/dam at rest) that error exceeds
+    1e-12 relative — which is why FAST is judged against it (test_gpu_parity)."""
+    c = load_golden(name)
+    ld, err, _ = Oracle(c, precision="ld").rhs(c["u"])
+    assert err == 0
+    ref = c["du_lf"]
+    abs_err = np.abs(ref - ld).max()
+    assert abs_err <= 1e-10 * (1.0 + np.abs(ld).max())
+    assert abs_err > 0.0  # genuinely a different (more precise) evaluation
