@@ -58,48 +58,63 @@ def dist_env():
 
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 50 ms; only samples whose
+    timestamp falls inside the timed region (mark_start/mark_stop) are kept."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 5.0
+            while not self.lines and time.time() < deadline:  # wait for the first sample
+                time.sleep(0.02)
         except FileNotFoundError:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
+        time.sleep(0.12)  # let the last in-window sample arrive
 
     def stop(self) -> dict:
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], None, set()
+        sm, mx, pw, reasons = [], None, [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if self.t0 is not None and not (self.t0 <= ts <= (self.t1 or ts) + 0.06):
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for n, v in zip(names, f[4:8]):
@@ -107,7 +122,8 @@ class ClockSampler:
                     reasons.add(n)
         sm.sort()
         med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
 
 
 # ---------------------------------------------------------------------------
@@ -140,13 +156,19 @@ def run_reference(args, rank, world):
     return 0
 
 
-def workload_config(args, k1d):
+def workload_config(args, k1d, world=1):
     K = 2 * k1d * k1d
-    return {"workload": f"C4: modal ESDG N={args.N}, K1D={k1d} (K={K} curved tris, warp {args.warp}), "
-                        "smooth wave + lake bathymetry, periodic [-1,1]^2, LF flux, LSRK45",
-            "N": args.N, "K1D": k1d, "K": K, "warp": args.warp, "scheme": "hybridized",
-            "mode": args.mode, "step": "one LSRK45 step = 5 RHS stages",
-            "l2": "inputs larger than L2 (device-resident state+geometry >> 126 MB)"}
+    cfg = {"workload": f"C4: modal ESDG N={args.N}, K1D={k1d} (K={K} curved tris, warp {args.warp}), "
+                       "smooth wave + lake bathymetry, periodic [-1,1]^2, LF flux, LSRK45",
+           "N": args.N, "K1D": k1d, "K": K, "warp": args.warp, "scheme": "hybridized",
+           "mode": args.mode, "step": "one LSRK45 step = 5 RHS stages",
+           "l2": "inputs larger than L2 (device-resident state+geometry >> 126 MB)"}
+    if world > 1:
+        cfg["partition"] = (f"weak scaling: {world} y-strips of a K1D x (K1D*{world}) periodic mesh on "
+                            f"[-1,1]x[-{world},{world}], {K} elements per GPU, per-stage NCCL halo "
+                            "exchange of face traces")
+        cfg["parallelism"] = f"element partition x{world}"
+    return cfg
 
 
 def cpu_baseline(args):
@@ -227,10 +249,14 @@ def run_ours(args, rank, world, local):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # weak scaling: every rank owns a K1D x K1D periodic block (no data-path exchange
-    # between blocks in this round)
+    # weak scaling: rank r owns y-strip r (K1D x K1D quads) of a global
+    # K1D x (K1D*world) periodic mesh; one halo exchange of face traces per stage
+    # (paper_2005_02516_b200/partition.py, NCCL point-to-point over NVLink).
     t0 = time.time()
-    case = capi.Case("smooth", N=args.N, nx=args.k1d, warp=args.warp, seed=23)
+    if world > 1:
+        case = capi.Case("smooth", N=args.N, nx=args.k1d, warp=args.warp, seed=23, strips=world, strip=rank)
+    else:
+        case = capi.Case("smooth", N=args.N, nx=args.k1d, warp=args.warp, seed=23)
     mode = capi.MODE_FAST if args.mode == "fast" else capi.MODE_PARITY
     h = case.handle(mode=mode, device=local)
     u0 = case.u0()
@@ -238,11 +264,34 @@ def run_ours(args, rank, world, local):
     K, Np = case.K, case.Np
     dof = K * Np * 3
     dt = case.dt
+    stream = torch.cuda.Stream(device=local)
+    h.set_stream(stream.cuda_stream)
     h.set_state(u0)
-    stream = torch.cuda.ExternalStream(h.stream, device=local)
+    plan = None
+    if world > 1:
+        from paper_2005_02516_b200.partition import StripHalo, exchange, trace_tensor
+
+        t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        dt = float(t.item())
+        plan = StripHalo(world, rank, args.k1d, K)
+        trace = trace_tensor(h)
+
+    def steps(n, sync):
+        if plan is None:
+            h.step(dt, n, sync=sync)
+            return
+        with torch.cuda.stream(stream):
+            for _ in range(n):
+                for s_ in range(5):
+                    h.stage_volume(s_, dt)
+                    exchange(trace, plan)
+                    h.stage_surface(s_, dt)
+        if sync:
+            h.check()
 
     # warm-up
-    h.step(dt, args.warmup, sync=True)
+    steps(args.warmup, True)
     torch.cuda.synchronize()
     # ---- timed region: device-resident LSRK45 steps
     h.enable_timers(True)
@@ -254,10 +303,12 @@ def run_ours(args, rank, world, local):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
     e0.record(stream)
-    h.step(dt, args.steps, sync=False)
+    steps(args.steps, False)
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark_stop()
     if dist:
         dist.barrier()
     clk = clocks.stop()
@@ -277,7 +328,7 @@ def run_ours(args, rank, world, local):
     uh = torch.empty((K, 3, Np), dtype=torch.float64, pin_memory=True).numpy()
     uh[...] = u0
     h.set_state(uh)
-    h.step(dt, 1)
+    steps(1, True)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -285,7 +336,7 @@ def run_ours(args, rank, world, local):
     ee0.record(stream)
     for _ in range(args.e2e_steps):
         h.set_state(uh)               # H2D of the step's input state
-        h.step(dt, 1, sync=False)     # 5 stages on the device
+        steps(1, False)               # 5 stages on the device (+ halo exchanges)
         h.get_state(uh, with_res=False)  # D2H of the step's result
     ee1.record(stream)
     torch.cuda.synchronize()
@@ -347,7 +398,7 @@ def run_ours(args, rank, world, local):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, args.k1d),
+        "config": workload_config(args, args.k1d, world),
         "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes,
                 "path": "swedg_set_state (pinned H2D) + swedg_step_lsrk45(1) + swedg_get_state (D2H)"},

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SWEDG_ABI_VERSION 1
+#define SWEDG_ABI_VERSION 2
 
 /* status codes */
 #define SWEDG_OK 0
@@ -105,6 +105,11 @@ typedef struct {
     /* connectivity (mesh.hpp:143-154, 333-373) */
     const int* nbr;  /* [K][3]  neighbour element of face f, -1 = wall (FaceType::Wall) */
     const int* perm; /* [K][nf] FaceMatch::perm[k][f][s]: neighbour surface slot (ignored on walls) */
+
+    /* multi-rank (element partition): neighbour ids K..K+n_halo-1 address halo
+     * slots whose face traces the caller fills between swedg_stage_volume and
+     * swedg_stage_surface (hybridized scheme).  0 for a single rank. */
+    int n_halo;
 } swedg_desc;
 
 /* ---- lifecycle ------------------------------------------------------------ */
@@ -137,6 +142,14 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync);
 int swedg_state_device_ptr(swedg_handle h, double** u, double** res);
 /* du = rhs(u) with device pointers, stream-ordered, no host sync. */
 int swedg_rhs_device(swedg_handle h, const double* u_dev, double* du_dev, double t);
+/* Stage-level stepping for multi-rank runs: one LSRK45 stage (0..4) split at the
+ * halo exchange.  swedg_stage_volume runs the projection+volume kernel and
+ * writes the owned elements' face traces; the caller then fills the halo trace
+ * slots (device pointer below, layout [K + n_halo][3][nf]); swedg_stage_surface
+ * runs the fused surface + lift + M^-1 + register update.  Stream-ordered. */
+int swedg_stage_volume(swedg_handle h, int stage, double dt);
+int swedg_stage_surface(swedg_handle h, int stage, double dt);
+int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo);
 /* Check the device error record (syncs the stream). */
 int swedg_check(swedg_handle h);
 

@@ -37,6 +37,9 @@ typedef struct {
     double g;        /* <= 0: the problem's default */
     unsigned seed;   /* SMOOTH: mt19937 seed of smooth_state */
     int threads;     /* host threads, <= 0: hardware concurrency */
+    int strips;      /* > 1: build only y-strip `strip` of a global nx x (ny*strips) mesh */
+    int strip;       /*      (periodic problems, hybridized): owned rows + 2 halo rows;
+                        strip == -1: the whole global strip mesh in one piece */
 } swedg_case_config;
 
 int swedg_case_build(const swedg_case_config* cfg, swedg_case* out);

@@ -373,6 +373,17 @@ int oracle_rhs_from_proj(const oracle_ops *op, const double *proj, double *du,
     return e;
 }
 
+/* proj holds n_proj_elems element blocks (owned + halo slots addressed by nbr) */
+int oracle_rhs_from_proj_n(const oracle_ops *op, const double *proj, int n_proj_elems, double *du,
+                           const int *elems, int n_elems, int *bad_elem) {
+    size_t n = (size_t)n_proj_elems * 3 * (op->nq + op->nf);
+    real *p = (real *)malloc(sizeof(real) * n);
+    for (size_t i = 0; i < n; ++i) p[i] = proj[i];
+    int e = rhs_from_proj_real(op, p, du, elems, n_elems, bad_elem);
+    free(p);
+    return e;
+}
+
 /* projection kept in REAL precision between the two phases */
 int oracle_rhs(const oracle_ops *op, const double *u, double *du, double *proj_scratch,
                int *bad_elem) {

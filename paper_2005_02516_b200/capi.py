@@ -61,10 +61,11 @@ class _Desc(C.Structure):
         ("Vq", _dp), ("Vf", _dp), ("Pq", _dp), ("Qr", _dp), ("Qs", _dp), ("wf", _dp),
         ("face_index", _ip), ("M_diag", _dp),
         ("gf", _dp), ("sJ", _dp), ("nx", _dp), ("ny", _dp), ("J_vol", _dp), ("Mh_inv", _dp),
-        ("nbr", _ip), ("perm", _ip),
+        ("nbr", _ip), ("perm", _ip), ("n_halo", C.c_int),
     ]
 
 
+ABI_VERSION = 2
 _lib = None
 
 
@@ -106,6 +107,9 @@ def lib() -> C.CDLL:
     L.swedg_enable_timers.argtypes = [vp, C.c_int]
     L.swedg_read_timers.argtypes = [vp, _dp, C.POINTER(C.c_longlong), C.c_int]
     L.swedg_probe_fp64_peak.argtypes = [C.c_int, C.c_int, _dp]
+    L.swedg_stage_volume.argtypes = [vp, C.c_int, C.c_double]
+    L.swedg_stage_surface.argtypes = [vp, C.c_int, C.c_double]
+    L.swedg_trace_device_ptr.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
     _lib = L
     return L
 
@@ -117,6 +121,7 @@ EXPORTED = [
     "swedg_rhs_device", "swedg_check", "swedg_last_error", "swedg_create_error",
     "swedg_launch_count", "swedg_device_bytes", "swedg_abi_version", "swedg_debug_bathymetry",
     "swedg_enable_timers", "swedg_read_timers", "swedg_probe_fp64_peak",
+    "swedg_stage_volume", "swedg_stage_surface", "swedg_trace_device_ptr",
 ]
 
 
@@ -156,7 +161,7 @@ class Handle:
     def __init__(self, *, scheme: int, N: int, Np: int, nq: int, nf: int, npf: int, K: int,
                  g: float, Qr, Qs, wf, gf, sJ, nx, ny, nbr, perm, Vq=None, Vf=None, Pq=None,
                  Mh_inv=None, face_index=None, M_diag=None, J_vol=None,
-                 penalty: int = PENALTY_LF, mode: int = MODE_FAST, device: int = 0):
+                 penalty: int = PENALTY_LF, mode: int = MODE_FAST, device: int = 0, n_halo: int = 0):
         L = lib()
         self.sizes = Sizes(N, Np, nq, nf, npf, K)
         self.scheme = scheme
@@ -177,7 +182,7 @@ class Handle:
             return _pi(a)
 
         d = _Desc()
-        d.abi_version = 1
+        d.abi_version = ABI_VERSION
         d.scheme, d.penalty, d.mode = scheme, penalty, mode
         d.N, d.Np, d.nq, d.nf, d.npf, d.K = N, Np, nq, nf, npf, K
         d.g = float(g)
@@ -186,6 +191,7 @@ class Handle:
         d.face_index, d.M_diag = i(face_index), f(M_diag)
         d.gf, d.sJ, d.nx, d.ny, d.J_vol, d.Mh_inv = f(gf), f(sJ), f(nx), f(ny), f(J_vol), f(Mh_inv)
         d.nbr, d.perm = i(nbr), i(perm)
+        d.n_halo = int(n_halo)
         h = C.c_void_p()
         rc = L.swedg_create(C.byref(d), C.byref(h))
         if rc != SWEDG_OK:
@@ -272,6 +278,21 @@ class Handle:
         self._check(self._lib.swedg_get_state(self._h, _p(u), _p(r), C.byref(t)))
         return u, r, t.value
 
+    # -- stage-level stepping (multi-rank halo exchange between the two kernels)
+    def stage_volume(self, stage: int, dt: float):
+        self._check(self._lib.swedg_stage_volume(self._h, int(stage), float(dt)))
+
+    def stage_surface(self, stage: int, dt: float):
+        self._check(self._lib.swedg_stage_surface(self._h, int(stage), float(dt)))
+
+    def trace_info(self):
+        """(device pointer, n_owned, n_halo) of the face-trace buffer [K+n_halo][3][nf]."""
+        p = C.c_void_p()
+        a = C.c_longlong()
+        b = C.c_longlong()
+        self._check(self._lib.swedg_trace_device_ptr(self._h, C.byref(p), C.byref(a), C.byref(b)))
+        return p.value, a.value, b.value
+
     def enable_timers(self, on: bool = True):
         self._check(self._lib.swedg_enable_timers(self._h, 1 if on else 0))
 
@@ -354,7 +375,7 @@ PROBLEMS = {"lake": PROBLEM_LAKE, "vortex": PROBLEM_VORTEX, "dambreak": PROBLEM_
 class _CaseCfg(C.Structure):
     _fields_ = [("problem", C.c_int), ("scheme", C.c_int), ("N", C.c_int), ("nx", C.c_int),
                 ("ny", C.c_int), ("warp", C.c_double), ("cfl", C.c_double), ("g", C.c_double),
-                ("seed", C.c_uint), ("threads", C.c_int)]
+                ("seed", C.c_uint), ("threads", C.c_int), ("strips", C.c_int), ("strip", C.c_int)]
 
 
 def _setup_lib():
@@ -382,12 +403,16 @@ class Case:
     """A problem built by the native setup (lake / vortex / dambreak / smooth)."""
 
     def __init__(self, problem="smooth", *, scheme=SCHEME_HYBRIDIZED, N=4, nx=16, ny=None,
-                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0):
+                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0):
+        """strips > 1: rank `strip`'s y-strip of a global nx x (ny*strips) periodic mesh on
+        [-Lx/2,Lx/2] x [-strips*Ly/2, strips*Ly/2] (weak scaling); its 2 halo rows follow the
+        K owned elements (below: slots K..K+2nx, above: K+2nx..K+4nx)."""
         L = _setup_lib()
         cfg = _CaseCfg()
         cfg.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
         cfg.scheme, cfg.N, cfg.nx, cfg.ny = scheme, N, nx, ny if ny is not None else nx
         cfg.warp, cfg.cfl, cfg.g, cfg.seed, cfg.threads = warp, cfl, g, seed, threads
+        cfg.strips, cfg.strip = strips, strip
         h = C.c_void_p()
         rc = L.swedg_case_build(C.byref(cfg), C.byref(h))
         if rc != SWEDG_OK:
@@ -402,6 +427,8 @@ class Case:
         self.dt = L.swedg_case_dt(self._c)
         self.min_edge = L.swedg_case_min_edge(self._c)
         self.nstate = self.nq if scheme == SCHEME_SBP else self.Np
+        self.n_halo = d.n_halo
+        self.nx = nx
 
     def array(self, name: str) -> np.ndarray:
         n = C.c_size_t()

@@ -562,6 +562,26 @@ Mesh uniform_tri_mesh(int nx, int ny, const Domain& dom, bool flip_below_center)
     return m;
 }
 
+// Quad rows [j_lo, j_hi) of a global nx x ny_tot grid on `dom` (rows outside
+// [0, ny_tot) are the periodic images, used as halo rows of a y-strip).
+Mesh uniform_tri_mesh_rows(int nx, int j_lo, int j_hi, int ny_tot, const Domain& dom) {
+    Mesh m;
+    m.dom = dom;
+    const int nr = j_hi - j_lo;
+    m.verts.reserve((size_t)(nx + 1) * (nr + 1));
+    for (int j = j_lo; j <= j_hi; ++j)
+        for (int i = 0; i <= nx; ++i) m.verts.push_back({dom.xmin() + dom.Lx * i / nx, dom.ymin() + dom.Ly * j / ny_tot});
+    auto vid = [&](int i, int j) { return (j - j_lo) * (nx + 1) + i; };
+    m.tris.reserve((size_t)2 * nx * nr);
+    for (int j = j_lo; j < j_hi; ++j)
+        for (int i = 0; i < nx; ++i) {
+            int v00 = vid(i, j), v10 = vid(i + 1, j), v01 = vid(i, j + 1), v11 = vid(i + 1, j + 1);
+            m.tris.push_back({v00, v10, v11});
+            m.tris.push_back({v00, v11, v01});
+        }
+    return m;
+}
+
 void set_mapping_degree(Mesh& m, int N, int threads) {
     m.Nmap = N;
     std::vector<double> lx, ly;
@@ -801,6 +821,8 @@ struct swedg_case_s {
     std::vector<double> gf, sJ, nx, ny, J_vol, Mh_inv;
     std::vector<int> nbr, nbr_face, face_type, perm;
     std::vector<double> u0, b, xy_vol, xy_surf, map_coeffs, volq_w, shift;
+    bool periodic_x = true, periodic_y = true;
+    int n_halo = 0;
 };
 
 namespace {
@@ -880,8 +902,7 @@ void build_geometry_and_ops(swedg_case_s& c, int threads) {
         }
     });
     // connectivity arrays + face matching
-    const bool periodic = c.cfg.problem != SWEDG_PROBLEM_DAMBREAK;
-    std::vector<FaceInfo> faces = connect(c.mesh, periodic, periodic);
+    std::vector<FaceInfo> faces = connect(c.mesh, c.periodic_x, c.periodic_y);
     const int npf = R.npf;
     c.nbr.assign((size_t)K * 3, -1);
     c.nbr_face.assign((size_t)K * 3, -1);
@@ -941,6 +962,42 @@ Cons vortex_exact(double x, double y, double t, double g) {
 
 double lake_bathymetry(double x, double) { return 0.1 * std::sin(2.0 * M_PI * x) * std::cos(2.0 * M_PI * x) + 0.5; }
 
+// Keep the owned rows of a strip (local rows 1..ny) as elements 0..K-1 and turn
+// the two halo rows into halo slots: below row -> K + [0, 2nx), above row ->
+// K + 2nx + [0, 2nx).  Per-element arrays shrink to the owned elements.
+void compact_strip(swedg_case_s& c) {
+    const long row = 2L * c.cfg.nx;
+    const long K_all = c.K, K_own = K_all - 2 * row;
+    auto new_id = [&](long id) -> long {
+        const long r = id / row, t = id - r * row;
+        if (r == 0) return K_own + t;
+        if (id >= K_all - row) return K_own + row + t;
+        return id - row;
+    };
+    auto shrink = [&](std::vector<double>& v) {
+        if (v.empty()) return;
+        const size_t per = v.size() / (size_t)K_all;
+        v.erase(v.begin(), v.begin() + (size_t)row * per);
+        v.resize((size_t)K_own * per);
+    };
+    auto shrink_i = [&](std::vector<int>& v) {
+        const size_t per = v.size() / (size_t)K_all;
+        v.erase(v.begin(), v.begin() + (size_t)row * per);
+        v.resize((size_t)K_own * per);
+    };
+    for (auto* v : {&c.gf, &c.sJ, &c.nx, &c.ny, &c.J_vol, &c.Mh_inv, &c.u0, &c.b, &c.xy_vol, &c.xy_surf,
+                    &c.map_coeffs, &c.shift})
+        shrink(*v);
+    shrink_i(c.nbr_face);
+    shrink_i(c.face_type);
+    shrink_i(c.perm);
+    shrink_i(c.nbr);
+    for (auto& n : c.nbr)
+        if (n >= 0) n = (int)new_id(n);
+    c.K = K_own;
+    c.n_halo = (int)(2 * row);
+}
+
 void build_case(swedg_case_s& c) {
     const swedg_case_config& cfg = c.cfg;
     int threads = cfg.threads > 0 ? cfg.threads : (int)std::max(1u, std::thread::hardware_concurrency());
@@ -980,7 +1037,22 @@ void build_case(swedg_case_s& c) {
             throw std::invalid_argument("unknown problem");
     }
     const bool dam = cfg.problem == SWEDG_PROBLEM_DAMBREAK;
-    c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny, dom, dam);
+    const int P = cfg.strips > 1 ? cfg.strips : 1;
+    c.periodic_x = c.periodic_y = !dam;
+    if (P > 1 && cfg.strip == -1) {  // the whole global strip mesh in one piece (reference for tests)
+        if (dam) throw std::invalid_argument("strip partitions need a periodic problem");
+        dom.Ly *= P;
+        c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny * P, dom, false);
+    } else if (P > 1) {
+        if (dam || cfg.scheme != SWEDG_SCHEME_HYBRIDIZED)
+            throw std::invalid_argument("strip partitions need a periodic problem and the hybridized scheme");
+        if (cfg.strip < 0 || cfg.strip >= P) throw std::invalid_argument("strip index out of range");
+        dom.Ly *= P;  // global domain; strip rows are the owned part of it
+        c.periodic_y = false;
+        c.mesh = uniform_tri_mesh_rows(cfg.nx, cfg.strip * cfg.ny - 1, (cfg.strip + 1) * cfg.ny + 1, cfg.ny * P, dom);
+    } else {
+        c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny, dom, dam);
+    }
     if (dam) snap_vertices_to_curve(c.mesh, qc);
     set_mapping_degree(c.mesh, cfg.N, threads);
     if (dam) {
@@ -1113,6 +1185,7 @@ void build_case(swedg_case_s& c) {
                 for (int i = 0; i < nq; ++i) uk[i] = h;
         }
     }
+    if (P > 1 && cfg.strip >= 0) compact_strip(c);
 }
 
 }  // namespace
@@ -1173,6 +1246,7 @@ int swedg_case_fill_desc(swedg_case c, swedg_desc* d) {
     d->Mh_inv = c->Mh_inv.empty() ? nullptr : c->Mh_inv.data();
     d->nbr = c->nbr.data();
     d->perm = c->perm.data();
+    d->n_halo = c->n_halo;
     return SWEDG_OK;
 }
 

@@ -37,6 +37,8 @@ struct Buf {
 
 struct swedg_handle_s {
     int scheme, penalty, mode, N, Np, nq, nf, npf, nh, K;
+    int n_halo = 0;           // halo element slots after the K owned elements (multi-rank)
+    unsigned stage_cur = 0;   // stage id of the open stage-level call (swedg_stage_*)
     double g;
     int device;
     int nsm = 148;
@@ -192,6 +194,7 @@ int kernel_occupancy(const void* kern, int device, int threads, size_t smem) {
 
 struct StageArgs {
     const double* u_in;
+    int parts = 3;  // bit 0: volume kernel, bit 1: surface/update kernel
     double* proj;       // optional
     bool rk;            // fused RK update on (h->u, h->res)
     double a, b, dt;
@@ -202,6 +205,7 @@ struct StageArgs {
 
 template <int N>
 int run_modal_stage(swedg_handle h, const StageArgs& sa) {
+    if (sa.parts & 1) {
     ModalVolParams vp;
     vp.K = h->K;
     vp.g = h->g;
@@ -249,7 +253,12 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         }
     }
     h->launches++;
-
+    }
+    if (!(sa.parts & 2)) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+        return SWEDG_OK;
+    }
     ModalSurfParams sp;
     sp.K = h->K;
     sp.g = h->g;
@@ -453,6 +462,9 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     if (!d || !out) return fail(nullptr, SWEDG_ERR_INVALID, "null descriptor");
     *out = nullptr;
     if (d->abi_version != SWEDG_ABI_VERSION) return fail(nullptr, SWEDG_ERR_INVALID, "ABI version mismatch");
+    if (d->n_halo < 0) return fail(nullptr, SWEDG_ERR_INVALID, "n_halo must be >= 0");
+    if (d->n_halo > 0 && d->scheme == SWEDG_SCHEME_SBP)
+        return fail(nullptr, SWEDG_ERR_UNSUPPORTED, "halo (multi-rank) elements are supported for the hybridized scheme");
     if (d->scheme != SWEDG_SCHEME_HYBRIDIZED && d->scheme != SWEDG_SCHEME_SBP)
         return fail(nullptr, SWEDG_ERR_INVALID, "unknown scheme");
     if (d->N < 1 || d->N > 4) return fail(nullptr, SWEDG_ERR_UNSUPPORTED, "degree must be 1..4");
@@ -487,6 +499,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->npf = npf;
     h->nh = d->nq + nf;
     h->K = d->K;
+    h->n_halo = d->n_halo;
     h->g = d->g;
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
@@ -512,7 +525,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     for (size_t k = 0; k < K; ++k)
         for (int f = 0; f < 3; ++f) {
             int nb = d->nbr[k * 3 + f];
-            if (nb < -1 || nb >= h->K) {
+            if (nb < -1 || nb >= h->K + h->n_halo) {
                 fail(h, SWEDG_ERR_INVALID, "neighbour index out of range in element " + std::to_string(k));
                 return bail(SWEDG_ERR_INVALID);
             }
@@ -574,7 +587,8 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
         if (dalloc(h, &h->Minv, K * Np * Np) || upload(h, h->Minv, d->Mh_inv, K * Np * Np)) return bail(h->last_code);
         if (dalloc(h, &h->bs, K * nh) || dalloc(h, &h->src, K * 2 * nh)) return bail(h->last_code);
-        if (dalloc(h, &h->trace, K * 3 * nf) || dalloc(h, &h->accf, K * 3 * nf) || dalloc(h, &h->T1, K * 3 * Np))
+        if (dalloc(h, &h->trace, (K + (size_t)h->n_halo) * 3 * nf) || dalloc(h, &h->accf, K * 3 * nf) ||
+            dalloc(h, &h->T1, K * 3 * Np))
             return bail(h->last_code);
     } else {
         std::vector<double> minv(K * nq);
@@ -784,7 +798,7 @@ int swedg_entropy_projection(swedg_handle h, const double* u, double t, double* 
     if (upload(h, h->utmp, u, K * 3 * h->Np)) return h->last_code;
     h->call_stage0 = h->next_stage;
     h->call_stage_t.assign(1, t);
-    StageArgs sa{h->utmp, h->proj, false, 0, 0, 0, h->du, h->next_stage++, false};
+    StageArgs sa{h->utmp, 3, h->proj, false, 0, 0, 0, h->du, h->next_stage++, false};
     if (run_stage(h, sa)) return h->last_code;
     CUDA_TRY(h, cudaMemcpyAsync(proj, h->proj, K * 3 * h->nh * 8, cudaMemcpyDeviceToHost, h->stream));
     int rc = check_errors(h);
@@ -800,7 +814,7 @@ int swedg_rhs(swedg_handle h, const double* u, double t, double* du) {
     if (upload(h, h->utmp, u, n)) return h->last_code;
     h->call_stage0 = h->next_stage;
     h->call_stage_t.assign(1, t);
-    StageArgs sa{h->utmp, nullptr, false, 0, 0, 0, h->du, h->next_stage++, false};
+    StageArgs sa{h->utmp, 3, nullptr, false, 0, 0, 0, h->du, h->next_stage++, false};
     if (run_stage(h, sa)) return h->last_code;
     CUDA_TRY(h, cudaMemcpyAsync(du, h->du, n * 8, cudaMemcpyDeviceToHost, h->stream));
     return check_errors(h);
@@ -812,7 +826,7 @@ int swedg_rhs_device(swedg_handle h, const double* u_dev, double* du_dev, double
     if (h->scheme == SWEDG_SCHEME_SBP && ensure_scratch(h)) return h->last_code;
     h->call_stage0 = h->next_stage;
     h->call_stage_t.assign(1, t);
-    StageArgs sa{u_dev, nullptr, false, 0, 0, 0, du_dev, h->next_stage++, false};
+    StageArgs sa{u_dev, 3, nullptr, false, 0, 0, 0, du_dev, h->next_stage++, false};
     return run_stage(h, sa);
 }
 
@@ -860,12 +874,46 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
         const double t0 = h->t;
         for (int s = 0; s < 5; ++s) {
             h->call_stage_t.push_back(t0 + Lsrk45::c[s] * dt);
-            StageArgs sa{h->u, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, h->next_stage++, true};
+            StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, h->next_stage++, true};
             if (run_stage(h, sa)) return h->last_code;
         }
         h->t = t0 + dt;
     }
     if (sync) return check_errors(h);
+    return SWEDG_OK;
+}
+
+int swedg_stage_volume(swedg_handle h, int stage, double dt) {
+    if (!h || stage < 0 || stage > 4) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
+        return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
+    cudaSetDevice(h->device);
+    if (stage == 0) {
+        h->call_stage0 = h->next_stage;
+        h->call_stage_t.clear();
+    }
+    h->stage_cur = h->next_stage++;
+    h->call_stage_t.push_back(h->t + Lsrk45::c[stage] * dt);
+    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true};
+    return run_stage(h, sa);
+}
+
+int swedg_stage_surface(swedg_handle h, int stage, double dt) {
+    if (!h || stage < 0 || stage > 4) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    cudaSetDevice(h->device);
+    StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true};
+    int rc = run_stage(h, sa);
+    if (rc == SWEDG_OK && stage == 4) h->t = h->t + dt;
+    return rc;
+}
+
+int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (trace) *trace = h->trace;
+    if (n_owned) *n_owned = h->K;
+    if (n_halo) *n_halo = h->n_halo;
     return SWEDG_OK;
 }
 

@@ -53,6 +53,7 @@ def lib(precision: str = "double"):
         _lib.oracle_rhs_sbp.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
         _lib.oracle_step_lsrk45.argtypes = [C.POINTER(OracleOps), _dp, _dp, C.c_double, C.c_int, _ip]
         _lib.oracle_rhs_subset.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
+        _lib.oracle_rhs_from_proj_n.argtypes = [C.POINTER(OracleOps), _dp, C.c_int, _dp, _ip, C.c_int, _ip]
         _libs[precision] = _lib
     return _libs[precision]
 
@@ -163,6 +164,17 @@ class Oracle:
                                        0 if ei is None else len(ei), C.byref(bad))
         return du, err, bad.value
 
+    def rhs_from_proj(self, proj_all):
+        """du of the K owned elements from projections of owned + halo element slots
+        (proj_all: [K + n_halo][3][nh]; nbr may address the halo slots)."""
+        proj_all = np.ascontiguousarray(proj_all, dtype=np.float64)
+        du = np.zeros((self.K, 3, self.Np))
+        bad = C.c_int(-1)
+        ei = np.arange(self.K, dtype=np.int32)
+        err = self.L.oracle_rhs_from_proj_n(C.byref(self.op), _p(proj_all), int(proj_all.shape[0]), _p(du),
+                                            _pi(ei), self.K, C.byref(bad))
+        return du, err, bad.value
+
     def step_lsrk45(self, u, res, dt, nsteps):
         u = np.array(u, dtype=np.float64, copy=True)
         res = np.array(res, dtype=np.float64, copy=True)
@@ -170,3 +182,17 @@ class Oracle:
         err = self.L.oracle_step_lsrk45(C.byref(self.op), _p(u), _p(res), float(dt), int(nsteps),
                                        C.byref(bad))
         return u, res, err
+
+
+def case_dict(c) -> dict:
+    """A native-setup case (paper_2005_02516_b200.capi.Case) in the golden-fixture layout."""
+    d = {"scheme": [c.scheme], "N": [c.N], "Np": [c.Np], "nq": [c.nq], "nf": [c.nf], "npf": [c.npf],
+         "K": [c.K], "g": [c.g], "surfq_w": c.array("surfq_w"), "gf": c.array("gf"), "sJ": c.array("sJ"),
+         "nx": c.array("nx"), "ny": c.array("ny"), "nbr": c.iarray("nbr"), "perm": c.iarray("perm"),
+         "b": c.b(), "u": c.u0(), "ref_Vq": c.array("Vq"), "ref_Vf": c.array("Vf"), "ref_Pq": c.array("Pq")}
+    if c.scheme == 1:
+        d.update(sbp_Qx=c.array("Qr"), sbp_Qy=c.array("Qs"), sbp_face_index=c.iarray("face_index"),
+                 sbp_M_diag=c.array("M_diag"), J_vol=c.array("J_vol"))
+    else:
+        d.update(ref_Qh_x=c.array("Qr"), ref_Qh_y=c.array("Qs"), Mh_inv=c.array("Mh_inv"))
+    return {k: np.asarray(v) for k, v in d.items()}

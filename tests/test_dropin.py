@@ -23,7 +23,7 @@ def test_cpp_dropin_against_reference():
 def test_dropin_adapter_header_compiles_standalone(tmp_path):
     """The adapter header is self-contained C++17 over the C ABI (no torch, no CUDA types)."""
     src = tmp_path / "t.cpp"
-    src.write_text('#include "swedg_b200.hpp"\nint main() { return swedg_abi_version() == 1 ? 0 : 1; }\n')
+    src.write_text('#include "swedg_b200.hpp"\nint main() { return swedg_abi_version() == SWEDG_ABI_VERSION ? 0 : 1; }\n')
     r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I", os.path.join(REPO, "include"), str(src)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
