@@ -20,6 +20,7 @@
 #include "modal_kernels.cuh"
 #include "modal_fast.cuh"
 #include "modal_warp_n4.cuh"
+#include "modal_quad_n4.cuh"
 #include "sbp_kernels.cuh"
 
 using namespace swedg;
@@ -236,6 +237,12 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
         } else if (N == 4 && h->vol_variant == 0) {
+            auto kern = modal_volume_quad_n4_kernel;
+            const size_t qsm = QuadN4::bytes();
+            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, QuadN4::T, qsm);
+            int grid = std::min((h->K + 4 * QuadN4::WARPS - 1) / (4 * QuadN4::WARPS), occ * h->nsm);
+            kern<<<std::max(grid, 1), QuadN4::T, qsm, h->stream>>>(vp);
+        } else if (N == 4 && h->vol_variant == 3) {
             auto kern = modal_volume_warp_n4_kernel;
             const size_t wsm = WarpN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, WarpN4::T, wsm);
@@ -504,7 +511,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
-        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : 0);
+        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : 0));
     }
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
