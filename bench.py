@@ -222,7 +222,8 @@ def flops_bytes_per_element(N):
     # surface+update kernel: traces (own + neighbour), acc_f, T1, surf (m,nx,ny), src_f,
     # nbr/perm, Mh_inv, u, res in; u, res out
     surf_flops = 71 * nf + 6 * Np * nf + 2 * Np * Np * 3 + 15 * Np
-    surf_bytes = 8 * (3 * nf * 2 + 3 * nf + 3 * Np + 3 * nf + 2 * nf + Np * Np + 3 * Np * 2 + 3 * Np * 2) + 4 * (3 + nf)
+    # (M_h^{-1} stored symmetric-packed in FAST mode: Np(Np+1)/2 doubles)
+    surf_bytes = 8 * (3 * nf * 2 + 3 * nf + 3 * Np + 3 * nf + 2 * nf + Np * (Np + 1) // 2 + 3 * Np * 2 + 3 * Np * 2) + 4 * (3 + nf)
     return {"vol_flops": vol_flops, "vol_bytes": vol_bytes, "surf_flops": surf_flops, "surf_bytes": surf_bytes,
             "U": U, "Np": Np, "nq": nq, "nf": nf, "nh": nh}
 

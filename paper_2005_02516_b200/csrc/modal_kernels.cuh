@@ -327,7 +327,8 @@ struct ModalSurfParams {
     const double* src;    // [K][2][nh]
     const int* nbr;       // [K][3]
     const int* perm;      // [K][nf]
-    const double* Minv;   // [K][Np][Np]
+    const double* Minv;   // [K][Np][Np] (PARITY)
+    const double* Mpk;    // [K][Np(Np+1)/2] symmetric-packed M_h^{-1} (FAST): row-major upper triangle
     double* du;           // rhs mode output [K][3][Np]
     double* u;            // RK mode state
     double* res;          // RK mode register
@@ -435,13 +436,25 @@ modal_surface_kernel(ModalSurfParams prm) {
     __syncthreads();
     // du = Mh_inv modal; finiteness; fused LSRK45 register update
     if (act && s < Np) {
-        const double* Mi = prm.Minv + (size_t)k * Np * Np + s;
         double du[3] = {0.0, 0.0, 0.0};
+        if constexpr (P) {
+            const double* Mi = prm.Minv + (size_t)k * Np * Np + s;
 #pragma unroll
-        for (int m = 0; m < Np; ++m) {
-            const double mim = Mi[m * Np];
+            for (int m = 0; m < Np; ++m) {
+                const double mim = Mi[m * Np];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) du[c] = A::fma(mim, smod[e][c * Np + m], du[c]);
+                for (int c = 0; c < 3; ++c) du[c] = A::fma(mim, smod[e][c * Np + m], du[c]);
+            }
+        } else {
+            // packed symmetric: entry (a <= b) at a*Np - a*(a-1)/2 + (b - a)
+            const double* Mk = prm.Mpk + (size_t)k * (Np * (Np + 1) / 2);
+#pragma unroll
+            for (int m = 0; m < Np; ++m) {
+                const int a = s < m ? s : m, b = s < m ? m : s;
+                const double mim = Mk[a * Np - a * (a - 1) / 2 + (b - a)];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) du[c] = A::fma(mim, smod[e][c * Np + m], du[c]);
+            }
         }
         if (!(isfinite(du[0]) && isfinite(du[1]) && isfinite(du[2])))
             record_error(prm.err, prm.stage_id, 1, k);

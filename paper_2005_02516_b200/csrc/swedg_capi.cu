@@ -43,7 +43,9 @@ struct swedg_handle_s {
     double g;
     int device;
     int nsm = 148;
-    int vol_variant = 0;  // FAST volume kernel: 0 = best for N (warp/TMEM at N=4), 1 = two-row, 2 = row
+    // FAST volume kernel (env SWEDG_VOLUME_KERNEL): 0 = default (N=4: warp/TMEM), 1 = "tworow",
+    // 2 = "row", 4 = "quad" (N=4, 4 elements/warp; measured slower: latency-bound at 6 warps/SM)
+    int vol_variant = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // device buffers
@@ -51,6 +53,7 @@ struct swedg_handle_s {
     double* gf = nullptr;    // [K][4][nrow]
     double* surf = nullptr;  // [K][3][nf]  w*sJ, nx, ny
     double* Minv = nullptr;  // modal: [K][Np][Np]; SBP: [K][nq] diagonal
+    double* Mpk = nullptr;   // modal FAST: [K][Np(Np+1)/2] symmetrised packed M_h^{-1}
     int* nbr = nullptr;      // [K][3]
     int* perm = nullptr;     // [K][nf]
     int* fidx = nullptr;     // SBP face_index [nf]
@@ -236,13 +239,13 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
-        } else if (N == 4 && h->vol_variant == 0) {
+        } else if (N == 4 && h->vol_variant == 4) {
             auto kern = modal_volume_quad_n4_kernel;
             const size_t qsm = QuadN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, QuadN4::T, qsm);
             int grid = std::min((h->K + 4 * QuadN4::WARPS - 1) / (4 * QuadN4::WARPS), occ * h->nsm);
             kern<<<std::max(grid, 1), QuadN4::T, qsm, h->stream>>>(vp);
-        } else if (N == 4 && h->vol_variant == 3) {
+        } else if (N == 4 && h->vol_variant == 0) {
             auto kern = modal_volume_warp_n4_kernel;
             const size_t wsm = WarpN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, WarpN4::T, wsm);
@@ -279,6 +282,7 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     sp.nbr = h->nbr;
     sp.perm = h->perm;
     sp.Minv = h->Minv;
+    sp.Mpk = h->Mpk;
     sp.du = sa.du_out;
     sp.u = h->u;
     sp.res = h->res;
@@ -511,7 +515,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
-        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : 0));
+        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "quad" ? 4 : 0));
     }
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
@@ -593,6 +597,18 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     }
     if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
         if (dalloc(h, &h->Minv, K * Np * Np) || upload(h, h->Minv, d->Mh_inv, K * Np * Np)) return bail(h->last_code);
+        {  // FAST: symmetrised, packed upper triangle (M_h^{-1} is SPD; 960 vs 1800 B/elem at N=4)
+            const int np2 = Np * (Np + 1) / 2;
+            std::vector<double> pk(K * np2);
+            for (size_t k = 0; k < K; ++k) {
+                const double* M = d->Mh_inv + k * Np * Np;
+                double* o = pk.data() + k * np2;
+                for (int a = 0; a < Np; ++a)
+                    for (int b = a; b < Np; ++b) *o++ = 0.5 * (M[a + b * Np] + M[b + a * Np]);
+            }
+            if (dalloc(h, &h->Mpk, pk.size()) || upload(h, h->Mpk, pk.data(), pk.size())) return bail(h->last_code);
+            cudaStreamSynchronize(h->stream);  // pk goes out of scope
+        }
         if (dalloc(h, &h->bs, K * nh) || dalloc(h, &h->src, K * 2 * nh)) return bail(h->last_code);
         if (dalloc(h, &h->trace, (K + (size_t)h->n_halo) * 3 * nf) || dalloc(h, &h->accf, K * 3 * nf) ||
             dalloc(h, &h->T1, K * 3 * Np))
@@ -626,7 +642,7 @@ int swedg_destroy(swedg_handle h) {
     if (!h) return SWEDG_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* ptrs[] = {h->ops, h->gf, h->surf, h->Minv, h->nbr, h->perm, h->fidx, h->bs, h->src, h->u,
+    void* ptrs[] = {h->ops, h->gf, h->surf, h->Minv, h->Mpk, h->nbr, h->perm, h->fidx, h->bs, h->src, h->u,
                     h->res, h->utmp, h->du, h->proj, h->trace, h->accf, h->T1, h->err};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -689,7 +705,6 @@ int swedg_probe_fp64_peak(int device, int reps, double* tflops) {
     if (!tflops) return SWEDG_ERR_INVALID;
     if (cudaSetDevice(device) != cudaSuccess) return SWEDG_ERR_CUDA;
     int nsm = 148;
-    int vol_variant = 0;  // FAST volume kernel: 0 = best for N (warp/TMEM at N=4), 1 = two-row, 2 = row
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double* d = nullptr;
     cudaMalloc(&d, 8);
