@@ -368,16 +368,46 @@ modal_surface_kernel(ModalSurfParams prm) {
     const bool act = k < prm.K;
     const double g = prm.g;
 
+    // ---- issue every independent global load up front (memory-level parallelism:
+    //      ncu showed this kernel long-scoreboard bound with phase-serial loads)
+    double t1r[3] = {0, 0, 0}, ur[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, mrow[Np];
+    if (act && s < Np) {
+        const size_t o = (size_t)k * 3 * Np + s;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            t1r[c] = prm.T1[o + c * Np];
+            if (prm.rk_mode) {
+                ur[c] = prm.u[o + c * Np];
+                rr[c] = prm.res[o + c * Np];
+            }
+        }
+        if constexpr (P) {
+            const double* Mi = prm.Minv + (size_t)k * Np * Np + s;
+#pragma unroll
+            for (int m = 0; m < Np; ++m) mrow[m] = Mi[m * Np];
+        } else {
+            const double* Mk = prm.Mpk + (size_t)k * (Np * (Np + 1) / 2);
+#pragma unroll
+            for (int m = 0; m < Np; ++m) {
+                const int a = s < m ? s : m, b = s < m ? m : s;
+                mrow[m] = Mk[a * Np - a * (a - 1) / 2 + (b - a)];
+            }
+        }
+    }
+
     if (act && s < nf) {
         const int f = s / npf;
+        const int nb = prm.nbr[(size_t)k * 3 + f];
+        const int jn = prm.perm[(size_t)k * nf + s];
         const double* tr = prm.trace + (size_t)k * 3 * nf + s;
         const double* af = prm.accf + (size_t)k * 3 * nf + s;
         const double* sf = prm.surf + (size_t)k * 3 * nf + s;
+        const double* srf = prm.src + (size_t)k * 2 * nh + nq + s;
         double ui[3] = {tr[0], tr[nf], tr[2 * nf]};
         double acc[3] = {af[0], af[nf], af[2 * nf]};
         const double m = sf[0], nxi = sf[nf], nyi = sf[2 * nf];
+        const double srx = srf[0], sry = srf[nh];
         const double Bx = A::mul(m, nxi), By = A::mul(m, nyi);
-        const int nb = prm.nbr[(size_t)k * 3 + f];
         double up[3];
         if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
             const double un = A::add(A::mul(ui[1], nxi), A::mul(ui[2], nyi));
@@ -385,8 +415,7 @@ modal_surface_kernel(ModalSurfParams prm) {
             up[1] = A::sub(ui[1], A::mul(A::mul(2.0, un), nxi));
             up[2] = A::sub(ui[2], A::mul(A::mul(2.0, un), nyi));
         } else {
-            const int j = prm.perm[(size_t)k * nf + s];
-            const double* tn = prm.trace + (size_t)nb * 3 * nf + j;
+            const double* tn = prm.trace + (size_t)nb * 3 * nf + jn;
             up[0] = tn[0];
             up[1] = tn[nf];
             up[2] = tn[2 * nf];
@@ -415,46 +444,30 @@ modal_surface_kernel(ModalSurfParams prm) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) acc[c] = A::sub(acc[c], A::mul(m, A::mul(hl, A::sub(up[c], ui[c]))));
         }
-        const double* sr = prm.src + (size_t)k * 2 * nh + nq + s;
         const double mgh = A::mul(-g, ui[0]);
         sst[e][s] = A::sub(0.0, acc[0]);
-        sst[e][nf + s] = A::sub(A::mul(mgh, sr[0]), acc[1]);
-        sst[e][2 * nf + s] = A::sub(A::mul(mgh, sr[nh]), acc[2]);
+        sst[e][nf + s] = A::sub(A::mul(mgh, srx), acc[1]);
+        sst[e][2 * nf + s] = A::sub(A::mul(mgh, sry), acc[2]);
     }
     __syncthreads();
     // modal = T1 + Vf^T stacked_surface  (solver.hpp:285-286)
     if (act && s < Np) {
-        const double* t1 = prm.T1 + (size_t)k * 3 * Np + s;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double t2 = 0.0;
 #pragma unroll
             for (int i = 0; i < nf; ++i) t2 = A::fma(sVf[i + s * nf], sst[e][c * nf + i], t2);
-            smod[e][c * Np + s] = A::add(t1[c * Np], t2);
+            smod[e][c * Np + s] = A::add(t1r[c], t2);
         }
     }
     __syncthreads();
     // du = Mh_inv modal; finiteness; fused LSRK45 register update
     if (act && s < Np) {
         double du[3] = {0.0, 0.0, 0.0};
-        if constexpr (P) {
-            const double* Mi = prm.Minv + (size_t)k * Np * Np + s;
 #pragma unroll
-            for (int m = 0; m < Np; ++m) {
-                const double mim = Mi[m * Np];
+        for (int m = 0; m < Np; ++m) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) du[c] = A::fma(mim, smod[e][c * Np + m], du[c]);
-            }
-        } else {
-            // packed symmetric: entry (a <= b) at a*Np - a*(a-1)/2 + (b - a)
-            const double* Mk = prm.Mpk + (size_t)k * (Np * (Np + 1) / 2);
-#pragma unroll
-            for (int m = 0; m < Np; ++m) {
-                const int a = s < m ? s : m, b = s < m ? m : s;
-                const double mim = Mk[a * Np - a * (a - 1) / 2 + (b - a)];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) du[c] = A::fma(mim, smod[e][c * Np + m], du[c]);
-            }
+            for (int c = 0; c < 3; ++c) du[c] = A::fma(mrow[m], smod[e][c * Np + m], du[c]);
         }
         if (!(isfinite(du[0]) && isfinite(du[1]) && isfinite(du[2])))
             record_error(prm.err, prm.stage_id, 1, k);
@@ -462,9 +475,9 @@ modal_surface_kernel(ModalSurfParams prm) {
         if (prm.rk_mode) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const double r = A::fma(prm.rk_a, prm.res[o + c * Np], A::mul(prm.dt, du[c]));
+                const double r = A::fma(prm.rk_a, rr[c], A::mul(prm.dt, du[c]));
                 prm.res[o + c * Np] = r;
-                prm.u[o + c * Np] = A::fma(prm.rk_b, r, prm.u[o + c * Np]);
+                prm.u[o + c * Np] = A::fma(prm.rk_b, r, ur[c]);
             }
         } else {
 #pragma unroll
