@@ -349,7 +349,7 @@ struct SurfCfg {
 };
 
 template <int N, bool P>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 8)
 modal_surface_kernel(ModalSurfParams prm) {
     using D = ModalDims<N>;
     using A = Ar<P>;
@@ -358,19 +358,26 @@ modal_surface_kernel(ModalSurfParams prm) {
     constexpr int L = SurfCfg<N>::L, E = SurfCfg<N>::E, T = SurfCfg<N>::T;
     if (prm.early_exit && error_pending(prm.err)) return;
 
+    constexpr int NPK = Np * (Np + 1) / 2;
     __shared__ double sVf[nf * Np];
     __shared__ double sst[E][3 * nf];
     __shared__ double smod[E][3 * Np];
+    __shared__ double sMpk[P ? 1 : E * NPK];
     const int tid = threadIdx.x;
     for (int x = tid; x < nf * Np; x += T) sVf[x] = prm.ops[O::Vf + x];
     const int e = tid / L, s = tid % L;
     const int k = blockIdx.x * E + e;
     const bool act = k < prm.K;
     const double g = prm.g;
+    if constexpr (!P) {  // packed M_h^{-1} of the block's elements: one contiguous coalesced copy
+        const int k0 = blockIdx.x * E, ne = min(E, prm.K - k0);
+        const double* src = prm.Mpk + (size_t)k0 * NPK;
+        for (int x = tid; x < ne * NPK; x += T) sMpk[x] = src[x];
+    }
 
     // ---- issue every independent global load up front (memory-level parallelism:
     //      ncu showed this kernel long-scoreboard bound with phase-serial loads)
-    double t1r[3] = {0, 0, 0}, ur[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, mrow[Np];
+    double t1r[3] = {0, 0, 0}, ur[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, mrow[P ? Np : 1];
     if (act && s < Np) {
         const size_t o = (size_t)k * 3 * Np + s;
 #pragma unroll
@@ -385,13 +392,6 @@ modal_surface_kernel(ModalSurfParams prm) {
             const double* Mi = prm.Minv + (size_t)k * Np * Np + s;
 #pragma unroll
             for (int m = 0; m < Np; ++m) mrow[m] = Mi[m * Np];
-        } else {
-            const double* Mk = prm.Mpk + (size_t)k * (Np * (Np + 1) / 2);
-#pragma unroll
-            for (int m = 0; m < Np; ++m) {
-                const int a = s < m ? s : m, b = s < m ? m : s;
-                mrow[m] = Mk[a * Np - a * (a - 1) / 2 + (b - a)];
-            }
         }
     }
 
@@ -466,8 +466,15 @@ modal_surface_kernel(ModalSurfParams prm) {
         double du[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int m = 0; m < Np; ++m) {
+            double mm;
+            if constexpr (P) {
+                mm = mrow[m];
+            } else {  // packed symmetric: entry (a <= b) at a*Np - a*(a-1)/2 + (b - a)
+                const int a = s < m ? s : m, b = s < m ? m : s;
+                mm = sMpk[e * NPK + a * Np - a * (a - 1) / 2 + (b - a)];
+            }
 #pragma unroll
-            for (int c = 0; c < 3; ++c) du[c] = A::fma(mrow[m], smod[e][c * Np + m], du[c]);
+            for (int c = 0; c < 3; ++c) du[c] = A::fma(mm, smod[e][c * Np + m], du[c]);
         }
         if (!(isfinite(du[0]) && isfinite(du[1]) && isfinite(du[2])))
             record_error(prm.err, prm.stage_id, 1, k);
