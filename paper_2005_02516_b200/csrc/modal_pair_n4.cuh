@@ -1,0 +1,398 @@
+// FAST-mode modal volume kernel for N = 4, v5: TWO elements per warp (one per
+// half-warp), 16 lanes per element, lane l' = lane % 16 owns stacked rows l'
+// and l'+16; rows 32..39 are split over the 16 lanes by column parity.
+//
+// Rationale (ncu, profiles/r1_v3c_volume_full_k512.md): the warp-per-element
+// kernel is L1-bound (83 % L1, 63 % FP64) because every node-j operand is a
+// shared-memory broadcast that feeds only one pair per lane.  With two rows per
+// lane and two elements per warp a node-j fetch (2 addresses, one per half)
+// feeds 64 pairs, and every projection broadcast serves two elements, halving
+// shared traffic per element while keeping one warp = one unit of work (no
+// __syncthreads) and 16 warps per SM.  The skew-operator rows of the lane's
+// three rows and its projection rows stay in TENSOR MEMORY (512 columns), the
+// next pair's u/gf/b stream in with cp.async during the flux loops.
+//
+//   loop A  rows l', l'+16      x columns 0..24          (25 steps, 2 pairs/lane)
+//   loop B  row 32+(l'&7)       x columns of parity l'>>3 (13 steps, shfl_xor(8) reduce)
+//   loop C  rows l', l'+16 (<25) x columns 25..39          (15 steps)
+#pragma once
+
+#include <stdint.h>
+
+#include "modal_quad_n4.cuh"
+
+namespace swedg {
+
+struct PairN4 {
+    static constexpr int Np = 15, nq = 25, nf = 15, nh = 40;
+    static constexpr int WARPS = 16, T = WARPS * 32;
+    // TMEM columns (32-bit); every (QA,QB) pair = 4 columns, a double = 2 columns
+    static constexpr int tA = 0;     // Q row l'      : 40 columns j
+    static constexpr int tB = 160;   // Q row l'+16   : 40 columns j
+    static constexpr int tC = 320;   // Q row 32+(l'&7): 13 column slots
+    static constexpr int tV = 372;   // V rows of l', l'+16, 32+(l'&7): 3 x 15 doubles (packed)
+    static constexpr int tP = 462;   // Pq row l'     : 25 doubles
+    static constexpr int tcols = 512;
+    // per-element work block (doubles)
+    static constexpr int wA = 0, wB = 80, wC = 160, wD = 240;  // double2[40]: (hu,hv) (u,v) (g1,g2) (g3,g4)
+    static constexpr int wH = 320;   // h[40]
+    static constexpr int wBs = 360;  // b[40]
+    static constexpr int wU = 400;   // 45 modal u            | stacked rows (75)
+    static constexpr int wV = 448;   // 75 entropy variables
+    static constexpr int wVh = 524;  // 45 projected variables
+    static constexpr int work_stride = 578;   // == 2 (mod 16)
+    static constexpr int stage_stride = 246;  // staging per element: u[45](+1) | gf[160] | b[40]
+    static constexpr int sU = 0, sG = 46, sB = 206;
+    static constexpr int per_warp = 2 * work_stride + 2 * stage_stride;
+    static constexpr int ops_len = 376;       // Vq (25 x 15, col-major) for the lift, +1 pad
+    static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
+};
+
+__global__ void __launch_bounds__(PairN4::T, 1)
+modal_volume_pair_n4_kernel(ModalVolParams prm) {
+    using W = PairN4;
+    using O = ModalOps<4>;
+    constexpr int Np = W::Np, nq = W::nq, nf = W::nf, nh = W::nh;
+    if (prm.early_exit && error_pending(prm.err)) return;
+
+    extern __shared__ __align__(16) double smem[];
+    __shared__ uint32_t tmem_base_sh;
+    double* sVq = smem;  // 25 x 15
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int half = lane >> 4, lp = lane & 15;
+    double* wbase = smem + W::ops_len + warp * W::per_warp;
+    double* work = wbase + half * W::work_stride;           // this lane's element
+    double* stage = wbase + 2 * W::work_stride;              // 2 elements, raw layouts
+    const double2* nA = reinterpret_cast<const double2*>(work + W::wA);
+    const double2* nB = reinterpret_cast<const double2*>(work + W::wB);
+    const double2* nC = reinterpret_cast<const double2*>(work + W::wC);
+    const double2* nD = reinterpret_cast<const double2*>(work + W::wD);
+    const double* nH = work + W::wH;
+
+    // ---- CTA setup
+    for (int x = threadIdx.x; x < nq * Np; x += W::T) sVq[x] = prm.ops[O::Vq + x];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_addr_u32(&tmem_base_sh)),
+                     "n"(W::tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16);
+    const int rA = lp, rB = lp + 16, rC = 32 + (lp & 7), par = lp >> 3;
+    if (warp < 4) {
+        const double* QA = prm.ops + O::QA;
+        const double* QB = prm.ops + O::QB;
+        for (int j = 0; j < nh; ++j) {
+            tmem_st4(tbase + W::tA + 4 * j, QA[rA + j * nh], QB[rA + j * nh]);
+            tmem_st4(tbase + W::tB + 4 * j, QA[rB + j * nh], QB[rB + j * nh]);
+        }
+        for (int s = 0; s < 13; ++s) {
+            const int j = par + 2 * s;
+            const bool ok = j < nq;
+            tmem_st4(tbase + W::tC + 4 * s, ok ? QA[rC + j * nh] : 0.0, ok ? QB[rC + j * nh] : 0.0);
+        }
+        const double* gVq = prm.ops + O::Vq;
+        const double* gVf = prm.ops + O::Vf;
+        const double* gPq = prm.ops + O::Pq;
+        const int rows[3] = {rA, rB, rC};
+        for (int q = 0; q < 3; ++q)
+            for (int m = 0; m < Np; ++m) {
+                const int r = rows[q];
+                tmem_st2(tbase + W::tV + 30 * q + 2 * m, r < nq ? gVq[r + m * nq] : gVf[(r - nq) + m * nf]);
+            }
+        for (int i = 0; i < nq; ++i) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? gPq[lp + i * Np] : 0.0);
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    const double g = prm.g, ig = 1.0 / g, g2 = 2.0 * g;
+    const int npairs = (prm.K + 1) / 2;
+    const int gw = blockIdx.x * W::WARPS + warp, nw = gridDim.x * W::WARPS;
+
+    auto issue = [&](int pr) {
+        const int k0 = 2 * pr;
+        if (k0 + 1 < prm.K) {
+            // u: 2 x 45 doubles (8 B granules: element blocks are 246 apart)
+            const double* gu = prm.u + (size_t)k0 * 3 * Np;
+            for (int x = lane; x < 90; x += 32) {
+                const int e = x / 45, r = x - e * 45;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sU + r)),
+                             "l"(gu + x)
+                             : "memory");
+            }
+            // gf: 2 x 160 doubles; b: 2 x 40 doubles — element k0 even, so 16 B aligned
+            const double* gg = prm.gf + (size_t)k0 * 4 * nh;
+            for (int x = lane; x < 160; x += 32) {
+                const int e = (2 * x) / 160, r = 2 * x - e * 160;
+                cp_async16(stage + e * W::stage_stride + W::sG + r, gg + 2 * x);
+            }
+            const double* gb = prm.bs + (size_t)k0 * nh;
+            for (int x = lane; x < 40; x += 32) {
+                const int e = (2 * x) / 40, r = 2 * x - e * 40;
+                cp_async16(stage + e * W::stage_stride + W::sB + r, gb + 2 * x);
+            }
+        } else if (k0 < prm.K) {  // odd K: last element alone
+            for (int r = lane; r < 45; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
+            for (int r = lane; r < 160; r += 32) stage[W::sG + r] = prm.gf[(size_t)k0 * 160 + r];
+            for (int r = lane; r < 40; r += 32) stage[W::sB + r] = prm.bs[(size_t)k0 * 40 + r];
+        }
+        cp_async_commit();
+    };
+
+    if (gw < npairs) issue(gw);
+    for (int pr = gw; pr < npairs; pr += nw) {
+        const int k = 2 * pr + half;
+        const bool valid = k < prm.K;
+        cp_async_wait_all();
+        __syncwarp();
+        // ---- park: staging -> work (u, b, g pairs), freeing the staging for the next pair
+        {
+            const double* st = stage + half * W::stage_stride;
+            for (int r = lp; r < 45; r += 16) work[W::wU + r] = st[W::sU + r];
+            for (int r = lp; r < 40; r += 16) {
+                work[W::wBs + r] = st[W::sB + r];
+                reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(st[W::sG + r], st[W::sG + nh + r]);
+                reinterpret_cast<double2*>(work + W::wD)[r] =
+                    make_double2(st[W::sG + 2 * nh + r], st[W::sG + 3 * nh + r]);
+            }
+        }
+        __syncwarp();
+        if (pr + nw < npairs) issue(pr + nw);
+
+        // ---- entropy variables at volume points rA (all) and rB (< 25)
+        {
+            double Va[16], Vb[16];
+            tmem_ld32d(tbase + W::tV, Va);          // doubles 0..15: row rA (15), rB starts at 15
+            tmem_ld32d(tbase + W::tV + 32, Vb);     // doubles 16..31
+            // unpack: row rA = d[0..14], row rB = d[15..29]
+            double uq[2][3] = {};
+#pragma unroll
+            for (int m = 0; m < Np; ++m) {
+                const double u0 = work[W::wU + m], u1 = work[W::wU + Np + m], u2 = work[W::wU + 2 * Np + m];
+                const double a = Va[m];
+                const double b = (m + 15 < 16) ? Va[m + 15] : Vb[m - 1];
+                uq[0][0] = __fma_rn(a, u0, uq[0][0]);
+                uq[0][1] = __fma_rn(a, u1, uq[0][1]);
+                uq[0][2] = __fma_rn(a, u2, uq[0][2]);
+                uq[1][0] = __fma_rn(b, u0, uq[1][0]);
+                uq[1][1] = __fma_rn(b, u1, uq[1][1]);
+                uq[1][2] = __fma_rn(b, u2, uq[1][2]);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int i = q == 0 ? rA : rB;
+                if (i < nq) {
+                    if (valid && !(uq[q][0] > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                    const double inv = 1.0 / uq[q][0];
+                    const double vx = uq[q][1] * inv, vy = uq[q][2] * inv;
+                    work[W::wV + i] = g * (uq[q][0] + work[W::wBs + i]) - 0.5 * (vx * vx + vy * vy);
+                    work[W::wV + nq + i] = vx;
+                    work[W::wV + 2 * nq + i] = vy;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- vh = Pq v (lane l' = output m)
+        {
+            double Pa[16], Pb[16];
+            tmem_ld32d(tbase + W::tP, Pa);            // doubles 0..15
+            tmem_ld16d(tbase + W::tP + 32, Pb);       // doubles 16..23
+            Pb[8] = tmem_ld2d(tbase + W::tP + 48);    // double 24 (last allocated columns)
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int i = 0; i < nq; ++i) {
+                const double p = i < 16 ? Pa[i] : Pb[i - 16];
+                s0 = __fma_rn(p, work[W::wV + i], s0);
+                s1 = __fma_rn(p, work[W::wV + nq + i], s1);
+                s2 = __fma_rn(p, work[W::wV + 2 * nq + i], s2);
+            }
+            if (lp < Np) {
+                work[W::wVh + lp] = s0;
+                work[W::wVh + Np + lp] = s1;
+                work[W::wVh + 2 * Np + lp] = s2;
+            }
+        }
+        __syncwarp();
+        // ---- projected states at rows rA, rB, rC (rC only lanes l' < 8 store)
+        Row5 RA, RB, RC;
+        {
+            double Va[16], Vb[16], Vc[16];
+            tmem_ld32d(tbase + W::tV, Va);        // doubles 0..15
+            tmem_ld32d(tbase + W::tV + 32, Vb);   // 16..31
+            tmem_ld32d(tbase + W::tV + 64, Vc);   // 32..47 (row rC = doubles 30..44)
+            double vt[3][3] = {};
+#pragma unroll
+            for (int m = 0; m < Np; ++m) {
+                const double h0 = work[W::wVh + m], h1 = work[W::wVh + Np + m], h2 = work[W::wVh + 2 * Np + m];
+                const double a = Va[m];
+                const double b = (m + 15 < 16) ? Va[m + 15] : Vb[m - 1];
+                const double c = (m + 30 < 32) ? Vb[m + 14] : Vc[m - 2];
+                vt[0][0] = __fma_rn(a, h0, vt[0][0]);
+                vt[0][1] = __fma_rn(a, h1, vt[0][1]);
+                vt[0][2] = __fma_rn(a, h2, vt[0][2]);
+                vt[1][0] = __fma_rn(b, h0, vt[1][0]);
+                vt[1][1] = __fma_rn(b, h1, vt[1][1]);
+                vt[1][2] = __fma_rn(b, h2, vt[1][2]);
+                vt[2][0] = __fma_rn(c, h0, vt[2][0]);
+                vt[2][1] = __fma_rn(c, h1, vt[2][1]);
+                vt[2][2] = __fma_rn(c, h2, vt[2][2]);
+            }
+            auto finish = [&](Row5& r, const int q, const int row) {
+                const double h = (vt[q][0] + 0.5 * (vt[q][1] * vt[q][1] + vt[q][2] * vt[q][2])) * ig - work[W::wBs + row];
+                r.U = h * vt[q][1];
+                r.V = h * vt[q][2];
+                r.u = vt[q][1];
+                r.v = vt[q][2];
+                r.gh4 = g2 * h;
+                const double2 c = nC[row], d = nD[row];
+                r.g1 = c.x;
+                r.g2 = c.y;
+                r.g3 = d.x;
+                r.g4 = d.y;
+                r.a0 = r.a1 = r.a2 = 0.0;
+                if (q < 2 || lp < 8) {
+                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                    reinterpret_cast<double2*>(work + W::wA)[row] = make_double2(r.U, r.V);
+                    reinterpret_cast<double2*>(work + W::wB)[row] = make_double2(r.u, r.v);
+                    work[W::wH + row] = h;
+                    if (valid && row >= nq) {
+                        double* tr = prm.trace + (size_t)k * 3 * nf + (row - nq);
+                        tr[0] = h;
+                        tr[nf] = r.U;
+                        tr[2 * nf] = r.V;
+                    }
+                    if (valid && prm.proj) {
+                        double* pj = prm.proj + (size_t)k * 3 * nh + row;
+                        pj[0] = h;
+                        pj[nh] = r.U;
+                        pj[2 * nh] = r.V;
+                    }
+                }
+            };
+            finish(RA, 0, rA);
+            finish(RB, 1, rB);
+            finish(RC, 2, rC);
+        }
+        __syncwarp();
+        // ---- loop A: rows rA, rB x volume columns 0..24
+#pragma unroll 1
+        for (int j0 = 0; j0 < 24; j0 += 4) {
+            double2 qa[4], qb[4];
+            tmem_ld16(tbase + W::tA + 4 * j0, qa);
+            tmem_ld16(tbase + W::tB + 4 * j0, qb);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int j = j0 + p;
+                const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
+                const double hj = nH[j];
+                pair5(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
+                pair5(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
+            }
+        }
+        {
+            const double2 qa = tmem_ld4(tbase + W::tA + 4 * 24), qb = tmem_ld4(tbase + W::tB + 4 * 24);
+            const double2 A = nA[24], B = nB[24], C = nC[24], D = nD[24];
+            pair5(RA, qa, A, B, C.x, C.y, D.x, D.y, nH[24]);
+            pair5(RB, qb, A, B, C.x, C.y, D.x, D.y, nH[24]);
+        }
+        // rows 25..31 (rB for l' >= 9) are complete surface rows
+        if (valid && rB >= nq) {
+            double* af = prm.accf + (size_t)k * 3 * nf + (rB - nq);
+            af[0] = 2.0 * RB.a0;
+            af[nf] = RB.a1;
+            af[2 * nf] = RB.a2;
+        }
+        // ---- loop B: row rC x columns of parity `par`
+        {
+            double2 qc[16];
+            tmem_ld16(tbase + W::tC, *reinterpret_cast<double2(*)[4]>(&qc[0]));
+            tmem_ld16(tbase + W::tC + 16, *reinterpret_cast<double2(*)[4]>(&qc[4]));
+            tmem_ld16(tbase + W::tC + 32, *reinterpret_cast<double2(*)[4]>(&qc[8]));
+            tmem_ld16(tbase + W::tC + 48, *reinterpret_cast<double2(*)[4]>(&qc[12]));
+#pragma unroll
+            for (int s = 0; s < 13; ++s) {
+                const int j = par + 2 * s;
+                if (j < nq) {
+                    const double2 C = nC[j], D = nD[j];
+                    pair5(RC, qc[s], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
+                }
+            }
+            RC.a0 += __shfl_xor_sync(0xffffffffu, RC.a0, 8);
+            RC.a1 += __shfl_xor_sync(0xffffffffu, RC.a1, 8);
+            RC.a2 += __shfl_xor_sync(0xffffffffu, RC.a2, 8);
+            if (valid && lp < 8) {
+                double* af = prm.accf + (size_t)k * 3 * nf + (rC - nq);
+                af[0] = 2.0 * RC.a0;
+                af[nf] = RC.a1;
+                af[2 * nf] = RC.a2;
+            }
+        }
+        // ---- loop C: volume rows rA (all), rB (l' <= 8) x surface columns 25..39
+        const bool bvol = rB < nq;
+#pragma unroll 1
+        for (int j0 = nq; j0 < nh; j0 += 4) {
+            double2 qa[4], qb[4];
+            tmem_ld16(tbase + W::tA + 4 * j0, qa);
+            tmem_ld16(tbase + W::tB + 4 * j0, qb);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int j = j0 + p;
+                if (j < nh) {
+                    const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
+                    const double hj = nH[j];
+                    pair5(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
+                    if (bvol) pair5(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
+                }
+            }
+        }
+        // ---- stacked = src - acc on volume rows, then T1 = Vq^T stacked
+        {
+            double* stk = work + W::wU;  // modal u is dead
+            const double* sr = prm.src + (size_t)k * 2 * nh;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int row = q == 0 ? rA : rB;
+                const Row5& r = q == 0 ? RA : RB;
+                if (row < nq) {
+                    const double mgh = -g * nH[row];
+                    stk[row] = -2.0 * r.a0;
+                    stk[nq + row] = valid ? mgh * sr[row] - r.a1 : 0.0;
+                    stk[2 * nq + row] = valid ? mgh * sr[nh + row] - r.a2 : 0.0;
+                }
+            }
+        }
+        __syncwarp();
+        {
+            const double* stk = work + W::wU;
+            const int m = lp < Np ? lp : Np - 1;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int i = 0; i < nq; ++i) {
+                const double v = sVq[i + m * nq];
+                s0 = __fma_rn(v, stk[i], s0);
+                s1 = __fma_rn(v, stk[nq + i], s1);
+                s2 = __fma_rn(v, stk[2 * nq + i], s2);
+            }
+            if (valid && lp < Np) {
+                double* out = prm.T1 + (size_t)k * 3 * Np;
+                out[lp] = s0;
+                out[Np + lp] = s1;
+                out[2 * Np + lp] = s2;
+            }
+        }
+        __syncwarp();
+    }
+    cp_async_wait_all();
+
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(W::tcols));
+}
+
+}  // namespace swedg

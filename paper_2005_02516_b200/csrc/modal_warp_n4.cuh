@@ -98,6 +98,28 @@ __device__ __forceinline__ void tmem_ld32d(uint32_t taddr, double (&d)[16]) {
     for (int p = 0; p < 16; ++p) d[p] = __hiloint2double(r[2 * p + 1], r[2 * p]);
 }
 
+// 16 columns -> 8 doubles
+__device__ __forceinline__ void tmem_ld16d(uint32_t taddr, double (&d)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int p = 0; p < 8; ++p) d[p] = __hiloint2double(r[2 * p + 1], r[2 * p]);
+}
+
+// 2 columns -> 1 double
+__device__ __forceinline__ double tmem_ld2d(uint32_t taddr) {
+    uint32_t r0, r1;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(taddr) : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return __hiloint2double(r1, r0);
+}
+
 __device__ __forceinline__ void tmem_st2(uint32_t taddr, double a) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__double2loint(a)),
                  "r"(__double2hiint(a))

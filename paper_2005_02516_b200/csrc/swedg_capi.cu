@@ -21,6 +21,7 @@
 #include "modal_fast.cuh"
 #include "modal_warp_n4.cuh"
 #include "modal_quad_n4.cuh"
+#include "modal_pair_n4.cuh"
 #include "sbp_kernels.cuh"
 
 using namespace swedg;
@@ -239,6 +240,12 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
+        } else if (N == 4 && h->vol_variant == 5) {
+            auto kern = modal_volume_pair_n4_kernel;
+            const size_t psm = PairN4::bytes();
+            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
+            int grid = std::min((h->K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
+            kern<<<std::max(grid, 1), PairN4::T, psm, h->stream>>>(vp);
         } else if (N == 4 && h->vol_variant == 4) {
             auto kern = modal_volume_quad_n4_kernel;
             const size_t qsm = QuadN4::bytes();
@@ -515,7 +522,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
-        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "quad" ? 4 : 0));
+        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "quad" ? 4 : (sv == "pair" ? 5 : 0)));
     }
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
