@@ -221,26 +221,35 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
         // ---- projected states at rows rA, rB, rC (rC only lanes l' < 8 store)
         Row5 RA, RB, RC;
         {
-            double Va[16], Vb[16], Vc[16];
-            tmem_ld32d(tbase + W::tV, Va);        // doubles 0..15
-            tmem_ld32d(tbase + W::tV + 32, Vb);   // 16..31
-            tmem_ld32d(tbase + W::tV + 64, Vc);   // 32..47 (row rC = doubles 30..44)
             double vt[3][3] = {};
+            {  // rows rA (doubles 0..14) and rB (15..29)
+                double Va[16], Vb[16];
+                tmem_ld32d(tbase + W::tV, Va);        // doubles 0..15
+                tmem_ld32d(tbase + W::tV + 32, Vb);   // 16..31
 #pragma unroll
-            for (int m = 0; m < Np; ++m) {
-                const double h0 = work[W::wVh + m], h1 = work[W::wVh + Np + m], h2 = work[W::wVh + 2 * Np + m];
-                const double a = Va[m];
-                const double b = (m + 15 < 16) ? Va[m + 15] : Vb[m - 1];
-                const double c = (m + 30 < 32) ? Vb[m + 14] : Vc[m - 2];
-                vt[0][0] = __fma_rn(a, h0, vt[0][0]);
-                vt[0][1] = __fma_rn(a, h1, vt[0][1]);
-                vt[0][2] = __fma_rn(a, h2, vt[0][2]);
-                vt[1][0] = __fma_rn(b, h0, vt[1][0]);
-                vt[1][1] = __fma_rn(b, h1, vt[1][1]);
-                vt[1][2] = __fma_rn(b, h2, vt[1][2]);
-                vt[2][0] = __fma_rn(c, h0, vt[2][0]);
-                vt[2][1] = __fma_rn(c, h1, vt[2][1]);
-                vt[2][2] = __fma_rn(c, h2, vt[2][2]);
+                for (int m = 0; m < Np; ++m) {
+                    const double h0 = work[W::wVh + m], h1 = work[W::wVh + Np + m], h2 = work[W::wVh + 2 * Np + m];
+                    const double a = Va[m];
+                    const double b = (m + 15 < 16) ? Va[m + 15] : Vb[m - 1];
+                    vt[0][0] = __fma_rn(a, h0, vt[0][0]);
+                    vt[0][1] = __fma_rn(a, h1, vt[0][1]);
+                    vt[0][2] = __fma_rn(a, h2, vt[0][2]);
+                    vt[1][0] = __fma_rn(b, h0, vt[1][0]);
+                    vt[1][1] = __fma_rn(b, h1, vt[1][1]);
+                    vt[1][2] = __fma_rn(b, h2, vt[1][2]);
+                }
+            }
+            {  // row rC (doubles 30..44)
+                double Vb[16], Vc[16];
+                tmem_ld32d(tbase + W::tV + 32, Vb);   // 16..31
+                tmem_ld32d(tbase + W::tV + 64, Vc);   // 32..47
+#pragma unroll
+                for (int m = 0; m < Np; ++m) {
+                    const double c = (m + 30 < 32) ? Vb[m + 14] : Vc[m - 2];
+                    vt[2][0] = __fma_rn(c, work[W::wVh + m], vt[2][0]);
+                    vt[2][1] = __fma_rn(c, work[W::wVh + Np + m], vt[2][1]);
+                    vt[2][2] = __fma_rn(c, work[W::wVh + 2 * Np + m], vt[2][2]);
+                }
             }
             auto finish = [&](Row5& r, const int q, const int row) {
                 const double h = (vt[q][0] + 0.5 * (vt[q][1] * vt[q][1] + vt[q][2] * vt[q][2])) * ig - work[W::wBs + row];
@@ -279,6 +288,31 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             finish(RC, 2, rC);
         }
         __syncwarp();
+        // ---- loop B: row rC x columns of parity `par`
+        {
+#pragma unroll
+            for (int s0 = 0; s0 < 16; s0 += 4) {  // 4 column slots per TMEM load
+                double2 qc[4];
+                tmem_ld16(tbase + W::tC + 4 * s0, qc);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int j = par + 2 * (s0 + t);
+                    if (s0 + t < 13 && j < nq) {
+                        const double2 C = nC[j], D = nD[j];
+                        pair5(RC, qc[t], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
+                    }
+                }
+            }
+            RC.a0 += __shfl_xor_sync(0xffffffffu, RC.a0, 8);
+            RC.a1 += __shfl_xor_sync(0xffffffffu, RC.a1, 8);
+            RC.a2 += __shfl_xor_sync(0xffffffffu, RC.a2, 8);
+            if (valid && lp < 8) {
+                double* af = prm.accf + (size_t)k * 3 * nf + (rC - nq);
+                af[0] = 2.0 * RC.a0;
+                af[nf] = RC.a1;
+                af[2 * nf] = RC.a2;
+            }
+        }
         // ---- loop A: rows rA, rB x volume columns 0..24
 #pragma unroll 1
         for (int j0 = 0; j0 < 24; j0 += 4) {
@@ -306,31 +340,6 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             af[0] = 2.0 * RB.a0;
             af[nf] = RB.a1;
             af[2 * nf] = RB.a2;
-        }
-        // ---- loop B: row rC x columns of parity `par`
-        {
-            double2 qc[16];
-            tmem_ld16(tbase + W::tC, *reinterpret_cast<double2(*)[4]>(&qc[0]));
-            tmem_ld16(tbase + W::tC + 16, *reinterpret_cast<double2(*)[4]>(&qc[4]));
-            tmem_ld16(tbase + W::tC + 32, *reinterpret_cast<double2(*)[4]>(&qc[8]));
-            tmem_ld16(tbase + W::tC + 48, *reinterpret_cast<double2(*)[4]>(&qc[12]));
-#pragma unroll
-            for (int s = 0; s < 13; ++s) {
-                const int j = par + 2 * s;
-                if (j < nq) {
-                    const double2 C = nC[j], D = nD[j];
-                    pair5(RC, qc[s], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
-                }
-            }
-            RC.a0 += __shfl_xor_sync(0xffffffffu, RC.a0, 8);
-            RC.a1 += __shfl_xor_sync(0xffffffffu, RC.a1, 8);
-            RC.a2 += __shfl_xor_sync(0xffffffffu, RC.a2, 8);
-            if (valid && lp < 8) {
-                double* af = prm.accf + (size_t)k * 3 * nf + (rC - nq);
-                af[0] = 2.0 * RC.a0;
-                af[nf] = RC.a1;
-                af[2 * nf] = RC.a2;
-            }
         }
         // ---- loop C: volume rows rA (all), rB (l' <= 8) x surface columns 25..39
         const bool bvol = rB < nq;
