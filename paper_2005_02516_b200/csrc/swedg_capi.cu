@@ -44,8 +44,9 @@ struct swedg_handle_s {
     double g;
     int device;
     int nsm = 148;
-    // FAST volume kernel (env SWEDG_VOLUME_KERNEL): 0 = default (N=4: warp/TMEM), 1 = "tworow",
-    // 2 = "row", 4 = "quad" (N=4, 4 elements/warp; measured slower: latency-bound at 6 warps/SM)
+    // FAST volume kernel (env SWEDG_VOLUME_KERNEL): 0 = default (N=4: "pair", 2 elements/warp,
+    // TMEM operators), 1 = "tworow", 2 = "row", 3 = "warp" (N=4, warp/element, TMEM),
+    // 4 = "quad" (N=4, 4 elements/warp; measured slower: latency-bound at 6 warps/SM)
     int vol_variant = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -240,7 +241,7 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
-        } else if (N == 4 && h->vol_variant == 5) {
+        } else if (N == 4 && h->vol_variant == 0) {
             auto kern = modal_volume_pair_n4_kernel;
             const size_t psm = PairN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
@@ -252,7 +253,7 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, QuadN4::T, qsm);
             int grid = std::min((h->K + 4 * QuadN4::WARPS - 1) / (4 * QuadN4::WARPS), occ * h->nsm);
             kern<<<std::max(grid, 1), QuadN4::T, qsm, h->stream>>>(vp);
-        } else if (N == 4 && h->vol_variant == 0) {
+        } else if (N == 4 && h->vol_variant == 3) {
             auto kern = modal_volume_warp_n4_kernel;
             const size_t wsm = WarpN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, WarpN4::T, wsm);
@@ -522,7 +523,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
-        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "quad" ? 4 : (sv == "pair" ? 5 : 0)));
+        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : (sv == "quad" ? 4 : 0)));
     }
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
