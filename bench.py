@@ -367,10 +367,10 @@ def run_ours(args, rank, world, local):
         t = traffic.get(name)
         return None if not t else round(t["dram_bytes_per_element"] * K)
 
-    vol_traffic = _tr("modal_volume_kernel")
-    surf_traffic = _tr("modal_surface_kernel")
+    vol_traffic = _tr("volume")
+    surf_traffic = _tr("surface")
     roofline = {
-        "kernel": "modal_volume_kernel<4,fast> (entropy projection + flux differencing + volume lift)",
+        "kernel": "modal_volume_pair_n4_kernel (FAST: entropy projection + flux differencing + volume lift)",
         "bound": "fp64", "achieved": round(vol_tflops, 4), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
         "frac": round(vol_tflops / fp64_peak, 4), "traffic": vol_traffic,
         "traffic_note": "ncu --set full dram__bytes_read+write per element (profiles/ncu_traffic.json) x K",
@@ -380,7 +380,7 @@ def run_ours(args, rank, world, local):
         "flops_per_element": fb["vol_flops"],
     }
     roofline_surface = {
-        "kernel": "modal_surface_kernel<4,fast> (interface flux + LF + lift + Mh_inv + LSRK update)",
+        "kernel": "modal_surface_kernel<4,FAST> (interface flux + LF + lift + Mh_inv + LSRK update)",
         "bound": "hbm", "achieved": round(surf_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(surf_gbs / hbm_peak, 4), "traffic": surf_traffic, "peak_source": hbm_src,
         "algorithmic_bytes_per_launch": fb["surf_bytes"] * K, "avg_launch_ms": round(surf_avg_ms, 4),
