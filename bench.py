@@ -215,14 +215,15 @@ def flops_bytes_per_element(N):
     U = nq * (nq - 1) // 2 + nq * nf
     f_proj = 6 * Np * (2 * nq + nh) + 9 * (nq + nh)
     f_vol = 55 * U + 7 * nh
-    f_lift = 6 * Np * nh  # the N=4 FAST volume kernel lifts src - acc_vol over all stacked rows
-    vol_flops = f_proj + f_vol + f_lift
-    # volume kernel bytes: u, gf, b_stacked, src (all rows) in; traces, T1 out
-    vol_bytes = 8 * (3 * Np + 4 * nh + nh + 2 * nh + 3 * nf + 3 * Np)
-    # surface+update kernel: traces (own + neighbour), T1, w*sJ/nx/ny, nbr/perm,
-    # packed M_h^{-1}, u and res in; u and res out
+    f_lift_v = 6 * Np * nq
+    vol_flops = f_proj + f_vol + f_lift_v
+    # volume kernel bytes: u, gf, b_stacked, src (volume rows) in; traces, acc_f, T1 out
+    vol_bytes = 8 * (3 * Np + 4 * nh + nh + 2 * nq + 3 * nf + 3 * nf + 3 * Np)
+    # surface+update kernel: traces (own + neighbour), acc_f, T1, surf (m,nx,ny), src_f,
+    # nbr/perm, Mh_inv, u, res in; u, res out
     surf_flops = 71 * nf + 6 * Np * nf + 2 * Np * Np * 3 + 15 * Np
-    surf_bytes = 8 * (3 * nf * 2 + 3 * Np + 3 * nf + Np * (Np + 1) // 2 + 3 * Np * 2 + 3 * Np * 2) + 4 * (3 + nf)
+    # (M_h^{-1} stored symmetric-packed in FAST mode: Np(Np+1)/2 doubles)
+    surf_bytes = 8 * (3 * nf * 2 + 3 * nf + 3 * Np + 3 * nf + 2 * nf + Np * (Np + 1) // 2 + 3 * Np * 2 + 3 * Np * 2) + 4 * (3 + nf)
     return {"vol_flops": vol_flops, "vol_bytes": vol_bytes, "surf_flops": surf_flops, "surf_bytes": surf_bytes,
             "U": U, "Np": Np, "nq": nq, "nf": nf, "nh": nh}
 

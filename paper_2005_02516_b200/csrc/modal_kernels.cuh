@@ -49,7 +49,6 @@ struct ModalVolParams {
     ErrRec* err;
     unsigned stage_id;
     int early_exit;
-    int lift_all;       // FAST N=4: T1 lifts src - acc_volume over ALL stacked rows (no accf)
 };
 
 template <int N>
@@ -338,7 +337,6 @@ struct ModalSurfParams {
     ErrRec* err;
     unsigned stage_id;
     int early_exit;
-    int lift_all;         // T1 already holds Vq^T(src-acc)_vol + Vf^T(src_f - acc_f,vol)
 };
 
 template <int N>
@@ -405,18 +403,10 @@ modal_surface_kernel(ModalSurfParams prm) {
         const double* af = prm.accf + (size_t)k * 3 * nf + s;
         const double* sf = prm.surf + (size_t)k * 3 * nf + s;
         const double* srf = prm.src + (size_t)k * 2 * nh + nq + s;
-        const bool la = !P && prm.lift_all;
         double ui[3] = {tr[0], tr[nf], tr[2 * nf]};
-        double acc[3] = {0.0, 0.0, 0.0};
-        double srx = 0.0, sry = 0.0;
-        if (!la) {
-            acc[0] = af[0];
-            acc[1] = af[nf];
-            acc[2] = af[2 * nf];
-            srx = srf[0];
-            sry = srf[nh];
-        }
+        double acc[3] = {af[0], af[nf], af[2 * nf]};
         const double m = sf[0], nxi = sf[nf], nyi = sf[2 * nf];
+        const double srx = srf[0], sry = srf[nh];
         const double Bx = A::mul(m, nxi), By = A::mul(m, nyi);
         double up[3];
         if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
@@ -454,16 +444,10 @@ modal_surface_kernel(ModalSurfParams prm) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) acc[c] = A::sub(acc[c], A::mul(m, A::mul(hl, A::sub(up[c], ui[c]))));
         }
-        if (la) {  // source and the volume accumulator were lifted by the volume kernel
-            sst[e][s] = -acc[0];
-            sst[e][nf + s] = -acc[1];
-            sst[e][2 * nf + s] = -acc[2];
-        } else {
-            const double mgh = A::mul(-g, ui[0]);
-            sst[e][s] = A::sub(0.0, acc[0]);
-            sst[e][nf + s] = A::sub(A::mul(mgh, srx), acc[1]);
-            sst[e][2 * nf + s] = A::sub(A::mul(mgh, sry), acc[2]);
-        }
+        const double mgh = A::mul(-g, ui[0]);
+        sst[e][s] = A::sub(0.0, acc[0]);
+        sst[e][nf + s] = A::sub(A::mul(mgh, srx), acc[1]);
+        sst[e][2 * nf + s] = A::sub(A::mul(mgh, sry), acc[2]);
     }
     __syncthreads();
     // modal = T1 + Vf^T stacked_surface  (solver.hpp:285-286)

@@ -44,8 +44,7 @@ struct PairN4 {
     static constexpr int stage_stride = 246;  // staging per element: u[45](+1) | gf[160] | b[40]
     static constexpr int sU = 0, sG = 46, sB = 206;
     static constexpr int per_warp = 2 * work_stride + 2 * stage_stride;
-    static constexpr int ops_len = 600;       // Vq (25 x 15) and Vf (15 x 15), col-major, for the lift
-    static constexpr int wS = 400;   // stacked rows [3][40] (reuses u / v scratch: 120 doubles)
+    static constexpr int ops_len = 376;       // Vq (25 x 15, col-major) for the lift, +1 pad
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
 };
 
@@ -58,8 +57,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
-    double* sVq = smem;            // 25 x 15
-    double* sVf = smem + nq * Np;  // 15 x 15
+    double* sVq = smem;  // 25 x 15
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int half = lane >> 4, lp = lane & 15;
     double* wbase = smem + W::ops_len + warp * W::per_warp;
@@ -72,7 +70,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
     const double* nH = work + W::wH;
 
     // ---- CTA setup
-    for (int x = threadIdx.x; x < nq * Np + nf * Np; x += W::T) sVq[x] = prm.ops[O::Vq + x];  // Vq | Vf
+    for (int x = threadIdx.x; x < nq * Np; x += W::T) sVq[x] = prm.ops[O::Vq + x];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_addr_u32(&tmem_base_sh)),
@@ -308,14 +306,11 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             RC.a0 += __shfl_xor_sync(0xffffffffu, RC.a0, 8);
             RC.a1 += __shfl_xor_sync(0xffffffffu, RC.a1, 8);
             RC.a2 += __shfl_xor_sync(0xffffffffu, RC.a2, 8);
-            // rows 32..39 complete: stacked = src - acc_vol (lifted with T1 below)
-            if (lp < 8) {
-                double* stk = work + W::wS;
-                const double* sr = prm.src + (size_t)k * 2 * nh;
-                const double mgh = -g * nH[rC];
-                stk[rC] = -2.0 * RC.a0;
-                stk[nh + rC] = valid ? mgh * sr[rC] - RC.a1 : 0.0;
-                stk[2 * nh + rC] = valid ? mgh * sr[nh + rC] - RC.a2 : 0.0;
+            if (valid && lp < 8) {
+                double* af = prm.accf + (size_t)k * 3 * nf + (rC - nq);
+                af[0] = 2.0 * RC.a0;
+                af[nf] = RC.a1;
+                af[2 * nf] = RC.a2;
             }
         }
         // ---- loop A: rows rA, rB x volume columns 0..24
@@ -339,14 +334,12 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             pair5(RA, qa, A, B, C.x, C.y, D.x, D.y, nH[24]);
             pair5(RB, qb, A, B, C.x, C.y, D.x, D.y, nH[24]);
         }
-        // rows 25..31 (rB for l' >= 9) are complete surface rows -> stacked
-        if (rB >= nq) {
-            double* stk = work + W::wS;
-            const double* sr = prm.src + (size_t)k * 2 * nh;
-            const double mgh = -g * nH[rB];
-            stk[rB] = -2.0 * RB.a0;
-            stk[nh + rB] = valid ? mgh * sr[rB] - RB.a1 : 0.0;
-            stk[2 * nh + rB] = valid ? mgh * sr[nh + rB] - RB.a2 : 0.0;
+        // rows 25..31 (rB for l' >= 9) are complete surface rows
+        if (valid && rB >= nq) {
+            double* af = prm.accf + (size_t)k * 3 * nf + (rB - nq);
+            af[0] = 2.0 * RB.a0;
+            af[nf] = RB.a1;
+            af[2 * nf] = RB.a2;
         }
         // ---- loop C: volume rows rA (all), rB (l' <= 8) x surface columns 25..39
         const bool bvol = rB < nq;
@@ -366,9 +359,9 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 }
             }
         }
-        // ---- stacked = src - acc on volume rows; T1 = Vq^T st_vol + Vf^T st_surf (all 40 rows)
+        // ---- stacked = src - acc on volume rows, then T1 = Vq^T stacked
         {
-            double* stk = work + W::wS;
+            double* stk = work + W::wU;  // modal u is dead
             const double* sr = prm.src + (size_t)k * 2 * nh;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -377,29 +370,22 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 if (row < nq) {
                     const double mgh = -g * nH[row];
                     stk[row] = -2.0 * r.a0;
-                    stk[nh + row] = valid ? mgh * sr[row] - r.a1 : 0.0;
-                    stk[2 * nh + row] = valid ? mgh * sr[nh + row] - r.a2 : 0.0;
+                    stk[nq + row] = valid ? mgh * sr[row] - r.a1 : 0.0;
+                    stk[2 * nq + row] = valid ? mgh * sr[nh + row] - r.a2 : 0.0;
                 }
             }
         }
         __syncwarp();
         {
-            const double* stk = work + W::wS;
+            const double* stk = work + W::wU;
             const int m = lp < Np ? lp : Np - 1;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
             for (int i = 0; i < nq; ++i) {
                 const double v = sVq[i + m * nq];
                 s0 = __fma_rn(v, stk[i], s0);
-                s1 = __fma_rn(v, stk[nh + i], s1);
-                s2 = __fma_rn(v, stk[2 * nh + i], s2);
-            }
-#pragma unroll
-            for (int i = 0; i < nf; ++i) {
-                const double v = sVf[i + m * nf];
-                s0 = __fma_rn(v, stk[nq + i], s0);
-                s1 = __fma_rn(v, stk[nh + nq + i], s1);
-                s2 = __fma_rn(v, stk[2 * nh + nq + i], s2);
+                s1 = __fma_rn(v, stk[nq + i], s1);
+                s2 = __fma_rn(v, stk[2 * nq + i], s2);
             }
             if (valid && lp < Np) {
                 double* out = prm.T1 + (size_t)k * 3 * Np;

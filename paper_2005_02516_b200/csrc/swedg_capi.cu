@@ -227,8 +227,6 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     vp.err = h->err;
     vp.stage_id = sa.stage_id;
     vp.early_exit = sa.early_exit ? 1 : 0;
-    const bool lift_all = (N == 4 && h->mode == SWEDG_MODE_FAST && h->vol_variant == 0);
-    vp.lift_all = lift_all ? 1 : 0;
     using VC = VolCfg<N>;
     const size_t smem = VolSmem<N>::bytes(VC::E);
     const int nblk_needed = (h->K + VC::E - 1) / VC::E;
@@ -303,7 +301,6 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     sp.err = h->err;
     sp.stage_id = sa.stage_id;
     sp.early_exit = sa.early_exit ? 1 : 0;
-    sp.lift_all = (N == 4 && h->mode == SWEDG_MODE_FAST && h->vol_variant == 0) ? 1 : 0;
     using SC = SurfCfg<N>;
     const int grid = (h->K + SC::E - 1) / SC::E;
     {
