@@ -138,6 +138,9 @@ int swedg_get_state(swedg_handle h, double* u, double* res, double* t);
 /* nsteps LSRK45 steps of size dt on the device-resident state (solver.hpp:466-484).
  * Stream-ordered; errors are checked (one device sync) when sync != 0. */
 int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync);
+/* Replay nsteps >= 2 as a captured one-step CUDA graph (default on; off while
+ * per-kernel timers are enabled). */
+int swedg_set_graphs(swedg_handle h, int on);
 /* Raw device pointers of the resident state (for zero-copy interop). */
 int swedg_state_device_ptr(swedg_handle h, double** u, double** res);
 /* du = rhs(u) with device pointers, stream-ordered, no host sync. */

@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
     L.swedg_enable_timers.argtypes = [vp, C.c_int]
     L.swedg_read_timers.argtypes = [vp, _dp, C.POINTER(C.c_longlong), C.c_int]
     L.swedg_probe_fp64_peak.argtypes = [C.c_int, C.c_int, _dp]
+    L.swedg_set_graphs.argtypes = [vp, C.c_int]
     L.swedg_stage_volume.argtypes = [vp, C.c_int, C.c_double]
     L.swedg_stage_surface.argtypes = [vp, C.c_int, C.c_double]
     L.swedg_trace_device_ptr.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
@@ -121,7 +122,7 @@ EXPORTED = [
     "swedg_rhs_device", "swedg_check", "swedg_last_error", "swedg_create_error",
     "swedg_launch_count", "swedg_device_bytes", "swedg_abi_version", "swedg_debug_bathymetry",
     "swedg_enable_timers", "swedg_read_timers", "swedg_probe_fp64_peak",
-    "swedg_stage_volume", "swedg_stage_surface", "swedg_trace_device_ptr",
+    "swedg_stage_volume", "swedg_stage_surface", "swedg_trace_device_ptr", "swedg_set_graphs",
 ]
 
 
@@ -304,6 +305,9 @@ class Handle:
 
     def step(self, dt: float, nsteps: int = 1, sync: bool = True):
         self._check(self._lib.swedg_step_lsrk45(self._h, float(dt), int(nsteps), 1 if sync else 0))
+
+    def set_graphs(self, on: bool):
+        self._check(self._lib.swedg_set_graphs(self._h, 1 if on else 0))
 
     def check(self):
         self._check(self._lib.swedg_check(self._h))

@@ -80,6 +80,13 @@ struct swedg_handle_s {
     long last_elem = -1;
     double last_t = 0.0;
     std::string last_msg;
+    // CUDA graph of one LSRK45 step (10 kernels + step counter), replayed nsteps times
+    cudaGraphExec_t graph_exec = nullptr;
+    double graph_dt = 0.0;
+    cudaStream_t graph_stream = nullptr;
+    int graph_mode = -1, graph_penalty = -1;
+    unsigned graph_base = 0;
+    bool use_graphs = true;
     // per-kernel-class event timers
     bool timers = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -633,8 +640,8 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     if (dalloc(h, &h->u, ns) || dalloc(h, &h->res, ns)) return bail(h->last_code);
     if (h->scheme == SWEDG_SCHEME_SBP && dalloc(h, &h->du, ns)) return bail(h->last_code);
     if (dalloc(h, &h->err, 1)) return bail(h->last_code);
-    unsigned long long none = kNoError;
-    if (cudaMemcpyAsync(h->err, &none, sizeof(none), cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+    ErrRec none_rec{kNoError, 0ull};
+    if (cudaMemcpyAsync(h->err, &none_rec, sizeof(none_rec), cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
         cudaMemsetAsync(h->u, 0, ns * sizeof(double), h->stream) != cudaSuccess ||
         cudaMemsetAsync(h->res, 0, ns * sizeof(double), h->stream) != cudaSuccess ||
         cudaMemsetAsync(h->src, 0, K * 2 * (h->scheme == SWEDG_SCHEME_SBP ? nq : nh) * sizeof(double), h->stream) != cudaSuccess)
@@ -659,6 +666,7 @@ int swedg_destroy(swedg_handle h) {
         cudaEventDestroy(p.second.second);
     }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return SWEDG_OK;
@@ -893,13 +901,76 @@ int swedg_state_device_ptr(swedg_handle h, double** u, double** res) {
     return SWEDG_OK;
 }
 
+namespace {
+// Capture one LSRK45 step on the handle's stream into a CUDA graph (cached per
+// dt / stream / mode / penalty).  Stage ids baked into the graph are
+// graph_base..graph_base+4; record_error adds 5 x the device step counter.
+int capture_step_graph(swedg_handle h, double dt) {
+    if (h->graph_exec && h->graph_dt == dt && h->graph_stream == h->stream && h->graph_mode == h->mode &&
+        h->graph_penalty == h->penalty)
+        return SWEDG_OK;
+    if (h->graph_exec) {
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    h->graph_base = h->next_stage;
+    h->next_stage += 5;
+    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = SWEDG_OK;
+    const long long l0 = h->launches;
+    for (int s = 0; s < 5 && rc == SWEDG_OK; ++s) {
+        StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, h->graph_base + s, true};
+        rc = run_stage(h, sa);
+    }
+    step_counter_kernel<<<1, 1, 0, h->stream>>>(h->err);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    h->launches = l0;  // captured, not launched
+    if (rc != SWEDG_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        h->graph_exec = nullptr;
+        return fail(h, SWEDG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    h->graph_dt = dt;
+    h->graph_stream = h->stream;
+    h->graph_mode = h->mode;
+    h->graph_penalty = h->penalty;
+    return SWEDG_OK;
+}
+}  // namespace
+
 int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
     if (!h) return SWEDG_ERR_INVALID;
     if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
     if (nsteps < 0) return fail(h, SWEDG_ERR_INVALID, "nsteps must be >= 0");
     cudaSetDevice(h->device);
-    h->call_stage0 = h->next_stage;
     h->call_stage_t.clear();
+    // launch-bound regime (small K): replay a captured one-step graph; per-kernel
+    // timers need individual launches, so they disable the graph path
+    const bool graphs = h->use_graphs && !h->timers && nsteps >= 2;
+    if (graphs) {
+        if (capture_step_graph(h, dt)) return h->last_code;
+        h->call_stage0 = h->graph_base;
+        CUDA_TRY(h, cudaMemsetAsync(&h->err->step_ctr, 0, sizeof(unsigned long long), h->stream));
+        for (int n = 0; n < nsteps; ++n) {
+            const double t0 = h->t;
+            for (int s = 0; s < 5; ++s) h->call_stage_t.push_back(t0 + Lsrk45::c[s] * dt);
+            CUDA_TRY(h, cudaGraphLaunch(h->graph_exec, h->stream));
+            h->launches += 11;
+            h->t = t0 + dt;
+        }
+        // later individually launched stages must see a zero step counter
+        CUDA_TRY(h, cudaMemsetAsync(&h->err->step_ctr, 0, sizeof(unsigned long long), h->stream));
+        if (sync) return check_errors(h);
+        return SWEDG_OK;
+    }
+    h->call_stage0 = h->next_stage;
     for (int n = 0; n < nsteps; ++n) {
         const double t0 = h->t;
         for (int s = 0; s < 5; ++s) {
@@ -910,6 +981,12 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
         h->t = t0 + dt;
     }
     if (sync) return check_errors(h);
+    return SWEDG_OK;
+}
+
+int swedg_set_graphs(swedg_handle h, int on) {
+    if (!h) return SWEDG_ERR_INVALID;
+    h->use_graphs = on != 0;
     return SWEDG_OK;
 }
 

@@ -180,3 +180,32 @@ def test_oracle_agrees_with_gpu_on_perturbed_state():
     np.testing.assert_array_equal(h.rhs(u), ref)
     h.set_mode(capi.MODE_FAST)
     assert rel(h.rhs(u), ref) <= RHS_TOL
+
+
+def test_graph_replay_equals_individual_launches_and_reports_step():
+    """swedg_step_lsrk45 with nsteps >= 2 replays a captured one-step CUDA graph: bitwise
+    equal to individually launched steps; an error in a later step is attributed to the
+    right element and stage time."""
+    c = load_golden("c1_vortex")
+    dt = float(c["dt"][0])
+    h1 = make(c, capi.MODE_FAST)
+    h1.set_graphs(False)
+    h1.set_state(c["u"])
+    h1.step(dt, 6)
+    u1, r1, t1 = h1.get_state()
+    h2 = make(c, capi.MODE_FAST)
+    h2.set_state(c["u"])
+    h2.step(dt, 3)
+    h2.step(dt, 3)
+    u2, r2, t2 = h2.get_state()
+    np.testing.assert_array_equal(u1, u2)
+    np.testing.assert_array_equal(r1, r2)
+    assert t1 == t2
+    # positivity failure planted in element 7: reported with element id and a stage time
+    bad = np.array(c["u"], copy=True)
+    bad[7, 0, 0] = -1.0
+    h2.set_state(bad, None, 0.25)
+    with pytest.raises(capi.PositivityError) as ei:
+        h2.step(dt, 4)
+    assert ei.value.elem == 7 and "element 7" in str(ei.value)
+    assert abs(ei.value.t - 0.25) < 1e-12
