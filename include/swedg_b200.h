@@ -18,6 +18,9 @@
  *   rhs(ops, state[, proj])                         swedg_rhs                             :237-297
  *   rhs_sbp(ops, state)                             swedg_rhs                             :369-434
  *   step_lsrk45(state, rhs_fn, dt, res)             swedg_step_lsrk45 (device-resident)  :466-484
+ *   compute_invariants(fq, geo, u, b, g, t)         swedg_compute_invariants   diagnostics.hpp:237-267
+ *   l2_error(fq, geo, u, exact | ref_state, t)      swedg_l2_error             diagnostics.hpp:176-226
+ *   run(Case&) time loop + invariant sampling       swedg_run                  run.hpp:226-262
  *   exceptions (solver.hpp:176-180,288-290,468)     status codes + swedg_last_error
  *
  * Conventions
@@ -46,7 +49,7 @@
 extern "C" {
 #endif
 
-#define SWEDG_ABI_VERSION 2
+#define SWEDG_ABI_VERSION 3
 
 /* status codes */
 #define SWEDG_OK 0
@@ -159,6 +162,59 @@ int swedg_check(swedg_handle h);
 /* Bathymetry products of swedg_set_bathymetry, copied to host (testing):
  * b_stacked[K][nq+nf] (hybridized only, may be NULL), src[K][2][nq+nf] (SBP: [K][2][nq]). */
 int swedg_debug_bathymetry(swedg_handle h, double* b_stacked, double* src);
+
+/* ---- diagnostics on the device (diagnostics.hpp:142-267) ------------------
+ * FineQuad evaluations of the resident (or a host) state.  Every per-point term
+ * is computed in the reference's operation order (bit-for-bit the reference's
+ * terms, except the exact-solution values of SWEDG_DIAG_L2_VORTEX/LAKE, which
+ * use CUDA's exp/sincos); the sums are EXACT: fixed-point integer accumulators,
+ * rounded once to nearest — independent of launch shape and of the number of
+ * ranks, and within the reference's own serial-summation rounding of its result. */
+#define SWEDG_DIAG_INVARIANTS 0 /* compute_invariants (diagnostics.hpp:237-267) */
+#define SWEDG_DIAG_L2_REF 1     /* l2_error vs a discrete modal state (diagnostics.hpp:205-226) */
+#define SWEDG_DIAG_L2_VORTEX 2  /* l2_error vs vortex_exact (diagnostics.hpp:41-53, 176-202) */
+#define SWEDG_DIAG_L2_LAKE 3    /* l2_error vs the lake-at-rest state (run.hpp:125-127) */
+
+typedef struct {
+    int nfine;                /* FineQuad(N).rule.size(): volume_rule_by_degree(2N+2) */
+    const double* w;          /* [nfine] rule weights */
+    const double* V;          /* nfine x Np column-major: FineQuad::V */
+    const double* Vr;         /* nfine x Np: FineQuad::Vx (d/dr) */
+    const double* Vs;         /* nfine x Np: FineQuad::Vy (d/ds) */
+    const double* map_coeffs; /* [K][2][Np]: ElemGeom::map_coeffs (Np x 2 column-major per element) */
+    const double* Pq;         /* SBP: RefOperators::Pq (Np x nq) for project_nodal; hybridized: NULL */
+} swedg_diag_desc;
+
+int swedg_set_diagnostics(swedg_handle h, const swedg_diag_desc* d);
+/* compute_invariants of u (host state in the scheme's layout; NULL = resident
+ * state at the handle's t) with the bathymetry of swedg_set_bathymetry (SBP:
+ * projected, Case::modal_bathymetry).  out[6] = {t, mass, momentum_x,
+ * momentum_y, entropy, min_h} (Invariants).  h <= 0 at a fine point fails with
+ * SWEDG_ERR_POSITIVITY (entropy() -> check_positive).  Syncs. */
+int swedg_compute_invariants(swedg_handle h, const double* u, double t, double* out);
+/* l2_error of u (NULL = resident) for what = SWEDG_DIAG_L2_*: aux = u_ref
+ * [K][3][Np] (L2_REF), VortexParams {h_inf,u_inf,v_inf,beta,g,xc,yc} (L2_VORTEX),
+ * NULL (L2_LAKE).  out[4] = {err_h, err_hu, err_hv, combined} (ErrorReport).  Syncs. */
+int swedg_l2_error(swedg_handle h, int what, const double* u, const double* aux, double t, double* out);
+/* Raw exact accumulators (multi-rank): one record of swedg_diag_raw_bytes()
+ * bytes; swedg_diag_from_raw merges raw[nranks][n] records exactly (rank-count
+ * independent, bitwise) and finishes them to out[n][6] (l2: first 4 used). */
+size_t swedg_diag_raw_bytes(void);
+int swedg_diag_raw(swedg_handle h, int what, const double* u, const double* aux, double t, void* raw);
+int swedg_diag_from_raw(const void* raw, int nranks, int n, double* out);
+/* Run-loop sampling without host syncs: invariants of the resident state at
+ * the handle's t into device slot `slot`; read back n slots as out[n][6]. */
+int swedg_sample_invariants(swedg_handle h, int slot);
+int swedg_read_invariants(swedg_handle h, int n, double* out);
+int swedg_read_invariants_raw(swedg_handle h, int n, void* raw);
+/* run() (run.hpp:226-262) on the resident state: nsteps = ceil(tfinal/dt - 1e-12),
+ * step_dt = min(dt, tfinal - t), invariants sampled at the start, every
+ * sample_every steps (0 = max(1, nsteps/100)) and at the last step, into
+ * series[max_samples][6].  One host sync at the end. */
+int swedg_run(swedg_handle h, double dt, double tfinal, int sample_every, int max_samples, double* series,
+              int* nsamples, int* nsteps_done);
+/* Host reference of the exact accumulator: *out = correctly rounded sum of x[0..n). */
+int swedg_exact_sum(const double* x, size_t n, double* out);
 
 /* ---- errors ----------------------------------------------------------------- */
 /* Last failure: status code, element id (or -1), stage time, message. */

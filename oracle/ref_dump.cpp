@@ -280,6 +280,25 @@ int cmd_modal(const std::string& path, int N, int n, double warp, bool periodic,
     return 0;
 }
 
+// compute_invariants and both l2_error forms of the case's current state, the
+// way run() calls them (run.hpp:236-238, 264-270).
+void dump_diagnostics(Writer& w, const Case& c, const FineQuad& fq, const std::string& p) {
+    Invariants inv = compute_invariants(fq, c.geo, c.modal_solution(), c.modal_bathymetry(), c.cfg.g, c.time());
+    double iv[6] = {inv.t, inv.mass, inv.momentum_x, inv.momentum_y, inv.entropy, inv.min_h};
+    w.f64(p + "invariants", {6}, iv);
+    if (!c.ref_state.empty()) {
+        ErrorReport e = l2_error(fq, c.geo, c.modal_solution(), c.ref_state);
+        double ev[4] = {e.err_h, e.err_hu, e.err_hv, e.combined};
+        w.f64(p + "l2_ref", {4}, ev);
+        w.mats(p + "ref_state", c.ref_state);
+    }
+    if (c.exact) {
+        ErrorReport e = l2_error(fq, c.geo, c.modal_solution(), c.exact, c.time());
+        double ev[4] = {e.err_h, e.err_hu, e.err_hv, e.combined};
+        w.f64(p + "l2_exact", {4}, ev);
+    }
+}
+
 // Named reference problems through run.hpp's builders and run() loop.
 int cmd_problem(const std::string& path, const std::string& problem, int N,
                 const std::string& scheme, int n, double warp, double cfl, double tfinal,
@@ -348,6 +367,18 @@ int cmd_problem(const std::string& path, const std::string& problem, int N,
         w.mats("du_ec", du_ec);
         c.sops.penalty = Penalty::LaxFriedrichs;
     }
+    // diagnostics inputs and outputs (diagnostics.hpp:142-267) on the initial state
+    FineQuad fq(N);
+    w.vec("fine_w", fq.rule.w);
+    w.mat("fine_V", fq.V);
+    w.mat("fine_Vr", fq.Vx);
+    w.mat("fine_Vs", fq.Vy);
+    {
+        std::vector<Mat> mc;
+        for (auto& e : c.geo.elems) mc.push_back(e.map_coeffs);
+        w.mats("map_coeffs", mc);
+    }
+    dump_diagnostics(w, c, fq, "diag0_");
     if (tfinal > 0) {
         RunResult r = run(c);
         w.iscalar("run_steps", r.steps);
@@ -362,6 +393,10 @@ int cmd_problem(const std::string& path, const std::string& problem, int N,
             w.mats("u_final", c.hstate.u);
         else
             w.mats("u_final", c.nstate.u);
+        w.scalar("run_err_h", r.has_error ? r.error.err_h : -1.0);
+        w.scalar("run_err_hu", r.has_error ? r.error.err_hu : -1.0);
+        w.scalar("run_err_hv", r.has_error ? r.error.err_hv : -1.0);
+        dump_diagnostics(w, c, fq, "diag1_");
     }
     return 0;
 }

@@ -35,6 +35,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#ifndef M_PI /* glibc's value (c11 mode hides it) */
+#define M_PI 3.14159265358979323846
+#endif
+
 /* Internal arithmetic type.  Built twice: real = double (the reference's own
  * arithmetic, liboracle.so) and real = long double (-DORACLE_LONG_DOUBLE, x87 80-bit, liboracle_ld.so)
  * — the latter is the accuracy yardstick for the FAST kernels: on
@@ -519,4 +523,125 @@ int oracle_step_lsrk45(const oracle_ops *op, double *u, double *res, real dt, in
     free(du);
     free(proj);
     return err;
+}
+
+/* ---- diagnostics (diagnostics.hpp:142-267, run.hpp:65-68) -----------------
+ * Always double arithmetic (the terms are compared bit-for-bit).
+ *
+ * project_nodal (diagnostics.hpp:226-230): u_modal[k] = Pq * u_nodal[k],
+ * k-ascending dot products.  Pq is Np x nq column-major. */
+void oracle_project_nodal(int K, int Np, int nq, int ncol, const double *Pq, const double *u_nodal,
+                          double *u_modal) {
+    for (int k = 0; k < K; ++k)
+        for (int c = 0; c < ncol; ++c)
+            for (int n = 0; n < Np; ++n) {
+                double s = 0.0;
+                for (int q = 0; q < nq; ++q)
+                    s += Pq[n + (size_t)q * Np] * u_nodal[((size_t)k * ncol + c) * nq + q];
+                u_modal[((size_t)k * ncol + c) * Np + n] = s;
+            }
+}
+
+/* vortex_exact (diagnostics.hpp:41-53); p = VortexParams {h_inf, u_inf, v_inf,
+ * beta, g, xc, yc} */
+static void vortex_exact(const double *p, double x, double y, double t, double *ue) {
+    double xt = x - p[5] - p[1] * t;
+    double yt = y - p[6] - p[2] * t;
+    double r2 = xt * xt + yt * yt;
+    double e = exp(-(r2 - 1.0));
+    double h = p[0] - p[3] * p[3] / (32.0 * M_PI * M_PI) * e * e;
+    double uu = p[1] - p[3] / (2.0 * M_PI) * e * yt;
+    double vv = p[2] + p[3] / (2.0 * M_PI) * e * xt;
+    ue[0] = h;
+    ue[1] = h * uu;
+    ue[2] = h * vv;
+}
+
+/* Terms of compute_invariants (what = 0: wJ*h, wJ*hu, wJ*hv, wJ*entropy),
+ * l2_error vs a discrete state (what = 1: wJ*d*d per component), vs the
+ * vortex (what = 2) or vs the lake-at-rest state (what = 3), in the reference's accumulation order (element k, then
+ * fine point i).  FineQuad::element_geometry (diagnostics.hpp:155-165) gives
+ * xy = V*map, J = dr0*ds1 - ds0*dr1 with dr = Vr*map, ds = Vs*map.
+ *   u, u_ref [K][3][Np] modal; b [K][Np] modal; map [K][2][Np];
+ *   V, Vr, Vs nfine x Np column-major; w [nfine].
+ * Outputs (any may be NULL): terms [K][nfine][4], sums[4] = the reference's
+ * serial sums, *min_h.  Returns 0, ORACLE_ERR_POSITIVITY (h <= 0 at a fine
+ * point, entropy() -> check_positive, swe.hpp:47-48) or 3 (J <= 0), element
+ * in *bad_elem. */
+int oracle_diag(int K, int Np, int nfine, const double *w, const double *V, const double *Vr,
+                const double *Vs, const double *map, const double *u, const double *b,
+                const double *u_ref, const double *vortex, double t, double g, int what,
+                double *terms, double *sums, double *min_h, long *bad_elem) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    double mh = 1e300;
+    for (long k = 0; k < K; ++k) {
+        const double *mk = map + (size_t)k * 2 * Np;
+        const double *uk = u + (size_t)k * 3 * Np;
+        double dk[3 * 64];
+        if (what == 1) /* u_modal[k] - ref_modal[k] (diagnostics.hpp:210) */
+            for (int x = 0; x < 3 * Np; ++x) dk[x] = uk[x] - u_ref[(size_t)k * 3 * Np + x];
+        for (int i = 0; i < nfine; ++i) {
+            double xy[2], dr[2], ds[2];
+            for (int c = 0; c < 2; ++c) {
+                double a = 0.0, r = 0.0, q = 0.0;
+                for (int n = 0; n < Np; ++n) a += V[i + (size_t)n * nfine] * mk[c * Np + n];
+                for (int n = 0; n < Np; ++n) r += Vr[i + (size_t)n * nfine] * mk[c * Np + n];
+                for (int n = 0; n < Np; ++n) q += Vs[i + (size_t)n * nfine] * mk[c * Np + n];
+                xy[c] = a;
+                dr[c] = r;
+                ds[c] = q;
+            }
+            double J = dr[0] * ds[1] - ds[0] * dr[1];
+            if (J <= 0.0) {
+                if (bad_elem) *bad_elem = k;
+                return 3;
+            }
+            double wJ = w[i] * J;
+            const double *src = what == 1 ? dk : uk;
+            double uq[3];
+            for (int c = 0; c < 3; ++c) {
+                double a = 0.0;
+                for (int n = 0; n < Np; ++n) a += V[i + (size_t)n * nfine] * src[c * Np + n];
+                uq[c] = a;
+            }
+            double tm[4] = {0.0, 0.0, 0.0, 0.0};
+            if (what == 0) {
+                double bq = 0.0;
+                for (int n = 0; n < Np; ++n) bq += V[i + (size_t)n * nfine] * b[(size_t)k * Np + n];
+                if (!(uq[0] > 0.0)) {
+                    if (bad_elem) *bad_elem = k;
+                    return ORACLE_ERR_POSITIVITY;
+                }
+                double vx = uq[1] / uq[0], vy = uq[2] / uq[0];
+                double ent = 0.5 * uq[0] * (vx * vx + vy * vy) + 0.5 * g * uq[0] * uq[0] + g * uq[0] * bq;
+                tm[0] = wJ * uq[0];
+                tm[1] = wJ * uq[1];
+                tm[2] = wJ * uq[2];
+                tm[3] = wJ * ent;
+                if (uq[0] < mh) mh = uq[0]; /* std::min(min_h, h) */
+            } else if (what == 1) {
+                for (int c = 0; c < 3; ++c) tm[c] = wJ * uq[c] * uq[c];
+            } else {
+                double ue[3];
+                if (what == 2) {
+                    vortex_exact(vortex, xy[0], xy[1], t, ue);
+                } else { /* lake at rest, build_lake_case init (run.hpp:125-127, diagnostics.hpp:55-57) */
+                    ue[0] = 2.0 - (0.1 * sin(2.0 * M_PI * xy[0]) * cos(2.0 * M_PI * xy[0]) + 0.5);
+                    ue[1] = 0.0;
+                    ue[2] = 0.0;
+                }
+                for (int c = 0; c < 3; ++c) {
+                    double d = uq[c] - ue[c];
+                    tm[c] = wJ * d * d;
+                }
+            }
+            for (int c = 0; c < 4; ++c) s[c] += tm[c];
+            if (terms)
+                for (int c = 0; c < 4; ++c) terms[((size_t)k * nfine + i) * 4 + c] = tm[c];
+        }
+    }
+    if (sums)
+        for (int c = 0; c < 4; ++c) sums[c] = s[c];
+    if (min_h) *min_h = mh;
+    return ORACLE_OK;
 }

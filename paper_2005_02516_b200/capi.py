@@ -28,6 +28,12 @@ PENALTY_EC = 0
 PENALTY_LF = 1
 MODE_FAST = 0
 MODE_PARITY = 1
+DIAG_INVARIANTS = 0
+DIAG_L2_REF = 1
+DIAG_L2_VORTEX = 2
+DIAG_L2_LAKE = 3
+VORTEX_PARAMS = (1.0, 1.0, 0.0, 5.0, 2.0, 0.0, 0.0)  # VortexParams defaults (diagnostics.hpp:30-38)
+INVARIANT_FIELDS = ("t", "mass", "momentum_x", "momentum_y", "entropy", "min_h")
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
@@ -65,8 +71,13 @@ class _Desc(C.Structure):
     ]
 
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 _lib = None
+
+
+class _DiagDesc(C.Structure):
+    _fields_ = [("nfine", C.c_int), ("w", _dp), ("V", _dp), ("Vr", _dp), ("Vs", _dp), ("map_coeffs", _dp),
+                ("Pq", _dp)]
 
 
 def lib() -> C.CDLL:
@@ -111,6 +122,17 @@ def lib() -> C.CDLL:
     L.swedg_stage_volume.argtypes = [vp, C.c_int, C.c_double]
     L.swedg_stage_surface.argtypes = [vp, C.c_int, C.c_double]
     L.swedg_trace_device_ptr.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
+    L.swedg_set_diagnostics.argtypes = [vp, C.POINTER(_DiagDesc)]
+    L.swedg_compute_invariants.argtypes = [vp, _dp, C.c_double, _dp]
+    L.swedg_l2_error.argtypes = [vp, C.c_int, _dp, _dp, C.c_double, _dp]
+    L.swedg_diag_raw_bytes.restype = C.c_size_t
+    L.swedg_diag_raw.argtypes = [vp, C.c_int, _dp, _dp, C.c_double, vp]
+    L.swedg_diag_from_raw.argtypes = [vp, C.c_int, C.c_int, _dp]
+    L.swedg_sample_invariants.argtypes = [vp, C.c_int]
+    L.swedg_read_invariants.argtypes = [vp, C.c_int, _dp]
+    L.swedg_read_invariants_raw.argtypes = [vp, C.c_int, vp]
+    L.swedg_run.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, _dp, _ip, _ip]
+    L.swedg_exact_sum.argtypes = [_dp, C.c_size_t, _dp]
     _lib = L
     return L
 
@@ -123,6 +145,9 @@ EXPORTED = [
     "swedg_launch_count", "swedg_device_bytes", "swedg_abi_version", "swedg_debug_bathymetry",
     "swedg_enable_timers", "swedg_read_timers", "swedg_probe_fp64_peak",
     "swedg_stage_volume", "swedg_stage_surface", "swedg_trace_device_ptr", "swedg_set_graphs",
+    "swedg_set_diagnostics", "swedg_compute_invariants", "swedg_l2_error", "swedg_diag_raw_bytes",
+    "swedg_diag_raw", "swedg_diag_from_raw", "swedg_sample_invariants", "swedg_read_invariants",
+    "swedg_read_invariants_raw", "swedg_run", "swedg_exact_sum",
 ]
 
 
@@ -321,6 +346,70 @@ class Handle:
     def rhs_device(self, u_ptr: int, du_ptr: int, t: float = 0.0):
         self._check(self._lib.swedg_rhs_device(self._h, C.c_void_p(u_ptr), C.c_void_p(du_ptr), float(t)))
 
+    # -- diagnostics (diagnostics.hpp:142-267, run.hpp:226-262) -----------------
+    def set_diagnostics(self, *, w, V, Vr, Vs, map_coeffs, Pq=None):
+        """FineQuad arrays (V/Vr/Vs as [Np][nfine] = column-major nfine x Np) and the
+        per-element mapping coefficients [K][2][Np]; Pq for SBP (project_nodal)."""
+        keep = [_f64(a) for a in (w, V, Vr, Vs, map_coeffs)] + ([_f64(Pq)] if Pq is not None else [])
+        d = _DiagDesc()
+        d.nfine = int(keep[0].shape[0])
+        d.w, d.V, d.Vr, d.Vs, d.map_coeffs = (_p(a) for a in keep[:5])
+        d.Pq = _p(keep[5]) if Pq is not None else None
+        self._check(self._lib.swedg_set_diagnostics(self._h, C.byref(d)))
+
+    def compute_invariants(self, u=None, t: float = 0.0) -> dict:
+        """Invariants of u (None = the resident state at the handle's time)."""
+        out = np.zeros(6)
+        ua = None if u is None else _f64(u)
+        self._check(self._lib.swedg_compute_invariants(self._h, _p(ua), float(t), _p(out)))
+        return dict(zip(INVARIANT_FIELDS, out.tolist()))
+
+    def l2_error(self, what: int, u=None, aux=None, t: float = 0.0) -> np.ndarray:
+        """{err_h, err_hu, err_hv, combined}; aux = u_ref (DIAG_L2_REF) or VortexParams."""
+        out = np.zeros(4)
+        ua = None if u is None else _f64(u)
+        if what == DIAG_L2_VORTEX and aux is None:
+            aux = VORTEX_PARAMS
+        xa = None if aux is None else _f64(aux)
+        self._check(self._lib.swedg_l2_error(self._h, int(what), _p(ua), _p(xa), float(t), _p(out)))
+        return out
+
+    def diag_raw(self, what: int, u=None, aux=None, t: float = 0.0) -> bytes:
+        """Raw exact accumulators of one diagnostic (merge ranks with diag_from_raw)."""
+        buf = C.create_string_buffer(diag_raw_bytes())
+        ua = None if u is None else _f64(u)
+        if what == DIAG_L2_VORTEX and aux is None:
+            aux = VORTEX_PARAMS
+        xa = None if aux is None else _f64(aux)
+        self._check(self._lib.swedg_diag_raw(self._h, int(what), _p(ua), _p(xa), float(t), buf))
+        return buf.raw
+
+    def sample_invariants(self, slot: int):
+        self._check(self._lib.swedg_sample_invariants(self._h, int(slot)))
+
+    def read_invariants(self, n: int) -> np.ndarray:
+        out = np.zeros((n, 6))
+        self._check(self._lib.swedg_read_invariants(self._h, int(n), _p(out)))
+        return out
+
+    def read_invariants_raw(self, n: int) -> bytes:
+        buf = C.create_string_buffer(max(1, n * diag_raw_bytes()))
+        self._check(self._lib.swedg_read_invariants_raw(self._h, int(n), buf))
+        return buf.raw[: n * diag_raw_bytes()]
+
+    def run(self, dt: float, tfinal: float, sample_every: int = 0, max_samples: int | None = None):
+        """run() (run.hpp:226-262) on the resident state: returns (series [n][6], steps)."""
+        nsteps = int(np.ceil(tfinal / dt - 1e-12)) if tfinal > 0 else 0
+        if max_samples is None:
+            cad = sample_every if sample_every > 0 else max(1, nsteps // 100)
+            max_samples = nsteps // cad + 2
+        series = np.zeros((max_samples, 6))
+        ns = C.c_int()
+        done = C.c_int()
+        self._check(self._lib.swedg_run(self._h, float(dt), float(tfinal), int(sample_every), int(max_samples),
+                                        _p(series), C.byref(ns), C.byref(done)))
+        return series[: ns.value], done.value
+
     @property
     def launches(self) -> int:
         return int(self._lib.swedg_launch_count(self._h))
@@ -337,6 +426,35 @@ def probe_fp64_peak(device: int = 0, reps: int = 5) -> float:
     if rc != SWEDG_OK:
         raise SwedgError(rc, "fp64 peak probe failed")
     return t.value
+
+
+def diag_raw_bytes() -> int:
+    return int(lib().swedg_diag_raw_bytes())
+
+
+def diag_from_raw(raws, n: int = 1) -> np.ndarray:
+    """Merge raw records of several ranks ([rank][n] concatenated bytes) exactly and
+    finish them: out [n][6]."""
+    if isinstance(raws, (list, tuple)):
+        raws = b"".join(raws)
+    nb = diag_raw_bytes()
+    nranks = len(raws) // (nb * n)
+    out = np.zeros((n, 6))
+    buf = C.create_string_buffer(raws, len(raws))
+    rc = lib().swedg_diag_from_raw(buf, nranks, n, _p(out))
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, "swedg_diag_from_raw failed")
+    return out
+
+
+def exact_sum(x) -> float:
+    """Host reference of the device's exact accumulator (correctly rounded sum)."""
+    x = _f64(np.ravel(x))
+    out = C.c_double()
+    rc = lib().swedg_exact_sum(_p(x), x.size, C.byref(out))
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, "exact_sum: non-finite input")
+    return out.value
 
 
 def _err_class(rc: int):
@@ -363,6 +481,9 @@ def handle_from_case(c: dict, *, penalty: int = PENALTY_LF, mode: int = MODE_FAS
     h = Handle(**kw)
     if set_bathymetry:
         h.set_bathymetry(c["b"])
+    if "fine_w" in c and "map_coeffs" in c:
+        h.set_diagnostics(w=c["fine_w"], V=c["fine_V"], Vr=c["fine_Vr"], Vs=c["fine_Vs"],
+                          map_coeffs=c["map_coeffs"], Pq=c["ref_Pq"] if scheme == SCHEME_SBP else None)
     return h
 
 
@@ -454,9 +575,21 @@ class Case:
     def b(self) -> np.ndarray:
         return self.array("b").reshape(self.K, self.nstate)
 
-    def handle(self, *, penalty=PENALTY_LF, mode=MODE_FAST, device=0, set_bathymetry=True) -> "Handle":
-        return Handle.from_desc(self.desc, self, penalty=penalty, mode=mode, device=device,
-                                b=self.b() if set_bathymetry else None)
+    def handle(self, *, penalty=PENALTY_LF, mode=MODE_FAST, device=0, set_bathymetry=True,
+               diagnostics=True) -> "Handle":
+        h = Handle.from_desc(self.desc, self, penalty=penalty, mode=mode, device=device,
+                             b=self.b() if set_bathymetry else None)
+        if diagnostics:
+            h.set_diagnostics(**self.diag_arrays())
+        return h
+
+    def diag_arrays(self) -> dict:
+        """FineQuad(N) operators and mapping coefficients (diagnostics.hpp:142-165)."""
+        d = dict(w=self.array("fine_w"), V=self.array("fine_V"), Vr=self.array("fine_Vr"),
+                 Vs=self.array("fine_Vs"), map_coeffs=self.array("map_coeffs"))
+        if self.scheme == SCHEME_SBP:
+            d["Pq"] = self.array("Pq")
+        return d
 
     def close(self):
         if getattr(self, "_c", None):

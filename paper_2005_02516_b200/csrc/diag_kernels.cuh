@@ -1,0 +1,261 @@
+// Device diagnostics: compute_invariants and l2_error on the fine rule
+// (diagnostics.hpp:142-267), the callers on either side of the time loop
+// (run.hpp:236-270).  Not a hot path: a sample costs about one RK stage of
+// HBM traffic and runs every ~1% of the steps.
+//
+// One warp per element.  The warp stages the element's coefficients in shared
+// memory (SBP: projects the nodal state first, project_nodal,
+// diagnostics.hpp:226-230), then each lane evaluates fine points lane, lane+32:
+// the mapping (FineQuad::element_geometry, :155-165), the modal state and the
+// per-point terms, in the reference's operation order with no FMA contraction,
+// so every term is bit-for-bit the reference's.  The terms are summed exactly
+// (exact_sum.h): per-block fixed-point limbs in shared memory, merged into the
+// output record with integer atomics, rounded once on the host.
+#pragma once
+
+#include "exact_sum.h"
+#include "swedg_common.cuh"
+
+namespace swedg {
+
+enum DiagWhat { kDiagInvariants = 0, kDiagL2Ref = 1, kDiagL2Vortex = 2, kDiagL2Lake = 3 };
+
+// Raw device record of one diagnostic evaluation (layout shared with the host,
+// swedg_capi.cu; exported opaque through the C ABI for multi-rank merging).
+struct DiagRec {
+    long long limbs[4][exact::kLimbs];  // exact sums: invariants (mass, mx, my, entropy) / l2 (s0, s1, s2, -)
+    unsigned long long min_key;         // order-preserving key of min h (invariants)
+    unsigned long long bad;             // min over (element << 1 | kind): kind 0 = J <= 0, 1 = h <= 0; ~0 = none
+    unsigned int nonfinite;             // bit q: a non-finite term entered sum q
+    unsigned int what;
+    double t;
+};
+
+__host__ __device__ inline unsigned long long order_key(double x) {
+#ifdef __CUDA_ARCH__
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+#else
+    unsigned long long b;
+    __builtin_memcpy(&b, &x, 8);
+#endif
+    return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+inline double key_value(unsigned long long k) {
+    unsigned long long b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+    double x;
+    __builtin_memcpy(&x, &b, 8);
+    return x;
+}
+
+struct DiagParams {
+    int K, nfine, what, sbp, nq;
+    double g, t;
+    const double* fine;  // w[nfine] | V | Vr | Vs  (nfine x Np column-major each)
+    const double* Pq;    // SBP: Np x nq column-major
+    const double* map;   // [K][2][Np]
+    const double* u;     // [K][3][Np] modal, or SBP nodal [K][3][nq]
+    const double* b;     // invariants: [K][Np] modal, or SBP nodal [K][nq]
+    const double* uref;  // l2 vs discrete state: [K][3][Np] modal
+    double vortex[7];    // VortexParams {h_inf, u_inf, v_inf, beta, g, xc, yc}
+    DiagRec* rec;
+};
+
+__global__ void diag_init_kernel(DiagRec* r, double t, int what) {
+    long long* L = &r->limbs[0][0];
+    for (int i = threadIdx.x; i < 4 * exact::kLimbs; i += blockDim.x) L[i] = 0;
+    if (threadIdx.x == 0) {
+        r->min_key = order_key(1e300);  // Invariants::min_h starts at 1e300 (diagnostics.hpp:244)
+        r->bad = ~0ull;
+        r->nonfinite = 0;
+        r->what = (unsigned)what;
+        r->t = t;
+    }
+}
+
+constexpr int kDiagWarps = 4;
+
+template <int N>
+struct DiagDims {
+    static constexpr int Np = (N + 1) * (N + 2) / 2;
+    static constexpr int nq_max = 64;  // SBP nodes staged (N <= 4: 37)
+    // per-warp staging: u (3 Np), b (Np), map (2 Np), nodal (4 nq_max)
+    static constexpr int warp_doubles = 6 * Np + 4 * nq_max;
+};
+
+__device__ __forceinline__ void acc_add(long long* L, double x) {
+    int j;
+    int64_t d0, d1, d2;
+    if (!exact::split(x, j, d0, d1, d2)) return;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&L[j]), static_cast<unsigned long long>(d0));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&L[j + 1]), static_cast<unsigned long long>(d1));
+    if (d2) atomicAdd(reinterpret_cast<unsigned long long*>(&L[j + 2]), static_cast<unsigned long long>(d2));
+}
+
+// vortex_exact (diagnostics.hpp:41-53).  exp is CUDA's (<= 1 ulp), not glibc's:
+// the exact-solution terms are within rounding of the reference's, not bitwise.
+__device__ __forceinline__ void vortex_exact_dev(const double* p, double x, double y, double t, double* ue) {
+    const double pi = 3.14159265358979323846;
+    double xt = __dsub_rn(__dsub_rn(x, p[5]), __dmul_rn(p[1], t));
+    double yt = __dsub_rn(__dsub_rn(y, p[6]), __dmul_rn(p[2], t));
+    double r2 = __dadd_rn(__dmul_rn(xt, xt), __dmul_rn(yt, yt));
+    double e = exp(-__dsub_rn(r2, 1.0));
+    double c1 = __ddiv_rn(__dmul_rn(p[3], p[3]), __dmul_rn(__dmul_rn(32.0, pi), pi));
+    double h = __dsub_rn(p[0], __dmul_rn(__dmul_rn(c1, e), e));
+    double c2 = __ddiv_rn(p[3], __dmul_rn(2.0, pi));
+    double uu = __dsub_rn(p[1], __dmul_rn(__dmul_rn(c2, e), yt));
+    double vv = __dadd_rn(p[2], __dmul_rn(__dmul_rn(c2, e), xt));
+    ue[0] = h;
+    ue[1] = __dmul_rn(h, uu);
+    ue[2] = __dmul_rn(h, vv);
+}
+
+template <int N>
+__global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
+    using D = DiagDims<N>;
+    constexpr int Np = D::Np;
+    __shared__ long long acc[4][exact::kLimbs];
+    __shared__ double stage[kDiagWarps][D::warp_doubles];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 4 * exact::kLimbs; i += blockDim.x) (&acc[0][0])[i] = 0;
+    __syncthreads();
+
+    double* su = stage[wid];       // [3][Np] modal state (or u - u_ref)
+    double* sb = su + 3 * Np;      // [Np] modal bathymetry
+    double* sm = sb + Np;          // [2][Np] map coefficients
+    double* sn = sm + 2 * Np;      // SBP nodal staging [4][nq]
+    const int nfine = P.nfine, nq = P.nq;
+    const double* W = P.fine;
+    const double* V = W + nfine;
+    const double* Vr = V + (size_t)nfine * Np;
+    const double* Vs = Vr + (size_t)nfine * Np;
+    const bool inv = P.what == kDiagInvariants;
+    unsigned long long kmin = order_key(1e300), kbad = ~0ull;
+    unsigned nonfinite = 0;
+
+    for (long k = (long)blockIdx.x * kDiagWarps + wid; k < P.K; k += (long)gridDim.x * kDiagWarps) {
+        // ---- stage the element
+        for (int x = lane; x < 2 * Np; x += 32) sm[x] = P.map[(size_t)k * 2 * Np + x];
+        if (P.sbp) {
+            for (int x = lane; x < 3 * nq; x += 32) sn[x] = P.u[(size_t)k * 3 * nq + x];
+            if (inv)
+                for (int x = lane; x < nq; x += 32) sn[3 * nq + x] = P.b[(size_t)k * nq + x];
+            __syncwarp();
+            // project_nodal: (Pq u)(n, c) = sum_q Pq(n, q) u(q, c), q ascending
+            const int ncol = inv ? 4 : 3;
+            for (int x = lane; x < ncol * Np; x += 32) {
+                const int c = x / Np, n = x - c * Np;
+                double s = 0.0;
+                for (int q = 0; q < nq; ++q) s = __dadd_rn(s, __dmul_rn(P.Pq[n + (size_t)q * Np], sn[c * nq + q]));
+                su[x] = s;  // c = 3 lands in sb (= su + 3 Np)
+            }
+        } else {
+            for (int x = lane; x < 3 * Np; x += 32) su[x] = P.u[(size_t)k * 3 * Np + x];
+            if (inv)
+                for (int x = lane; x < Np; x += 32) sb[x] = P.b[(size_t)k * Np + x];
+        }
+        __syncwarp();
+        if (P.what == kDiagL2Ref) {  // u_modal[k] - ref_modal[k] (diagnostics.hpp:210)
+            for (int x = lane; x < 3 * Np; x += 32) su[x] = __dsub_rn(su[x], P.uref[(size_t)k * 3 * Np + x]);
+            __syncwarp();
+        }
+        // ---- fine points
+        for (int i = lane; i < nfine; i += 32) {
+            double xy[2], dr[2], ds[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                double a = 0.0, r = 0.0, q = 0.0;
+                for (int n = 0; n < Np; ++n) a = __dadd_rn(a, __dmul_rn(__ldg(V + i + (size_t)n * nfine), sm[c * Np + n]));
+                for (int n = 0; n < Np; ++n) r = __dadd_rn(r, __dmul_rn(__ldg(Vr + i + (size_t)n * nfine), sm[c * Np + n]));
+                for (int n = 0; n < Np; ++n) q = __dadd_rn(q, __dmul_rn(__ldg(Vs + i + (size_t)n * nfine), sm[c * Np + n]));
+                xy[c] = a;
+                dr[c] = r;
+                ds[c] = q;
+            }
+            const double J = __dsub_rn(__dmul_rn(dr[0], ds[1]), __dmul_rn(ds[0], dr[1]));
+            if (J <= 0.0) {  // "nonpositive Jacobian at fine point" (diagnostics.hpp:162)
+                kbad = min(kbad, (unsigned long long)k << 1);
+                continue;
+            }
+            const double wJ = __dmul_rn(__ldg(W + i), J);
+            double uq[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double a = 0.0;
+                for (int n = 0; n < Np; ++n) a = __dadd_rn(a, __dmul_rn(__ldg(V + i + (size_t)n * nfine), su[c * Np + n]));
+                uq[c] = a;
+            }
+            double tm[4];
+            int nt = 3;
+            if (inv) {
+                double bq = 0.0;
+                for (int n = 0; n < Np; ++n) bq = __dadd_rn(bq, __dmul_rn(__ldg(V + i + (size_t)n * nfine), sb[n]));
+                if (!(uq[0] > 0.0)) {  // entropy() -> check_positive (swe.hpp:47-48)
+                    kbad = min(kbad, ((unsigned long long)k << 1) | 1ull);
+                    continue;
+                }
+                const double h = uq[0];
+                const double vx = __ddiv_rn(uq[1], h), vy = __ddiv_rn(uq[2], h);
+                // 0.5 h (vx^2 + vy^2) + 0.5 g h h + g h b   (swe.hpp:50)
+                double ent = __dmul_rn(__dmul_rn(0.5, h), __dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
+                ent = __dadd_rn(ent, __dmul_rn(__dmul_rn(__dmul_rn(0.5, P.g), h), h));
+                ent = __dadd_rn(ent, __dmul_rn(__dmul_rn(P.g, h), bq));
+                tm[0] = __dmul_rn(wJ, h);
+                tm[1] = __dmul_rn(wJ, uq[1]);
+                tm[2] = __dmul_rn(wJ, uq[2]);
+                tm[3] = __dmul_rn(wJ, ent);
+                nt = 4;
+                kmin = min(kmin, order_key(h));
+            } else if (P.what == kDiagL2Ref) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) tm[c] = __dmul_rn(__dmul_rn(wJ, uq[c]), uq[c]);
+            } else {
+                double ue[3];
+                if (P.what == kDiagL2Vortex) {
+                    vortex_exact_dev(P.vortex, xy[0], xy[1], P.t, ue);
+                } else {  // lake at rest: (2 - lake_bathymetry(x), 0, 0) (run.hpp:125-127)
+                    const double a = __dmul_rn(__dmul_rn(2.0, 3.14159265358979323846), xy[0]);
+                    double sn_, cs_;
+                    sincos(a, &sn_, &cs_);
+                    ue[0] = __dsub_rn(2.0, __dadd_rn(__dmul_rn(__dmul_rn(0.1, sn_), cs_), 0.5));
+                    ue[1] = 0.0;
+                    ue[2] = 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double d = __dsub_rn(uq[c], ue[c]);
+                    tm[c] = __dmul_rn(__dmul_rn(wJ, d), d);
+                }
+            }
+            for (int q = 0; q < nt; ++q) {
+                if (!isfinite(tm[q])) {
+                    nonfinite |= 1u << q;
+                    continue;
+                }
+                acc_add(acc[q], tm[q]);
+            }
+        }
+        __syncwarp();
+    }
+    // ---- merge: warp minima, then block limbs -> record (integer adds: exact)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kbad = min(kbad, __shfl_xor_sync(0xffffffffu, kbad, o));
+        nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o);
+    }
+    if (lane == 0) {
+        if (inv) atomicMin(&P.rec->min_key, kmin);
+        if (kbad != ~0ull) atomicMin(&P.rec->bad, kbad);
+        if (nonfinite) atomicOr(&P.rec->nonfinite, nonfinite);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) exact::compact(reinterpret_cast<int64_t*>(acc[threadIdx.x]));
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * exact::kLimbs; i += blockDim.x) {
+        const long long v = (&acc[0][0])[i];
+        if (v) atomicAdd(reinterpret_cast<unsigned long long*>(&P.rec->limbs[0][0] + i), static_cast<unsigned long long>(v));
+    }
+}
+
+}  // namespace swedg

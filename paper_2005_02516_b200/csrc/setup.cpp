@@ -821,6 +821,7 @@ struct swedg_case_s {
     std::vector<double> gf, sJ, nx, ny, J_vol, Mh_inv;
     std::vector<int> nbr, nbr_face, face_type, perm;
     std::vector<double> u0, b, xy_vol, xy_surf, map_coeffs, volq_w, shift;
+    std::vector<double> fine_w, fine_V, fine_Vr, fine_Vs;  // FineQuad (diagnostics.hpp:142-153)
     bool periodic_x = true, periodic_y = true;
     int n_halo = 0;
 };
@@ -1095,6 +1096,15 @@ void build_case(swedg_case_s& c) {
         c.M_diag = c.sbp.M_diag;
         c.face_index = c.sbp.face_index;
     }
+    {  // FineQuad(N): degree-(2N+2) rule, basis and its gradients at the fine points
+        Rule2D fr = volume_rule_by_degree(2 * R.N + 2);
+        Mat fx, fy;
+        grad_vandermonde(R.N, fr.x, fr.y, fx, fy);
+        c.fine_w = fr.w;
+        c.fine_V = flat(vandermonde(R.N, fr.x, fr.y));
+        c.fine_Vr = flat(fx);
+        c.fine_Vs = flat(fy);
+    }
 
     // initial state (make_state / make_nodal_state, run.hpp builders)
     const int Np = R.Np, nq = R.nq;
@@ -1275,6 +1285,10 @@ const double* swedg_case_array(swedg_case c, const char* name, size_t* n) {
     else if (s == "ny") v = &c->ny;
     else if (s == "Mh_inv") v = &c->Mh_inv;
     else if (s == "face_shift") v = &c->shift;
+    else if (s == "fine_w") v = &c->fine_w;
+    else if (s == "fine_V") v = &c->fine_V;
+    else if (s == "fine_Vr") v = &c->fine_Vr;
+    else if (s == "fine_Vs") v = &c->fine_Vs;
     if (!v) return nullptr;
     if (n) *n = v->size();
     return v->data();

@@ -23,6 +23,7 @@
 #include "modal_quad_n4.cuh"
 #include "modal_pair_n4.cuh"
 #include "sbp_kernels.cuh"
+#include "diag_kernels.cuh"
 
 using namespace swedg;
 
@@ -70,6 +71,16 @@ struct swedg_handle_s {
     double* accf = nullptr;  // [K][3][nf]
     double* T1 = nullptr;    // [K][3][Np]
     ErrRec* err = nullptr;
+    // diagnostics (diag_kernels.cuh)
+    int nfine = 0;
+    double* fine = nullptr;    // fine rule: w | V | Vr | Vs
+    double* dPq = nullptr;     // SBP project_nodal operator (Np x nq)
+    double* map = nullptr;     // [K][2][Np] mapping coefficients
+    double* bmod = nullptr;    // bathymetry as given to swedg_set_bathymetry
+    double* uref = nullptr;    // l2_error reference state [K][3][Np]
+    DiagRec* drec = nullptr;   // one-shot record
+    DiagRec* series = nullptr; // run-loop samples
+    int series_cap = 0;
     size_t dev_bytes = 0;
     bool bathy_set = false;
     unsigned next_stage = 1;
@@ -93,9 +104,9 @@ struct swedg_handle_s {
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
     double timer_ms[2] = {0.0, 0.0};
     long long timer_n[2] = {0, 0};
-    // stage bookkeeping for error decoding (current call)
-    unsigned call_stage0 = 0;
-    std::vector<double> call_stage_t;
+    // stage time of every stage id issued since the last error check (error decoding)
+    unsigned stage_t0 = 0;
+    std::vector<double> stage_t;
     int nstate() const { return scheme == SWEDG_SCHEME_SBP ? nq : Np; }
 };
 
@@ -111,6 +122,15 @@ int fail(swedg_handle h, int code, const std::string& msg, long elem = -1, doubl
         g_create_error = msg;
     }
     return code;
+}
+
+// Allocate the next stage id and remember its stage time for error messages.
+unsigned new_stage(swedg_handle h, double t) {
+    const unsigned id = h->next_stage++;
+    if (h->stage_t.empty()) h->stage_t0 = id;
+    h->stage_t.resize(id - h->stage_t0 + 1, t);
+    h->stage_t[id - h->stage_t0] = t;
+    return id;
 }
 
 #define CUDA_TRY(h, expr)                                                                  \
@@ -444,13 +464,13 @@ int check_errors(swedg_handle h, bool projection_wrapped = true) {
     ErrRec rec;
     CUDA_TRY(h, cudaMemcpyAsync(&rec, h->err, sizeof(rec), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    const unsigned stage = (unsigned)(rec.key >> 33);
+    double t = h->t;
+    if (stage >= h->stage_t0 && stage - h->stage_t0 < h->stage_t.size()) t = h->stage_t[stage - h->stage_t0];
+    h->stage_t.clear();
     if (rec.key == kNoError) return SWEDG_OK;
-    unsigned stage = (unsigned)(rec.key >> 33);
     int kern = (int)((rec.key >> 32) & 1);
     long elem = (long)(rec.key & 0xffffffffull);
-    double t = h->t;
-    if (stage >= h->call_stage0 && stage - h->call_stage0 < h->call_stage_t.size())
-        t = h->call_stage_t[stage - h->call_stage0];
     // reset for the next call
     unsigned long long none = kNoError;
     CUDA_TRY(h, cudaMemcpyAsync(h->err, &none, sizeof(none), cudaMemcpyHostToDevice, h->stream));
@@ -472,6 +492,116 @@ int ensure_scratch(swedg_handle h) {
     size_t ns = (size_t)h->K * 3 * h->nstate();
     if (!h->utmp && dalloc(h, &h->utmp, ns)) return h->last_code;
     if (!h->du && dalloc(h, &h->du, ns)) return h->last_code;
+    return SWEDG_OK;
+}
+
+// ---- diagnostics helpers (diag_kernels.cuh) --------------------------------
+template <int N>
+void launch_diag_n(swedg_handle h, const double* u, int what, double t, const double* vortex, DiagRec* rec) {
+    diag_init_kernel<<<1, 256, 0, h->stream>>>(rec, t, what);
+    DiagParams P;
+    P.K = h->K;
+    P.nfine = h->nfine;
+    P.what = what;
+    P.sbp = h->scheme == SWEDG_SCHEME_SBP ? 1 : 0;
+    P.nq = h->nq;
+    P.g = h->g;
+    P.t = t;
+    P.fine = h->fine;
+    P.Pq = h->dPq;
+    P.map = h->map;
+    P.u = u;
+    P.b = h->bmod;
+    P.uref = h->uref;
+    for (int i = 0; i < 7; ++i) P.vortex[i] = vortex ? vortex[i] : 0.0;
+    P.rec = rec;
+    auto kern = diag_kernel<N>;
+    const int threads = 32 * kDiagWarps;
+    int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, threads, 0);
+    int grid = std::min((h->K + kDiagWarps - 1) / kDiagWarps, occ * h->nsm);
+    kern<<<std::max(grid, 1), threads, 0, h->stream>>>(P);
+    h->launches += 2;
+}
+
+int launch_diag(swedg_handle h, const double* u, int what, double t, const double* vortex, DiagRec* rec) {
+    if (!h->fine) return fail(h, SWEDG_ERR_INVALID, "diagnostics need swedg_set_diagnostics first");
+    if (what == kDiagInvariants && !h->bmod)
+        return fail(h, SWEDG_ERR_INVALID, "compute_invariants needs swedg_set_bathymetry first");
+    switch (h->N) {
+        case 1: launch_diag_n<1>(h, u, what, t, vortex, rec); break;
+        case 2: launch_diag_n<2>(h, u, what, t, vortex, rec); break;
+        case 3: launch_diag_n<3>(h, u, what, t, vortex, rec); break;
+        case 4: launch_diag_n<4>(h, u, what, t, vortex, rec); break;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("diagnostics launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+// Finish a (merged) record: exact limbs -> correctly rounded sums -> the
+// reference's Invariants / ErrorReport fields (diagnostics.hpp:196-200, 245-265).
+// out = {t, mass, momentum_x, momentum_y, entropy, min_h} or
+//       {err_h, err_hu, err_hv, combined, 0, 0}.  Returns a status; *elem set on failure.
+int finish_diag(const DiagRec& r, double* out, long* elem, std::string* msg) {
+    const unsigned long long none = ~0ull;
+    if (r.bad != none) {
+        const long k = (long)(r.bad >> 1);
+        if (elem) *elem = k;
+        if ((r.bad & 1) == 0) {
+            if (msg) *msg = "nonpositive Jacobian at fine point in element " + std::to_string(k);
+            return SWEDG_ERR_INVALID;
+        }
+        if (msg)
+            *msg = "nonpositive water height at a fine quadrature point in element " + std::to_string(k) +
+                   " (compute_invariants at t = " + std::to_string(r.t) + ")";
+        return SWEDG_ERR_POSITIVITY;
+    }
+    double s[4];
+    for (int q = 0; q < 4; ++q)
+        s[q] = (r.nonfinite >> q & 1) ? std::nan("") : exact::to_double(reinterpret_cast<const int64_t*>(r.limbs[q]));
+    if (r.what == kDiagInvariants) {
+        out[0] = r.t;
+        out[1] = s[0];
+        out[2] = s[1];
+        out[3] = s[2];
+        out[4] = s[3];
+        out[5] = key_value(r.min_key);
+    } else {
+        out[0] = std::sqrt(s[0]);
+        out[1] = std::sqrt(s[1]);
+        out[2] = std::sqrt(s[2]);
+        out[3] = std::sqrt(s[0] + s[1] + s[2]);
+        out[4] = 0.0;
+        out[5] = 0.0;
+    }
+    return SWEDG_OK;
+}
+
+// merge records of several ranks (integer limb sums: exact)
+DiagRec merge_diag(const DiagRec* recs, int nranks, int stride, int i) {
+    DiagRec m = recs[i];
+    for (int r = 1; r < nranks; ++r) {
+        const DiagRec& o = recs[(size_t)r * stride + i];
+        for (int q = 0; q < 4; ++q)
+            for (int j = 0; j < exact::kLimbs; ++j) m.limbs[q][j] += o.limbs[q][j];
+        m.min_key = std::min(m.min_key, o.min_key);
+        m.bad = std::min(m.bad, o.bad);
+        m.nonfinite |= o.nonfinite;
+    }
+    for (int q = 0; q < 4; ++q) exact::compact(reinterpret_cast<int64_t*>(m.limbs[q]));
+    return m;
+}
+
+// Stage the state argument of a diagnostics call: host u (copied to scratch)
+// or NULL = the resident state.
+int diag_state(swedg_handle h, const double* u, const double** dev) {
+    if (!u) {
+        *dev = h->u;
+        return SWEDG_OK;
+    }
+    if (ensure_scratch(h)) return h->last_code;
+    if (upload(h, h->utmp, u, (size_t)h->K * 3 * h->nstate())) return h->last_code;
+    *dev = h->utmp;
     return SWEDG_OK;
 }
 
@@ -657,8 +787,9 @@ int swedg_destroy(swedg_handle h) {
     if (!h) return SWEDG_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* ptrs[] = {h->ops, h->gf, h->surf, h->Minv, h->Mpk, h->nbr, h->perm, h->fidx, h->bs, h->src, h->u,
-                    h->res, h->utmp, h->du, h->proj, h->trace, h->accf, h->T1, h->err};
+    void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
+                    h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& p : h->ev_pending) {
@@ -782,13 +913,10 @@ int swedg_set_bathymetry(swedg_handle h, const double* b) {
     if (!h || !b) return SWEDG_ERR_INVALID;
     cudaSetDevice(h->device);
     const size_t nb = (size_t)h->K * (h->scheme == SWEDG_SCHEME_SBP ? h->nq : h->Np);
-    double* db = nullptr;
-    if (dalloc(h, &db, nb)) return h->last_code;
-    h->dev_bytes -= nb * sizeof(double);
-    if (upload(h, db, b, nb)) {
-        cudaFree(db);
-        return h->last_code;
-    }
+    // kept: compute_invariants reads the bathymetry (run.hpp:71-76)
+    if (!h->bmod && dalloc(h, &h->bmod, nb)) return h->last_code;
+    const double* db = h->bmod;
+    if (upload(h, h->bmod, b, nb)) return h->last_code;
     if (h->scheme == SWEDG_SCHEME_SBP) {
         switch (h->N) {
             case 1: launch_sbp_bathy<1>(h, db); break;
@@ -805,7 +933,6 @@ int swedg_set_bathymetry(swedg_handle h, const double* b) {
         }
     }
     cudaError_t e = cudaStreamSynchronize(h->stream);
-    cudaFree(db);
     if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("set_bathymetry: ") + cudaGetErrorString(e));
     h->bathy_set = true;
     return SWEDG_OK;
@@ -834,9 +961,8 @@ int swedg_entropy_projection(swedg_handle h, const double* u, double t, double* 
     const size_t K = h->K;
     if (!h->proj && dalloc(h, &h->proj, K * 3 * h->nh)) return h->last_code;
     if (upload(h, h->utmp, u, K * 3 * h->Np)) return h->last_code;
-    h->call_stage0 = h->next_stage;
-    h->call_stage_t.assign(1, t);
-    StageArgs sa{h->utmp, 3, h->proj, false, 0, 0, 0, h->du, h->next_stage++, false};
+    const unsigned sid = new_stage(h, t);
+    StageArgs sa{h->utmp, 3, h->proj, false, 0, 0, 0, h->du, sid, false};
     if (run_stage(h, sa)) return h->last_code;
     CUDA_TRY(h, cudaMemcpyAsync(proj, h->proj, K * 3 * h->nh * 8, cudaMemcpyDeviceToHost, h->stream));
     int rc = check_errors(h);
@@ -850,9 +976,8 @@ int swedg_rhs(swedg_handle h, const double* u, double t, double* du) {
     if (ensure_scratch(h)) return h->last_code;
     const size_t n = (size_t)h->K * 3 * h->nstate();
     if (upload(h, h->utmp, u, n)) return h->last_code;
-    h->call_stage0 = h->next_stage;
-    h->call_stage_t.assign(1, t);
-    StageArgs sa{h->utmp, 3, nullptr, false, 0, 0, 0, h->du, h->next_stage++, false};
+    const unsigned sid = new_stage(h, t);
+    StageArgs sa{h->utmp, 3, nullptr, false, 0, 0, 0, h->du, sid, false};
     if (run_stage(h, sa)) return h->last_code;
     CUDA_TRY(h, cudaMemcpyAsync(du, h->du, n * 8, cudaMemcpyDeviceToHost, h->stream));
     return check_errors(h);
@@ -862,9 +987,8 @@ int swedg_rhs_device(swedg_handle h, const double* u_dev, double* du_dev, double
     if (!h || !u_dev || !du_dev) return SWEDG_ERR_INVALID;
     cudaSetDevice(h->device);
     if (h->scheme == SWEDG_SCHEME_SBP && ensure_scratch(h)) return h->last_code;
-    h->call_stage0 = h->next_stage;
-    h->call_stage_t.assign(1, t);
-    StageArgs sa{u_dev, 3, nullptr, false, 0, 0, 0, du_dev, h->next_stage++, false};
+    const unsigned sid = new_stage(h, t);
+    StageArgs sa{u_dev, 3, nullptr, false, 0, 0, 0, du_dev, sid, false};
     return run_stage(h, sa);
 }
 
@@ -950,32 +1074,32 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
     if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
     if (nsteps < 0) return fail(h, SWEDG_ERR_INVALID, "nsteps must be >= 0");
     cudaSetDevice(h->device);
-    h->call_stage_t.clear();
     // launch-bound regime (small K): replay a captured one-step graph; per-kernel
     // timers need individual launches, so they disable the graph path
     const bool graphs = h->use_graphs && !h->timers && nsteps >= 2;
     if (graphs) {
         if (capture_step_graph(h, dt)) return h->last_code;
-        h->call_stage0 = h->graph_base;
-        CUDA_TRY(h, cudaMemsetAsync(&h->err->step_ctr, 0, sizeof(unsigned long long), h->stream));
+        // replay n, stage s reports id (first id of this call) + 5 n + s
+        const unsigned first = h->next_stage;
+        set_stage_offset_kernel<<<1, 1, 0, h->stream>>>(h->err, (unsigned long long)(first - h->graph_base));
         for (int n = 0; n < nsteps; ++n) {
             const double t0 = h->t;
-            for (int s = 0; s < 5; ++s) h->call_stage_t.push_back(t0 + Lsrk45::c[s] * dt);
+            for (int s = 0; s < 5; ++s) new_stage(h, t0 + Lsrk45::c[s] * dt);
             CUDA_TRY(h, cudaGraphLaunch(h->graph_exec, h->stream));
             h->launches += 11;
             h->t = t0 + dt;
         }
-        // later individually launched stages must see a zero step counter
-        CUDA_TRY(h, cudaMemsetAsync(&h->err->step_ctr, 0, sizeof(unsigned long long), h->stream));
+        // individually launched stages carry their own ids: offset back to 0
+        set_stage_offset_kernel<<<1, 1, 0, h->stream>>>(h->err, 0ull);
+        h->launches += 2;
         if (sync) return check_errors(h);
         return SWEDG_OK;
     }
-    h->call_stage0 = h->next_stage;
     for (int n = 0; n < nsteps; ++n) {
         const double t0 = h->t;
         for (int s = 0; s < 5; ++s) {
-            h->call_stage_t.push_back(t0 + Lsrk45::c[s] * dt);
-            StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, h->next_stage++, true};
+            const unsigned sid = new_stage(h, t0 + Lsrk45::c[s] * dt);
+            StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, sid, true};
             if (run_stage(h, sa)) return h->last_code;
         }
         h->t = t0 + dt;
@@ -996,12 +1120,7 @@ int swedg_stage_volume(swedg_handle h, int stage, double dt) {
     if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
         return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
     cudaSetDevice(h->device);
-    if (stage == 0) {
-        h->call_stage0 = h->next_stage;
-        h->call_stage_t.clear();
-    }
-    h->stage_cur = h->next_stage++;
-    h->call_stage_t.push_back(h->t + Lsrk45::c[stage] * dt);
+    h->stage_cur = new_stage(h, h->t + Lsrk45::c[stage] * dt);
     StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true};
     return run_stage(h, sa);
 }
@@ -1045,6 +1164,212 @@ int swedg_last_error(swedg_handle h, int* code, long* elem, double* t, char* msg
         std::strncpy(msg, h->last_msg.c_str(), len - 1);
         msg[len - 1] = 0;
     }
+    return SWEDG_OK;
+}
+
+// ---- diagnostics (diagnostics.hpp:142-267) ----------------------------------
+
+int swedg_set_diagnostics(swedg_handle h, const swedg_diag_desc* d) {
+    if (!h || !d) return SWEDG_ERR_INVALID;
+    if (d->nfine < 1 || !d->w || !d->V || !d->Vr || !d->Vs || !d->map_coeffs)
+        return fail(h, SWEDG_ERR_INVALID, "missing diagnostics array");
+    if (h->scheme == SWEDG_SCHEME_SBP && !d->Pq) return fail(h, SWEDG_ERR_INVALID, "SBP diagnostics need Pq");
+    if (h->scheme == SWEDG_SCHEME_SBP && h->nq > DiagDims<1>::nq_max)
+        return fail(h, SWEDG_ERR_UNSUPPORTED, "SBP node count above the diagnostics staging size");
+    cudaSetDevice(h->device);
+    const size_t Np = h->Np, nf = d->nfine, K = h->K;
+    std::vector<double> fine;
+    fine.reserve(nf * (1 + 3 * Np));
+    fine.insert(fine.end(), d->w, d->w + nf);
+    fine.insert(fine.end(), d->V, d->V + nf * Np);
+    fine.insert(fine.end(), d->Vr, d->Vr + nf * Np);
+    fine.insert(fine.end(), d->Vs, d->Vs + nf * Np);
+    if (h->fine) {
+        cudaFree(h->fine);
+        h->dev_bytes -= (size_t)h->nfine * (1 + 3 * Np) * sizeof(double);
+        h->fine = nullptr;
+    }
+    if (dalloc(h, &h->fine, fine.size()) || upload(h, h->fine, fine.data(), fine.size())) return h->last_code;
+    h->nfine = d->nfine;
+    if (!h->map && dalloc(h, &h->map, K * 2 * Np)) return h->last_code;
+    if (upload(h, h->map, d->map_coeffs, K * 2 * Np)) return h->last_code;
+    if (h->scheme == SWEDG_SCHEME_SBP) {
+        if (!h->dPq && dalloc(h, &h->dPq, Np * h->nq)) return h->last_code;
+        if (upload(h, h->dPq, d->Pq, Np * h->nq)) return h->last_code;
+    }
+    if (!h->drec && dalloc(h, &h->drec, 1)) return h->last_code;
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return SWEDG_OK;
+}
+
+size_t swedg_diag_raw_bytes(void) { return sizeof(DiagRec); }
+
+int swedg_diag_raw(swedg_handle h, int what, const double* u, const double* aux, double t, void* raw) {
+    if (!h || !raw || what < SWEDG_DIAG_INVARIANTS || what > SWEDG_DIAG_L2_LAKE) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    const double* du = nullptr;
+    if (diag_state(h, u, &du)) return h->last_code;
+    const double* vortex = nullptr;
+    if (what == SWEDG_DIAG_L2_REF) {
+        if (!aux) return fail(h, SWEDG_ERR_INVALID, "l2_error needs the reference state");
+        const size_t n = (size_t)h->K * 3 * h->Np;
+        if (!h->uref && dalloc(h, &h->uref, n)) return h->last_code;
+        if (upload(h, h->uref, aux, n)) return h->last_code;
+    } else if (what == SWEDG_DIAG_L2_VORTEX) {
+        if (!aux) return fail(h, SWEDG_ERR_INVALID, "vortex l2_error needs VortexParams");
+        vortex = aux;
+    }
+    if (!h->drec && dalloc(h, &h->drec, 1)) return h->last_code;
+    if (launch_diag(h, du, what, t, vortex, h->drec)) return h->last_code;
+    CUDA_TRY(h, cudaMemcpyAsync(raw, h->drec, sizeof(DiagRec), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return SWEDG_OK;
+}
+
+int swedg_diag_from_raw(const void* raw, int nranks, int n, double* out) {
+    if (!raw || !out || nranks < 1 || n < 0) return SWEDG_ERR_INVALID;
+    const DiagRec* recs = static_cast<const DiagRec*>(raw);
+    int rc = SWEDG_OK;
+    for (int i = 0; i < n; ++i) {
+        DiagRec m = merge_diag(recs, nranks, n, i);
+        int r = finish_diag(m, out + (size_t)i * 6, nullptr, nullptr);
+        if (r != SWEDG_OK && rc == SWEDG_OK) rc = r;
+    }
+    return rc;
+}
+
+int swedg_compute_invariants(swedg_handle h, const double* u, double t, double* out) {
+    if (!h || !out) return SWEDG_ERR_INVALID;
+    DiagRec r;
+    int rc = swedg_diag_raw(h, SWEDG_DIAG_INVARIANTS, u, nullptr, u ? t : h->t, &r);
+    if (rc) return rc;
+    long elem = -1;
+    std::string msg;
+    rc = finish_diag(r, out, &elem, &msg);
+    if (rc) return fail(h, rc, msg, elem, r.t);
+    return SWEDG_OK;
+}
+
+int swedg_l2_error(swedg_handle h, int what, const double* u, const double* aux, double t, double* out) {
+    if (!h || !out || what == SWEDG_DIAG_INVARIANTS) return SWEDG_ERR_INVALID;
+    DiagRec r;
+    int rc = swedg_diag_raw(h, what, u, aux, t, &r);
+    if (rc) return rc;
+    long elem = -1;
+    std::string msg;
+    double o[6];
+    rc = finish_diag(r, o, &elem, &msg);
+    if (rc) return fail(h, rc, msg, elem, t);
+    for (int i = 0; i < 4; ++i) out[i] = o[i];
+    return SWEDG_OK;
+}
+
+int swedg_sample_invariants(swedg_handle h, int slot) {
+    if (!h || slot < 0) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    if (slot >= h->series_cap) {  // grow (rare; syncs)
+        int cap = std::max(slot + 1, std::max(2 * h->series_cap, 128));
+        DiagRec* nb = nullptr;
+        if (dalloc(h, &nb, (size_t)cap)) return h->last_code;
+        if (h->series) {
+            CUDA_TRY(h, cudaMemcpyAsync(nb, h->series, sizeof(DiagRec) * h->series_cap, cudaMemcpyDeviceToDevice,
+                                        h->stream));
+            CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+            cudaFree(h->series);
+            h->dev_bytes -= sizeof(DiagRec) * (size_t)h->series_cap;
+        }
+        h->series = nb;
+        h->series_cap = cap;
+    }
+    return launch_diag(h, h->u, kDiagInvariants, h->t, nullptr, h->series + slot);
+}
+
+int swedg_read_invariants_raw(swedg_handle h, int n, void* raw) {
+    if (!h || !raw || n < 0 || n > h->series_cap) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    if (n) CUDA_TRY(h, cudaMemcpyAsync(raw, h->series, sizeof(DiagRec) * n, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return SWEDG_OK;
+}
+
+int swedg_read_invariants(swedg_handle h, int n, double* out) {
+    if (!h || !out || n < 0 || n > h->series_cap) return SWEDG_ERR_INVALID;
+    std::vector<DiagRec> recs((size_t)n);
+    int rc = swedg_read_invariants_raw(h, n, recs.data());
+    if (rc) return rc;
+    for (int i = 0; i < n; ++i) {
+        long elem = -1;
+        std::string msg;
+        rc = finish_diag(recs[i], out + (size_t)i * 6, &elem, &msg);
+        if (rc) return fail(h, rc, msg, elem, recs[i].t);
+    }
+    return SWEDG_OK;
+}
+
+// run() (run.hpp:226-262): the time loop with invariant sampling, device-resident.
+// Full-dt steps between samples replay the step graph; samples are enqueued on
+// the stream; the only host syncs are the final error check and the read-back.
+int swedg_run(swedg_handle h, double dt, double tfinal, int sample_every, int max_samples, double* series,
+              int* nsamples, int* nsteps_done) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    cudaSetDevice(h->device);
+    const int nsteps = tfinal > 0.0 ? (int)std::ceil(tfinal / dt - 1e-12) : 0;
+    const int cadence = sample_every > 0 ? sample_every : std::max(1, nsteps / 100);
+    const bool sample = series != nullptr && max_samples > 0;
+    int ns = 0, done = 0;
+    auto take = [&]() -> int {
+        if (!sample) return SWEDG_OK;
+        if (ns >= max_samples) return fail(h, SWEDG_ERR_INVALID, "more invariant samples than max_samples");
+        return swedg_sample_invariants(h, ns++);
+    };
+    if (take()) return h->last_code;
+    int pending = 0;  // full-dt steps not yet enqueued
+    auto flush = [&]() -> int {
+        if (pending == 0) return SWEDG_OK;
+        int rc = swedg_step_lsrk45(h, dt, pending, 0);
+        pending = 0;
+        return rc;
+    };
+    double t = h->t;
+    for (int s = 0; s < nsteps; ++s) {
+        const double step_dt = std::min(dt, tfinal - t);
+        if (step_dt <= 0.0) break;
+        if (step_dt == dt) {
+            ++pending;
+            t = t + dt;  // = the handle's t after the flush (t0 + dt per step)
+        } else {
+            if (flush()) return h->last_code;
+            if (swedg_step_lsrk45(h, step_dt, 1, 0)) return h->last_code;
+            t = h->t;
+        }
+        ++done;
+        if ((s + 1) % cadence == 0 || s + 1 == nsteps) {
+            if (flush() || take()) return h->last_code;
+        }
+    }
+    if (flush()) return h->last_code;
+    if (nsteps_done) *nsteps_done = done;
+    if (nsamples) *nsamples = ns;
+    if (check_errors(h)) return h->last_code;
+    if (sample) return swedg_read_invariants(h, ns, series);
+    return SWEDG_OK;
+}
+
+int swedg_exact_sum(const double* x, size_t n, double* out) {
+    if ((!x && n) || !out) return SWEDG_ERR_INVALID;
+    int64_t L[exact::kLimbs] = {0};
+    for (size_t i = 0; i < n; ++i) {
+        if (!std::isfinite(x[i])) return SWEDG_ERR_NONFINITE;
+        int j;
+        int64_t d0, d1, d2;
+        if (!exact::split(x[i], j, d0, d1, d2)) continue;
+        L[j] += d0;
+        L[j + 1] += d1;
+        L[j + 2] += d2;
+        if ((i & 0xfffff) == 0xfffff) exact::compact(L);  // keep limbs far from int64 overflow
+    }
+    *out = exact::to_double(L);
     return SWEDG_OK;
 }
 

@@ -40,21 +40,24 @@ struct Ar<false> {
 //   key = stage_id << 33 | kernel << 32 | element      kernel 0 = positivity, 1 = non-finite
 struct ErrRec {
     unsigned long long key;
-    unsigned long long step_ctr;  // CUDA-graph replays: steps completed in this call (see swedg_step_lsrk45)
+    // Stage-id offset added on the device: a captured step graph bakes the ids of
+    // its capture; before replays the host sets offset = (first id of the call) -
+    // (baked id) and each replay's last node adds 5, so every stage of every
+    // replay reports a unique, monotonically allocated id (swedg_step_lsrk45).
+    unsigned long long stage_offset;
 };
 constexpr unsigned long long kNoError = ~0ull;
 
 __device__ __forceinline__ void record_error(ErrRec* e, unsigned stage_id, int kernel, int elem) {
-    // a replayed step graph carries the stage ids of its first step; the device
-    // step counter turns them into the ids of the step actually running
-    stage_id += 5u * static_cast<unsigned>(*reinterpret_cast<volatile unsigned long long*>(&e->step_ctr));
+    stage_id += static_cast<unsigned>(*reinterpret_cast<volatile unsigned long long*>(&e->stage_offset));
     unsigned long long key = (static_cast<unsigned long long>(stage_id) << 33) |
                              (static_cast<unsigned long long>(kernel) << 32) |
                              static_cast<unsigned long long>(static_cast<unsigned>(elem));
     atomicMin(&e->key, key);
 }
 
-__global__ void step_counter_kernel(ErrRec* e) { e->step_ctr += 1; }
+__global__ void step_counter_kernel(ErrRec* e) { e->stage_offset += 5; }
+__global__ void set_stage_offset_kernel(ErrRec* e, unsigned long long v) { e->stage_offset = v; }
 
 __device__ __forceinline__ bool error_pending(const ErrRec* e) {
     return *reinterpret_cast<const volatile unsigned long long*>(&e->key) != kNoError;

@@ -54,6 +54,9 @@ def lib(precision: str = "double"):
         _lib.oracle_step_lsrk45.argtypes = [C.POINTER(OracleOps), _dp, _dp, C.c_double, C.c_int, _ip]
         _lib.oracle_rhs_subset.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
         _lib.oracle_rhs_from_proj_n.argtypes = [C.POINTER(OracleOps), _dp, C.c_int, _dp, _ip, C.c_int, _ip]
+        _lib.oracle_project_nodal.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
+        _lib.oracle_diag.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                     C.c_double, C.c_double, C.c_int, _dp, _dp, _dp, C.POINTER(C.c_long)]
         _libs[precision] = _lib
     return _libs[precision]
 
@@ -182,6 +185,43 @@ class Oracle:
         err = self.L.oracle_step_lsrk45(C.byref(self.op), _p(u), _p(res), float(dt), int(nsteps),
                                        C.byref(bad))
         return u, res, err
+
+
+VORTEX_PARAMS = np.array([1.0, 1.0, 0.0, 5.0, 2.0, 0.0, 0.0])  # VortexParams defaults (diagnostics.hpp:30-38)
+
+
+def project_nodal(Pq, u_nodal):
+    """Pq * u per element, k-ascending (diagnostics.hpp:226-230); u_nodal [K][ncol][nq]."""
+    u_nodal = np.ascontiguousarray(u_nodal, dtype=np.float64)
+    Pq = np.ascontiguousarray(Pq, dtype=np.float64)  # [nq][Np] == Np x nq column-major
+    K, ncol, nq = u_nodal.shape
+    Np = Pq.shape[1]
+    out = np.zeros((K, ncol, Np))
+    lib().oracle_project_nodal(K, Np, nq, ncol, _p(Pq), _p(u_nodal), _p(out))
+    return out
+
+
+def diag(fine, u_modal, *, what, b_modal=None, u_ref=None, t=0.0, g=0.0, vortex=VORTEX_PARAMS):
+    """Per-point terms [K][nfine][4] and the reference's serial sums of compute_invariants
+    (what=0), l2_error vs a discrete state (1) or vs the vortex (2).  fine: dict with
+    fine_w, fine_V, fine_Vr, fine_Vs ([Np][nfine] = column-major) and map_coeffs [K][2][Np].
+    Returns (terms, sums, min_h, err, bad_elem)."""
+    f = {k: np.ascontiguousarray(fine[k], dtype=np.float64) for k in
+         ("fine_w", "fine_V", "fine_Vr", "fine_Vs", "map_coeffs")}
+    u = np.ascontiguousarray(u_modal, dtype=np.float64)
+    K, _, Np = u.shape
+    nf = f["fine_w"].shape[0]
+    b = None if b_modal is None else np.ascontiguousarray(b_modal, dtype=np.float64)
+    ur = None if u_ref is None else np.ascontiguousarray(u_ref, dtype=np.float64)
+    vp = np.ascontiguousarray(vortex, dtype=np.float64)
+    terms = np.zeros((K, nf, 4))
+    sums = np.zeros(4)
+    mh = C.c_double(0.0)
+    bad = C.c_long(-1)
+    err = lib().oracle_diag(K, Np, nf, _p(f["fine_w"]), _p(f["fine_V"]), _p(f["fine_Vr"]), _p(f["fine_Vs"]),
+                            _p(f["map_coeffs"]), _p(u), _p(b), _p(ur), _p(vp), float(t), float(g), int(what),
+                            _p(terms), _p(sums), C.byref(mh), C.byref(bad))
+    return terms, sums, mh.value, err, bad.value
 
 
 def case_dict(c) -> dict:

@@ -136,3 +136,31 @@ def test_long_double_yardstick(name):
     abs_err = np.abs(ref - ld).max()
     assert abs_err <= 1e-10 * (1.0 + np.abs(ld).max())
     assert abs_err > 0.0  # genuinely a different (more precise) evaluation
+
+
+# ---- diagnostics (diagnostics.hpp:142-267): compute_invariants / l2_error ----
+@pytest.mark.parametrize("name", PROBLEMS_MODAL + PROBLEMS_SBP)
+def test_diagnostics_oracle_bitwise(name):
+    """oracle_diag's serial sums == the reference's compute_invariants and both
+    l2_error forms on the initial and the final run() state, bit for bit."""
+    from oracle_py import diag, project_nodal
+
+    c = load_golden(name)
+    sbp = int(c["scheme"][0]) == 1
+    g = float(c["g"][0])
+    for tag, key, t in (("diag0_", "u", 0.0), ("diag1_", "u_final", float(c["run_t"][0]))):
+        u, b = c[key], c["b"]
+        if sbp:
+            u = project_nodal(c["ref_Pq"], u)
+            b = project_nodal(c["ref_Pq"], b[:, None, :])[:, 0, :]
+        _, s, mh, err, _ = diag(c, u, what=0, b_modal=b, g=g, t=t)
+        assert err == 0
+        np.testing.assert_array_equal(np.r_[t, s, mh], c[tag + "invariants"])
+        for key_l2, what, kw in (("l2_ref", 1, {"u_ref": c.get(tag + "ref_state")}),
+                                 ("l2_exact", 2 if "vortex" in name else 3, {"t": t})):
+            if tag + key_l2 not in c:
+                continue
+            _, s, _, err, _ = diag(c, u, what=what, **kw)
+            assert err == 0
+            e = np.r_[np.sqrt(s[:3]), np.sqrt(s[0] + s[1] + s[2])]
+            np.testing.assert_array_equal(e, c[tag + key_l2])
