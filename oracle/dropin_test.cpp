@@ -14,6 +14,7 @@
 #include "swedg/run.hpp"
 #include "swedg/solver.hpp"
 #include "swedg_b200.hpp"
+#include "swedg_b200_run.hpp"
 
 using namespace swedg;
 
@@ -142,6 +143,58 @@ int main() {
         swedg_b200::set_bathymetry(par, c.nstate.b);
         auto du_par = swedg_b200::rhs(par, c.nstate);
         check(max_rel(du_par, du_ref) == 0.0, "SBP N=4 dam parity rhs bitwise", max_rel(du_par, du_ref));
+    }
+    // ---- run() time loop + diagnostics (run.hpp:226-284) through swedg_b200_run.hpp
+    struct RunCase {
+        ProblemId p;
+        Scheme s;
+        int N, n;
+        double warp, tfinal;
+        const char* tag;
+    };
+    for (const RunCase& rc : {RunCase{ProblemId::Vortex, Scheme::Hybridized, 3, 8, 0.0, 0.2, "vortex N=3"},
+                              RunCase{ProblemId::Lake, Scheme::Hybridized, 3, 6, 0.1, 0.05, "lake N=3 curved"},
+                              RunCase{ProblemId::Lake, Scheme::SbpLegendre, 3, 4, 0.1, 0.02, "SBP lake N=3"},
+                              RunCase{ProblemId::DamBreak, Scheme::SbpLegendre, 4, 10, 0.0, 0.02, "SBP dam N=4"}}) {
+        RunConfig cfg;
+        cfg.problem = rc.p;
+        cfg.scheme = rc.s;
+        cfg.degree = rc.N;
+        cfg.nx = cfg.ny = rc.n;
+        cfg.warp = rc.warp;
+        cfg.tfinal = rc.tfinal;
+        if (rc.p == ProblemId::DamBreak) cfg.cfl = 0.0625;
+        Case cr = build_case(cfg), cd = build_case(cfg);
+        FineQuad fq(cfg.degree);
+        Invariants i_ref = compute_invariants(fq, cr.geo, cr.modal_solution(), cr.modal_bathymetry(), cr.cfg.g, cr.time());
+        RunResult r_ref = run(cr);
+        auto ops = swedg_b200::make_device_ops(cd, swedg_b200::Mode::Parity);
+        Invariants i_dev = swedg_b200::compute_invariants(ops, cd);
+        const std::string tag = rc.tag;
+        auto rel = [](double a, double b) { return std::abs(a - b) / (1.0 + std::abs(b)); };
+        double d0 = std::max({rel(i_dev.mass, i_ref.mass), rel(i_dev.momentum_x, i_ref.momentum_x),
+                              rel(i_dev.momentum_y, i_ref.momentum_y), rel(i_dev.entropy, i_ref.entropy)});
+        check(d0 <= 1e-13 && i_dev.min_h == i_ref.min_h, tag + " compute_invariants (exact sums vs serial)", d0);
+        RunResult r_dev = swedg_b200::run(cd, ops);
+        check(r_dev.steps == r_ref.steps && r_dev.series.size() == r_ref.series.size() && r_dev.dt == r_ref.dt,
+              tag + " run(): steps and samples", (double)r_dev.steps);
+        double ds = 0.0;
+        bool times = true;
+        for (size_t i = 0; i < std::min(r_dev.series.size(), r_ref.series.size()); ++i) {
+            const Invariants &a = r_dev.series[i], &b = r_ref.series[i];
+            times = times && a.t == b.t && a.min_h == b.min_h;
+            ds = std::max({ds, rel(a.mass, b.mass), rel(a.momentum_x, b.momentum_x), rel(a.momentum_y, b.momentum_y),
+                           rel(a.entropy, b.entropy)});
+        }
+        check(times && ds <= 1e-13, tag + " run(): invariant series", ds);
+        const auto& ud = cd.sbp ? cd.nstate.u : cd.hstate.u;
+        const auto& ur = cr.sbp ? cr.nstate.u : cr.hstate.u;
+        check(max_rel(ud, ur) == 0.0 && cd.time() == cr.time(), tag + " run(): final state bitwise (parity)",
+              max_rel(ud, ur));
+        if (r_ref.has_error)
+            check(r_dev.has_error && rel(r_dev.error.combined, r_ref.error.combined) <= 1e-11 &&
+                      r_dev.error.h_mesh == r_ref.error.h_mesh,
+                  tag + " run(): L2 error", rel(r_dev.error.combined, r_ref.error.combined));
     }
     std::printf("%s\n", failures ? "FAILURES" : "all drop-in checks passed");
     return failures;
