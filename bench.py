@@ -349,6 +349,19 @@ def run_ours(args, rank, world, local):
     e2e_val = dof * world * 5 * args.e2e_steps / (e2e_ms * 1e-3) / 1e9
     state_bytes = K * 3 * Np * 8
 
+    # ---- device diagnostics (outside the timed region): one exact-sum
+    # compute_invariants sample of the resident state, as run() takes ~100 per run
+    h.sample_invariants(0)
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for _ in range(3):
+        h.sample_invariants(0)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    inv_ms = d0.elapsed_time(d1) / 3
+    inv = h.read_invariants(1)[0]
+
     # ---- roofline of the dominant kernel (volume: projection + flux differencing)
     fb = flops_bytes_per_element(args.N)
     vol_avg_ms = kms[0] / max(1, kn[0])
@@ -408,6 +421,9 @@ def run_ours(args, rank, world, local):
         "roofline_surface": roofline_surface,
         "cpu_baseline": cpu,
         "clocks": clk,
+        "diagnostics": {"invariants_ms": round(inv_ms, 4), "mass": inv[1], "entropy": inv[4],
+                        "note": "device compute_invariants (exact sums, fine rule degree 2N+2) of the "
+                                "final state, outside the timed region"},
         "setup_s": round(setup_s, 2),
         "device_bytes": h.device_bytes,
     }

@@ -52,6 +52,7 @@ struct DiagParams {
     int K, nfine, what, sbp, nq;
     double g, t;
     const double* fine;  // w[nfine] | V | Vr | Vs  (nfine x Np column-major each)
+    const double* wJ;    // [K][nfine] w_i * J_i of FineQuad::element_geometry (diag_wj_kernel)
     const double* Pq;    // SBP: Np x nq column-major
     const double* map;   // [K][2][Np]
     const double* u;     // [K][3][Np] modal, or SBP nodal [K][3][nq]
@@ -73,23 +74,87 @@ __global__ void diag_init_kernel(DiagRec* r, double t, int what) {
     }
 }
 
+// FineQuad::element_geometry (diagnostics.hpp:155-165), once per mesh:
+// J = dr0*ds1 - ds0*dr1 with dr = Vr*map, ds = Vs*map, stored as w_i*J_i (the
+// factor every diagnostic term starts with).  J <= 0 marks the element in *bad.
+template <int N>
+__global__ void diag_wj_kernel(int K, int nfine, const double* __restrict__ fine, const double* __restrict__ map,
+                               double* __restrict__ wJ, unsigned long long* bad) {
+    constexpr int Np = (N + 1) * (N + 2) / 2;
+    const double* W = fine;
+    const double* Vr = fine + nfine + (size_t)nfine * Np;
+    const double* Vs = Vr + (size_t)nfine * Np;
+    const long n = (long)K * nfine;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+        const long k = p / nfine;
+        const int i = (int)(p - k * nfine);
+        const double* mk = map + (size_t)k * 2 * Np;
+        double dr[2], ds[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            double r = 0.0, q = 0.0;
+            for (int m = 0; m < Np; ++m) r = __dadd_rn(r, __dmul_rn(__ldg(Vr + i + (size_t)m * nfine), mk[c * Np + m]));
+            for (int m = 0; m < Np; ++m) q = __dadd_rn(q, __dmul_rn(__ldg(Vs + i + (size_t)m * nfine), mk[c * Np + m]));
+            dr[c] = r;
+            ds[c] = q;
+        }
+        const double J = __dsub_rn(__dmul_rn(dr[0], ds[1]), __dmul_rn(ds[0], dr[1]));
+        if (J <= 0.0) atomicMin(bad, (unsigned long long)k);  // "nonpositive Jacobian at fine point" (:162)
+        wJ[p] = __dmul_rn(__ldg(W + i), J);
+    }
+}
+
 constexpr int kDiagWarps = 4;
+constexpr int kDiagBatch = 8;  // elements per warp batch: N=4 -> 8 x 36 = 288 (element, point) pairs
 
 template <int N>
 struct DiagDims {
     static constexpr int Np = (N + 1) * (N + 2) / 2;
     static constexpr int nq_max = 64;  // SBP nodes staged (N <= 4: 37)
-    // per-warp staging: u (3 Np), b (Np), map (2 Np), nodal (4 nq_max)
-    static constexpr int warp_doubles = 6 * Np + 4 * nq_max;
+    // per-warp staging: per element u (3 Np), b (Np), map (2 Np); SBP nodal scratch (4 nq_max)
+    static constexpr int elem_doubles = 6 * Np;
+    static constexpr int warp_doubles = kDiagBatch * elem_doubles + 4 * nq_max;
 };
 
-__device__ __forceinline__ void acc_add(long long* L, double x) {
-    int j;
-    int64_t d0, d1, d2;
-    if (!exact::split(x, j, d0, d1, d2)) return;
-    atomicAdd(reinterpret_cast<unsigned long long*>(&L[j]), static_cast<unsigned long long>(d0));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&L[j + 1]), static_cast<unsigned long long>(d1));
-    if (d2) atomicAdd(reinterpret_cast<unsigned long long*>(&L[j + 2]), static_cast<unsigned long long>(d2));
+// Warp-cooperative exact accumulation: every lane offers one term x (0 = none);
+// the warp adds all of them into its private limb array W.  Terms whose limb
+// index lies within one of the warp minimum go in one round: each lane's three
+// signed 32-bit digits are split into 16-bit halves, summed across the warp with
+// REDUX (|sum| < 2^21, exact in int32), recombined, and lanes 0..3 add the four
+// affected limbs (distinct addresses: no atomics).  Other lanes go in later rounds.
+__device__ __forceinline__ void warp_acc(long long* W, double x, int lane) {
+    int j = 0;
+    int64_t d0 = 0, d1 = 0, d2 = 0;
+    const bool has = exact::split(x, j, d0, d1, d2);
+    unsigned pending = __ballot_sync(0xffffffffu, has);
+    while (pending) {
+        const bool mine_p = (pending >> lane) & 1u;
+        const int jr = __reduce_min_sync(0xffffffffu, mine_p ? j : 0x7fffffff);
+        const bool mine = mine_p && j <= jr + 1;
+        const bool o1 = j == jr + 1;
+        int64_t s[4];
+        s[0] = mine && !o1 ? d0 : 0;
+        s[1] = mine ? (o1 ? d0 : d1) : 0;
+        s[2] = mine ? (o1 ? d1 : d2) : 0;
+        s[3] = mine && o1 ? d2 : 0;
+        long long tot = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t v = s[q];
+            const uint64_t m = static_cast<uint64_t>(v < 0 ? -v : v);  // < 2^32
+            int lo = static_cast<int>(m & 0xffffu), hi = static_cast<int>(m >> 16);
+            if (v < 0) {
+                lo = -lo;
+                hi = -hi;
+            }
+            const int slo = __reduce_add_sync(0xffffffffu, lo);
+            const int shi = __reduce_add_sync(0xffffffffu, hi);
+            if (lane == q) tot = static_cast<long long>(shi) * 65536ll + slo;
+        }
+        if (lane < 4 && tot) W[jr + lane] += tot;
+        pending &= ~__ballot_sync(0xffffffffu, mine);
+        __syncwarp();  // order this round's limb updates before the next round's
+    }
 }
 
 // vortex_exact (diagnostics.hpp:41-53).  exp is CUDA's (<= 1 ulp), not glibc's:
@@ -114,130 +179,153 @@ template <int N>
 __global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
     using D = DiagDims<N>;
     constexpr int Np = D::Np;
-    __shared__ long long acc[4][exact::kLimbs];
+    constexpr int L = exact::kLimbs;
+    __shared__ long long acc[kDiagWarps][4][L];
     __shared__ double stage[kDiagWarps][D::warp_doubles];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < 4 * exact::kLimbs; i += blockDim.x) (&acc[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < kDiagWarps * 4 * L; i += blockDim.x) (&acc[0][0][0])[i] = 0;
     __syncthreads();
 
-    double* su = stage[wid];       // [3][Np] modal state (or u - u_ref)
-    double* sb = su + 3 * Np;      // [Np] modal bathymetry
-    double* sm = sb + Np;          // [2][Np] map coefficients
-    double* sn = sm + 2 * Np;      // SBP nodal staging [4][nq]
+    long long(*W)[L] = acc[wid];
+    double* sw = stage[wid];                         // [batch][6 Np]: u (3 Np) | b (Np) | map (2 Np)
+    double* sn = sw + kDiagBatch * D::elem_doubles;  // SBP nodal scratch [4][nq]
     const int nfine = P.nfine, nq = P.nq;
-    const double* W = P.fine;
-    const double* V = W + nfine;
-    const double* Vr = V + (size_t)nfine * Np;
-    const double* Vs = Vr + (size_t)nfine * Np;
+    const double* V = P.fine + nfine;
     const bool inv = P.what == kDiagInvariants;
+    const bool exact_sol = P.what == kDiagL2Vortex || P.what == kDiagL2Lake;
     unsigned long long kmin = order_key(1e300), kbad = ~0ull;
     unsigned nonfinite = 0;
+    const long nbatch = ((long)P.K + kDiagBatch - 1) / kDiagBatch;
 
-    for (long k = (long)blockIdx.x * kDiagWarps + wid; k < P.K; k += (long)gridDim.x * kDiagWarps) {
-        // ---- stage the element
-        for (int x = lane; x < 2 * Np; x += 32) sm[x] = P.map[(size_t)k * 2 * Np + x];
+    for (long bt = (long)blockIdx.x * kDiagWarps + wid; bt < nbatch; bt += (long)gridDim.x * kDiagWarps) {
+        const long k0 = bt * kDiagBatch;
+        const int ne = (int)min((long)kDiagBatch, (long)P.K - k0);
+        // ---- stage the batch (coalesced: consecutive elements are contiguous)
         if (P.sbp) {
-            for (int x = lane; x < 3 * nq; x += 32) sn[x] = P.u[(size_t)k * 3 * nq + x];
-            if (inv)
-                for (int x = lane; x < nq; x += 32) sn[3 * nq + x] = P.b[(size_t)k * nq + x];
-            __syncwarp();
-            // project_nodal: (Pq u)(n, c) = sum_q Pq(n, q) u(q, c), q ascending
-            const int ncol = inv ? 4 : 3;
-            for (int x = lane; x < ncol * Np; x += 32) {
-                const int c = x / Np, n = x - c * Np;
-                double s = 0.0;
-                for (int q = 0; q < nq; ++q) s = __dadd_rn(s, __dmul_rn(P.Pq[n + (size_t)q * Np], sn[c * nq + q]));
-                su[x] = s;  // c = 3 lands in sb (= su + 3 Np)
+            for (int e = 0; e < ne; ++e) {
+                const long k = k0 + e;
+                double* se = sw + e * D::elem_doubles;
+                __syncwarp();
+                for (int x = lane; x < 3 * nq; x += 32) sn[x] = P.u[(size_t)k * 3 * nq + x];
+                if (inv)
+                    for (int x = lane; x < nq; x += 32) sn[3 * nq + x] = P.b[(size_t)k * nq + x];
+                __syncwarp();
+                // project_nodal: (Pq u)(n, c) = sum_q Pq(n, q) u(q, c), q ascending (diagnostics.hpp:226-230)
+                const int ncol = inv ? 4 : 3;
+                for (int x = lane; x < ncol * Np; x += 32) {
+                    const int c = x / Np, m = x - c * Np;
+                    double s = 0.0;
+                    for (int q = 0; q < nq; ++q)
+                        s = __dadd_rn(s, __dmul_rn(__ldg(P.Pq + m + (size_t)q * Np), sn[c * nq + q]));
+                    se[x] = s;  // c = 3 lands in the b slot (3 Np)
+                }
             }
         } else {
-            for (int x = lane; x < 3 * Np; x += 32) su[x] = P.u[(size_t)k * 3 * Np + x];
+            for (int x = lane; x < ne * 3 * Np; x += 32) {
+                const int e = x / (3 * Np);
+                sw[e * D::elem_doubles + (x - e * 3 * Np)] = P.u[(size_t)k0 * 3 * Np + x];
+            }
             if (inv)
-                for (int x = lane; x < Np; x += 32) sb[x] = P.b[(size_t)k * Np + x];
+                for (int x = lane; x < ne * Np; x += 32) {
+                    const int e = x / Np;
+                    sw[e * D::elem_doubles + 3 * Np + (x - e * Np)] = P.b[(size_t)k0 * Np + x];
+                }
         }
+        if (exact_sol)
+            for (int x = lane; x < ne * 2 * Np; x += 32) {
+                const int e = x / (2 * Np);
+                sw[e * D::elem_doubles + 4 * Np + (x - e * 2 * Np)] = P.map[(size_t)k0 * 2 * Np + x];
+            }
         __syncwarp();
         if (P.what == kDiagL2Ref) {  // u_modal[k] - ref_modal[k] (diagnostics.hpp:210)
-            for (int x = lane; x < 3 * Np; x += 32) su[x] = __dsub_rn(su[x], P.uref[(size_t)k * 3 * Np + x]);
+            for (int x = lane; x < ne * 3 * Np; x += 32) {
+                const int e = x / (3 * Np);
+                double& v = sw[e * D::elem_doubles + (x - e * 3 * Np)];
+                v = __dsub_rn(v, P.uref[(size_t)k0 * 3 * Np + x]);
+            }
             __syncwarp();
         }
-        // ---- fine points
-        for (int i = lane; i < nfine; i += 32) {
-            double xy[2], dr[2], ds[2];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                double a = 0.0, r = 0.0, q = 0.0;
-                for (int n = 0; n < Np; ++n) a = __dadd_rn(a, __dmul_rn(__ldg(V + i + (size_t)n * nfine), sm[c * Np + n]));
-                for (int n = 0; n < Np; ++n) r = __dadd_rn(r, __dmul_rn(__ldg(Vr + i + (size_t)n * nfine), sm[c * Np + n]));
-                for (int n = 0; n < Np; ++n) q = __dadd_rn(q, __dmul_rn(__ldg(Vs + i + (size_t)n * nfine), sm[c * Np + n]));
-                xy[c] = a;
-                dr[c] = r;
-                ds[c] = q;
-            }
-            const double J = __dsub_rn(__dmul_rn(dr[0], ds[1]), __dmul_rn(ds[0], dr[1]));
-            if (J <= 0.0) {  // "nonpositive Jacobian at fine point" (diagnostics.hpp:162)
-                kbad = min(kbad, (unsigned long long)k << 1);
-                continue;
-            }
-            const double wJ = __dmul_rn(__ldg(W + i), J);
-            double uq[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                double a = 0.0;
-                for (int n = 0; n < Np; ++n) a = __dadd_rn(a, __dmul_rn(__ldg(V + i + (size_t)n * nfine), su[c * Np + n]));
-                uq[c] = a;
-            }
-            double tm[4];
-            int nt = 3;
-            if (inv) {
-                double bq = 0.0;
-                for (int n = 0; n < Np; ++n) bq = __dadd_rn(bq, __dmul_rn(__ldg(V + i + (size_t)n * nfine), sb[n]));
-                if (!(uq[0] > 0.0)) {  // entropy() -> check_positive (swe.hpp:47-48)
-                    kbad = min(kbad, ((unsigned long long)k << 1) | 1ull);
-                    continue;
-                }
-                const double h = uq[0];
-                const double vx = __ddiv_rn(uq[1], h), vy = __ddiv_rn(uq[2], h);
-                // 0.5 h (vx^2 + vy^2) + 0.5 g h h + g h b   (swe.hpp:50)
-                double ent = __dmul_rn(__dmul_rn(0.5, h), __dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
-                ent = __dadd_rn(ent, __dmul_rn(__dmul_rn(__dmul_rn(0.5, P.g), h), h));
-                ent = __dadd_rn(ent, __dmul_rn(__dmul_rn(P.g, h), bq));
-                tm[0] = __dmul_rn(wJ, h);
-                tm[1] = __dmul_rn(wJ, uq[1]);
-                tm[2] = __dmul_rn(wJ, uq[2]);
-                tm[3] = __dmul_rn(wJ, ent);
-                nt = 4;
-                kmin = min(kmin, order_key(h));
-            } else if (P.what == kDiagL2Ref) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) tm[c] = __dmul_rn(__dmul_rn(wJ, uq[c]), uq[c]);
-            } else {
-                double ue[3];
-                if (P.what == kDiagL2Vortex) {
-                    vortex_exact_dev(P.vortex, xy[0], xy[1], P.t, ue);
-                } else {  // lake at rest: (2 - lake_bathymetry(x), 0, 0) (run.hpp:125-127)
-                    const double a = __dmul_rn(__dmul_rn(2.0, 3.14159265358979323846), xy[0]);
-                    double sn_, cs_;
-                    sincos(a, &sn_, &cs_);
-                    ue[0] = __dsub_rn(2.0, __dadd_rn(__dmul_rn(__dmul_rn(0.1, sn_), cs_), 0.5));
-                    ue[1] = 0.0;
-                    ue[2] = 0.0;
-                }
+        // ---- (element, fine point) pairs, 32 per warp step; every lane takes part in warp_acc
+        const int npair = ne * nfine;
+        for (int base = 0; base < npair; base += 32) {
+            const int pr = base + lane;
+            double tm[4] = {0.0, 0.0, 0.0, 0.0};
+            if (pr < npair) {
+                const int e = pr / nfine, i = pr - e * nfine;
+                const long k = k0 + e;
+                const double* se = sw + e * D::elem_doubles;
+                const double wJ = __ldg(P.wJ + (size_t)k0 * nfine + pr);
+                double uq[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const double d = __dsub_rn(uq[c], ue[c]);
-                    tm[c] = __dmul_rn(__dmul_rn(wJ, d), d);
+                    double a = 0.0;
+#pragma unroll
+                    for (int m = 0; m < Np; ++m) a = __dadd_rn(a, __dmul_rn(__ldg(V + i + (size_t)m * nfine), se[c * Np + m]));
+                    uq[c] = a;
                 }
-            }
-            for (int q = 0; q < nt; ++q) {
-                if (!isfinite(tm[q])) {
-                    nonfinite |= 1u << q;
-                    continue;
+                if (inv) {
+                    double bq = 0.0;
+#pragma unroll
+                    for (int m = 0; m < Np; ++m) bq = __dadd_rn(bq, __dmul_rn(__ldg(V + i + (size_t)m * nfine), se[3 * Np + m]));
+                    const double h = uq[0];
+                    if (!(h > 0.0)) {  // entropy() -> check_positive (swe.hpp:47-48)
+                        kbad = min(kbad, ((unsigned long long)k << 1) | 1ull);
+                    } else {
+                        const double vx = __ddiv_rn(uq[1], h), vy = __ddiv_rn(uq[2], h);
+                        // 0.5 h (vx^2 + vy^2) + 0.5 g h h + g h b   (swe.hpp:50)
+                        double ent = __dmul_rn(__dmul_rn(0.5, h), __dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)));
+                        ent = __dadd_rn(ent, __dmul_rn(__dmul_rn(__dmul_rn(0.5, P.g), h), h));
+                        ent = __dadd_rn(ent, __dmul_rn(__dmul_rn(P.g, h), bq));
+                        tm[0] = __dmul_rn(wJ, h);
+                        tm[1] = __dmul_rn(wJ, uq[1]);
+                        tm[2] = __dmul_rn(wJ, uq[2]);
+                        tm[3] = __dmul_rn(wJ, ent);
+                        kmin = min(kmin, order_key(h));
+                    }
+                } else if (P.what == kDiagL2Ref) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) tm[c] = __dmul_rn(__dmul_rn(wJ, uq[c]), uq[c]);
+                } else {
+                    double xy[2];
+                    const double* sm = se + 4 * Np;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        double a = 0.0;
+                        for (int m = 0; m < Np; ++m) a = __dadd_rn(a, __dmul_rn(__ldg(V + i + (size_t)m * nfine), sm[c * Np + m]));
+                        xy[c] = a;
+                    }
+                    double ue[3];
+                    if (P.what == kDiagL2Vortex) {
+                        vortex_exact_dev(P.vortex, xy[0], xy[1], P.t, ue);
+                    } else {  // lake at rest: (2 - lake_bathymetry(x), 0, 0) (run.hpp:125-127)
+                        const double a = __dmul_rn(__dmul_rn(2.0, 3.14159265358979323846), xy[0]);
+                        double sn_, cs_;
+                        sincos(a, &sn_, &cs_);
+                        ue[0] = __dsub_rn(2.0, __dadd_rn(__dmul_rn(__dmul_rn(0.1, sn_), cs_), 0.5));
+                        ue[1] = 0.0;
+                        ue[2] = 0.0;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double d = __dsub_rn(uq[c], ue[c]);
+                        tm[c] = __dmul_rn(__dmul_rn(wJ, d), d);
+                    }
                 }
-                acc_add(acc[q], tm[q]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (!isfinite(tm[q])) {
+                        nonfinite |= 1u << q;
+                        tm[q] = 0.0;
+                    }
             }
+            warp_acc(W[0], tm[0], lane);
+            warp_acc(W[1], tm[1], lane);
+            warp_acc(W[2], tm[2], lane);
+            if (inv) warp_acc(W[3], tm[3], lane);
         }
         __syncwarp();
     }
-    // ---- merge: warp minima, then block limbs -> record (integer adds: exact)
+    // ---- merge: warp minima; warps' limbs -> block limbs -> record (integer adds: exact)
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
@@ -250,10 +338,17 @@ __global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
         if (nonfinite) atomicOr(&P.rec->nonfinite, nonfinite);
     }
     __syncthreads();
-    if (threadIdx.x < 4) exact::compact(reinterpret_cast<int64_t*>(acc[threadIdx.x]));
+    for (int i = threadIdx.x; i < 4 * L; i += blockDim.x) {
+        long long s = 0;
+#pragma unroll
+        for (int w = 0; w < kDiagWarps; ++w) s += (&acc[w][0][0])[i];
+        (&acc[0][0][0])[i] = s;
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < 4 * exact::kLimbs; i += blockDim.x) {
-        const long long v = (&acc[0][0])[i];
+    if (threadIdx.x < 4) exact::compact(reinterpret_cast<int64_t*>(acc[0][threadIdx.x]));
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * L; i += blockDim.x) {
+        const long long v = (&acc[0][0][0])[i];
         if (v) atomicAdd(reinterpret_cast<unsigned long long*>(&P.rec->limbs[0][0] + i), static_cast<unsigned long long>(v));
     }
 }

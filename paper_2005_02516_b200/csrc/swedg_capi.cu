@@ -76,6 +76,8 @@ struct swedg_handle_s {
     double* fine = nullptr;    // fine rule: w | V | Vr | Vs
     double* dPq = nullptr;     // SBP project_nodal operator (Np x nq)
     double* map = nullptr;     // [K][2][Np] mapping coefficients
+    double* wJ = nullptr;      // [K][nfine] fine-rule w_i * J_i
+    long diag_bad_geom = -1;   // element with J <= 0 at a fine point (-1: none)
     double* bmod = nullptr;    // bathymetry as given to swedg_set_bathymetry
     double* uref = nullptr;    // l2_error reference state [K][3][Np]
     DiagRec* drec = nullptr;   // one-shot record
@@ -508,6 +510,7 @@ void launch_diag_n(swedg_handle h, const double* u, int what, double t, const do
     P.g = h->g;
     P.t = t;
     P.fine = h->fine;
+    P.wJ = h->wJ;
     P.Pq = h->dPq;
     P.map = h->map;
     P.u = u;
@@ -525,6 +528,10 @@ void launch_diag_n(swedg_handle h, const double* u, int what, double t, const do
 
 int launch_diag(swedg_handle h, const double* u, int what, double t, const double* vortex, DiagRec* rec) {
     if (!h->fine) return fail(h, SWEDG_ERR_INVALID, "diagnostics need swedg_set_diagnostics first");
+    if (h->diag_bad_geom >= 0)  // FineQuad::element_geometry throws (diagnostics.hpp:162)
+        return fail(h, SWEDG_ERR_INVALID,
+                    "nonpositive Jacobian at fine point in element " + std::to_string(h->diag_bad_geom),
+                    h->diag_bad_geom);
     if (what == kDiagInvariants && !h->bmod)
         return fail(h, SWEDG_ERR_INVALID, "compute_invariants needs swedg_set_bathymetry first");
     switch (h->N) {
@@ -789,7 +796,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
-                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series};
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& p : h->ev_pending) {
@@ -1188,6 +1195,11 @@ int swedg_set_diagnostics(swedg_handle h, const swedg_diag_desc* d) {
         cudaFree(h->fine);
         h->dev_bytes -= (size_t)h->nfine * (1 + 3 * Np) * sizeof(double);
         h->fine = nullptr;
+        if (h->wJ && h->nfine != (int)nf) {
+            cudaFree(h->wJ);
+            h->dev_bytes -= K * (size_t)h->nfine * sizeof(double);
+            h->wJ = nullptr;
+        }
     }
     if (dalloc(h, &h->fine, fine.size()) || upload(h, h->fine, fine.data(), fine.size())) return h->last_code;
     h->nfine = d->nfine;
@@ -1198,7 +1210,24 @@ int swedg_set_diagnostics(swedg_handle h, const swedg_diag_desc* d) {
         if (upload(h, h->dPq, d->Pq, Np * h->nq)) return h->last_code;
     }
     if (!h->drec && dalloc(h, &h->drec, 1)) return h->last_code;
+    // w_i * J_i at every fine point, once per mesh
+    if (!h->wJ && dalloc(h, &h->wJ, K * nf)) return h->last_code;
+    CUDA_TRY(h, cudaMemsetAsync(&h->drec->bad, 0xff, sizeof(unsigned long long), h->stream));
+    {
+        const int tb = 256;
+        const int grid = (int)std::min<size_t>((K * nf + tb - 1) / tb, (size_t)h->nsm * 8);
+        switch (h->N) {
+            case 1: diag_wj_kernel<1><<<grid, tb, 0, h->stream>>>(h->K, h->nfine, h->fine, h->map, h->wJ, &h->drec->bad); break;
+            case 2: diag_wj_kernel<2><<<grid, tb, 0, h->stream>>>(h->K, h->nfine, h->fine, h->map, h->wJ, &h->drec->bad); break;
+            case 3: diag_wj_kernel<3><<<grid, tb, 0, h->stream>>>(h->K, h->nfine, h->fine, h->map, h->wJ, &h->drec->bad); break;
+            case 4: diag_wj_kernel<4><<<grid, tb, 0, h->stream>>>(h->K, h->nfine, h->fine, h->map, h->wJ, &h->drec->bad); break;
+        }
+        h->launches++;
+    }
+    unsigned long long bad = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&bad, &h->drec->bad, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    h->diag_bad_geom = bad == ~0ull ? -1 : (long)bad;
     return SWEDG_OK;
 }
 
