@@ -216,6 +216,18 @@ int swedg_run(swedg_handle h, double dt, double tfinal, int sample_every, int ma
 /* Host reference of the exact accumulator: *out = correctly rounded sum of x[0..n). */
 int swedg_exact_sum(const double* x, size_t n, double* out);
 
+/* ---- volume-kernel cost study (bench.hpp:55-201) ---------
+ * R_GPU = t_ESDG / t_DG of the reference's two study kernels on the device:
+ * kernel_matvec (y = Q f(u), nodal x-flux) and kernel_fluxdiff
+ * (y_i = sum_j 2 Q_ij f_S(u_i, u_j); nq < n: kernel_fluxdiff_skew, the block
+ * j, i >= nq skipped).  Q n x n column-major (2 <= n <= 256), u/y [K][3][n].
+ * Both kernels run 2 untimed + reps timed launches (CUDA events);
+ * t_ms[2] = median {t_DG, t_ESDG}; y_dg / y_esdg (may be NULL) receive the
+ * outputs.  mode PARITY = the reference's arithmetic bit for bit; FAST = FMA
+ * and the reassociated EC flux.  No handle; stand-alone device buffers. */
+int swedg_ratio_kernels(int device, int n, int nq, int K, const double* Q, const double* u, double g, int mode,
+                        int reps, double* y_dg, double* y_esdg, double* t_ms);
+
 /* ---- errors ----------------------------------------------------------------- */
 /* Last failure: status code, element id (or -1), stage time, message. */
 int swedg_last_error(swedg_handle h, int* code, long* elem, double* t, char* msg, size_t len);

@@ -10,18 +10,26 @@
 // LSRK45 step (5 RHS stages).  Prints one JSON line.
 //
 //   swedg_refbench N K1D warmup steps threads [warp]
+//   swedg_refbench ratio K threads     (bench.hpp ratio_sweep: the R_CPU study, CSV)
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <string>
 #include <thread>
 
+#include "swedg/bench.hpp"
 #include "swedg/run.hpp"
 #include "swedg/solver.hpp"
 
 using namespace swedg;
 
 int main(int argc, char** argv) {
+    if (argc >= 2 && std::string(argv[1]) == "ratio") {
+        int K = argc > 2 ? std::atoi(argv[2]) : 64, threads = argc > 3 ? std::atoi(argv[3]) : 1;
+        std::fputs(ratios_csv(ratio_sweep(default_bench_sizes(), K, threads, 0)).c_str(), stdout);
+        return 0;
+    }
     if (argc < 6) {
         std::fprintf(stderr, "usage: swedg_refbench N K1D warmup steps threads [warp]\n");
         return 2;

@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "swedg/bench.hpp"
 #include "swedg/run.hpp"
 #include "swedg/solver.hpp"
 
@@ -486,6 +487,34 @@ int cmd_positivity(const std::string& path) {
     return 0;
 }
 
+// bench.hpp's volume-kernel cost study (kernel_matvec / kernel_fluxdiff /
+// kernel_fluxdiff_skew, bench.hpp:55-128) on the ratio_sweep operators and
+// states (random_operator / random_states, seeded as ratio_sweep does).
+int cmd_ratio(const std::string& path) {
+    Writer w(path);
+    const double g = 9.81;
+    const int K = 4;
+    std::vector<int> sizes = {6, 10, 15, 21, 28, 36, 50};
+    w.i32("sizes", {sizes.size()}, sizes.data());
+    for (int n : sizes) {
+        std::mt19937 rng(0u + static_cast<unsigned>(n));
+        Mat Q = random_operator(n, rng);
+        BenchStates s = random_states(n, K, rng);
+        std::string p = "n" + std::to_string(n) + "_";
+        w.mat(p + "Q", Q);
+        w.mats(p + "u", s.u);
+        w.mats(p + "y_dg", kernel_matvec(Q, s, g));
+        w.mats(p + "y_esdg", kernel_fluxdiff(Q, s, g));
+        // block-zero operator for the skew variant (nq = 2n/3)
+        int nq = (2 * n) / 3;
+        Mat Qz = Q;
+        Qz.bottomRightCorner(n - nq, n - nq).setZero();
+        w.iscalar(p + "nq", nq);
+        w.mats(p + "y_skew", kernel_fluxdiff_skew(Qz, nq, s, g));
+    }
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -499,6 +528,7 @@ int main(int argc, char** argv) {
     try {
         if (cmd == "ops") return cmd_ops(out);
         if (cmd == "positivity") return cmd_positivity(out);
+        if (cmd == "ratio") return cmd_ratio(out);
         if (cmd == "modal" && argc == 11)
             return cmd_modal(out, std::atoi(argv[3]), std::atoi(argv[4]), std::atof(argv[5]),
                              std::atoi(argv[6]) != 0, static_cast<unsigned>(std::atoi(argv[7])),

@@ -645,3 +645,65 @@ int oracle_diag(int K, int Np, int nfine, const double *w, const double *V, cons
     if (min_h) *min_h = mh;
     return ORACLE_OK;
 }
+
+/* ---- volume-kernel cost study (bench.hpp:55-128) ---------------------------
+ * u [K][3][n] (n x 3 column-major per element), Q n x n column-major, y [K][3][n].
+ * x-direction physical flux (swe.hpp:60-66) and EC flux (swe.hpp:69-85). */
+void oracle_ratio_matvec(int n, int K, const double *Q, const double *u, double g, double *y) {
+    double *f = (double *)malloc(sizeof(double) * 3 * (size_t)n);
+    for (int k = 0; k < K; ++k) {
+        const double *uk = u + (size_t)k * 3 * n;
+        for (int i = 0; i < n; ++i) {
+            double h = uk[i], hu = uk[n + i], hv = uk[2 * n + i];
+            double vx = hu / h, vy = hv / h;
+            double p = 0.5 * g * h * h;
+            f[i] = hu;
+            f[n + i] = hu * vx + p;
+            f[2 * n + i] = hu * vy;
+        }
+        for (int c = 0; c < 3; ++c) /* y = Q * f, k-ascending (Eigen shim product) */
+            for (int i = 0; i < n; ++i) {
+                double s = 0.0;
+                for (int j = 0; j < n; ++j) s += Q[i + (size_t)j * n] * f[c * n + j];
+                y[((size_t)k * 3 + c) * n + i] = s;
+            }
+    }
+    free(f);
+}
+
+static void ec_flux_x(const double *a, const double *b, double g, double *f) {
+    double uxL = a[1] / a[0], uyL = a[2] / a[0];
+    double uxR = b[1] / b[0], uyR = b[2] / b[0];
+    double h_avg = 0.5 * (a[0] + b[0]);
+    double h2_avg = 0.5 * (a[0] * a[0] + b[0] * b[0]);
+    double ux_avg = 0.5 * (uxL + uxR), uy_avg = 0.5 * (uyL + uyR);
+    double p = g * h_avg * h_avg - 0.5 * g * h2_avg;
+    double hu_avg = 0.5 * (a[1] + b[1]);
+    f[0] = hu_avg;
+    f[1] = hu_avg * ux_avg + p;
+    f[2] = hu_avg * uy_avg;
+}
+
+/* kernel_fluxdiff (nq = n) / kernel_fluxdiff_skew (nq < n): pass 1 j < nq over all
+ * rows, pass 2 j >= nq over rows i < nq; j outer, i inner. */
+void oracle_ratio_fluxdiff(int n, int nq, int K, const double *Q, const double *u, double g, double *y) {
+    for (int k = 0; k < K; ++k) {
+        const double *uk = u + (size_t)k * 3 * n;
+        double *yk = y + (size_t)k * 3 * n;
+        for (int x = 0; x < 3 * n; ++x) yk[x] = 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+            int j0 = pass == 0 ? 0 : nq, j1 = pass == 0 ? nq : n, i1 = pass == 0 ? n : nq;
+            for (int j = j0; j < j1; ++j) {
+                double uj[3] = {uk[j], uk[n + j], uk[2 * n + j]};
+                for (int i = 0; i < i1; ++i) {
+                    double ui[3] = {uk[i], uk[n + i], uk[2 * n + i]}, fs[3];
+                    ec_flux_x(ui, uj, g, fs);
+                    double q2 = 2.0 * Q[i + (size_t)j * n];
+                    yk[i] += q2 * fs[0];
+                    yk[n + i] += q2 * fs[1];
+                    yk[2 * n + i] += q2 * fs[2];
+                }
+            }
+        }
+    }
+}

@@ -133,6 +133,8 @@ def lib() -> C.CDLL:
     L.swedg_read_invariants_raw.argtypes = [vp, C.c_int, vp]
     L.swedg_run.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, _dp, _ip, _ip]
     L.swedg_exact_sum.argtypes = [_dp, C.c_size_t, _dp]
+    L.swedg_ratio_kernels.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.c_int,
+                                      _dp, _dp, _dp]
     _lib = L
     return L
 
@@ -147,7 +149,7 @@ EXPORTED = [
     "swedg_stage_volume", "swedg_stage_surface", "swedg_trace_device_ptr", "swedg_set_graphs",
     "swedg_set_diagnostics", "swedg_compute_invariants", "swedg_l2_error", "swedg_diag_raw_bytes",
     "swedg_diag_raw", "swedg_diag_from_raw", "swedg_sample_invariants", "swedg_read_invariants",
-    "swedg_read_invariants_raw", "swedg_run", "swedg_exact_sum",
+    "swedg_read_invariants_raw", "swedg_run", "swedg_exact_sum", "swedg_ratio_kernels",
 ]
 
 
@@ -445,6 +447,23 @@ def diag_from_raw(raws, n: int = 1) -> np.ndarray:
     if rc != SWEDG_OK:
         raise _err_class(rc)(rc, "swedg_diag_from_raw failed")
     return out
+
+
+def ratio_kernels(Q, u, *, g: float = 9.81, nq: int | None = None, mode: int = MODE_FAST, reps: int = 5,
+                  device: int = 0, outputs: bool = True):
+    """bench.hpp's study kernels on the device.  Q [n][n] stored column-major ([cols][rows]),
+    u [K][3][n].  Returns (t_dg_ms, t_esdg_ms, y_dg, y_esdg) (outputs None unless requested)."""
+    Q = _f64(Q)
+    u = _f64(u)
+    K, _, n = u.shape
+    y0 = np.zeros_like(u) if outputs else None
+    y1 = np.zeros_like(u) if outputs else None
+    t = np.zeros(2)
+    rc = lib().swedg_ratio_kernels(device, n, n if nq is None else int(nq), K, _p(Q), _p(u), float(g), int(mode),
+                                   int(reps), _p(y0), _p(y1), _p(t))
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, "swedg_ratio_kernels failed: " + lib().swedg_create_error().decode())
+    return float(t[0]), float(t[1]), y0, y1
 
 
 def exact_sum(x) -> float:

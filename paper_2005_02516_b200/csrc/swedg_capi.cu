@@ -8,6 +8,7 @@
 // launch, copy out and check the device error record.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +25,7 @@
 #include "modal_pair_n4.cuh"
 #include "sbp_kernels.cuh"
 #include "diag_kernels.cuh"
+#include "ratio_kernels.cuh"
 
 using namespace swedg;
 
@@ -1400,6 +1402,81 @@ int swedg_exact_sum(const double* x, size_t n, double* out) {
     }
     *out = exact::to_double(L);
     return SWEDG_OK;
+}
+
+int swedg_ratio_kernels(int device, int n, int nq, int K, const double* Q, const double* u, double g, int mode,
+                        int reps, double* y_dg, double* y_esdg, double* t_ms) {
+    if (n < 2 || n > kRatioThreads || nq < 1 || nq > n || K < 1 || !Q || !u || reps < 1 || !t_ms)
+        return SWEDG_ERR_INVALID;
+    if (cudaSetDevice(device) != cudaSuccess) return SWEDG_ERR_CUDA;
+    const size_t nu = (size_t)K * 3 * n;
+    double *dQ = nullptr, *du = nullptr, *dy0 = nullptr, *dy1 = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int rc = SWEDG_OK;
+    auto ok = [&](cudaError_t e) {
+        if (e != cudaSuccess && rc == SWEDG_OK)
+            rc = fail(nullptr, SWEDG_ERR_CUDA, std::string("swedg_ratio_kernels: ") + cudaGetErrorString(e));
+        return rc == SWEDG_OK;
+    };
+    if (ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) && ok(cudaMalloc(&dQ, sizeof(double) * n * n)) &&
+        ok(cudaMalloc(&du, sizeof(double) * nu)) && ok(cudaMalloc(&dy0, sizeof(double) * nu)) &&
+        ok(cudaMalloc(&dy1, sizeof(double) * nu)) && ok(cudaEventCreate(&ev[0])) && ok(cudaEventCreate(&ev[1])) &&
+        ok(cudaMemcpyAsync(dQ, Q, sizeof(double) * n * n, cudaMemcpyHostToDevice, st)) &&
+        ok(cudaMemcpyAsync(du, u, sizeof(double) * nu, cudaMemcpyHostToDevice, st))) {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        const int EB = n >= kRatioEBMinN ? kRatioEB : 1;
+        const int E = (kRatioThreads / n) * EB;  // elements per CTA tile
+        RatioParams p{n, nq, K, g, dQ, du, nullptr};
+        const bool parity = mode == SWEDG_MODE_PARITY;
+        auto kdg = parity ? (EB > 1 ? ratio_dg_kernel<true, kRatioEB> : ratio_dg_kernel<true, 1>)
+                          : (EB > 1 ? ratio_dg_kernel<false, kRatioEB> : ratio_dg_kernel<false, 1>);
+        auto kes = parity ? (EB > 1 ? ratio_esdg_kernel<true, kRatioEB> : ratio_esdg_kernel<true, 1>)
+                          : (EB > 1 ? ratio_esdg_kernel<false, kRatioEB> : ratio_esdg_kernel<false, 1>);
+        const size_t sm_dg = sizeof(double) * 4 * n * E, sm_es = sizeof(double) * 5 * n * E;
+        // the occupancy cache opts each kernel in once: use the largest staging size of any n
+        const size_t sm_max = sizeof(double) * 5 * kRatioThreads * kRatioEB;
+        const int occ_dg = kernel_occupancy(reinterpret_cast<const void*>(kdg), device, kRatioThreads, sm_max);
+        const int occ_es = kernel_occupancy(reinterpret_cast<const void*>(kes), device, kRatioThreads, sm_max);
+        const long blocks = ((long)K + E - 1) / E;
+        const int g_dg = (int)std::min<long>(blocks, (long)occ_dg * nsm);
+        const int g_es = (int)std::min<long>(blocks, (long)occ_es * nsm);
+        std::vector<float> tdg, tes;
+        for (int r = -2; r < reps && rc == SWEDG_OK; ++r) {  // 2 untimed warm-ups (bench.hpp:142-156)
+            float ms = 0.f;
+            p.y = dy0;
+            ok(cudaEventRecord(ev[0], st));
+            kdg<<<g_dg, kRatioThreads, sm_dg, st>>>(p);
+            ok(cudaEventRecord(ev[1], st));
+            ok(cudaEventSynchronize(ev[1]));
+            ok(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+            if (r >= 0) tdg.push_back(ms);
+            p.y = dy1;
+            ok(cudaEventRecord(ev[0], st));
+            kes<<<g_es, kRatioThreads, sm_es, st>>>(p);
+            ok(cudaEventRecord(ev[1], st));
+            ok(cudaEventSynchronize(ev[1]));
+            ok(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+            if (r >= 0) tes.push_back(ms);
+            ok(cudaGetLastError());
+        }
+        if (rc == SWEDG_OK) {
+            std::sort(tdg.begin(), tdg.end());
+            std::sort(tes.begin(), tes.end());
+            t_ms[0] = tdg[tdg.size() / 2];
+            t_ms[1] = tes[tes.size() / 2];
+            if (y_dg) ok(cudaMemcpyAsync(y_dg, dy0, sizeof(double) * nu, cudaMemcpyDeviceToHost, st));
+            if (y_esdg) ok(cudaMemcpyAsync(y_esdg, dy1, sizeof(double) * nu, cudaMemcpyDeviceToHost, st));
+            ok(cudaStreamSynchronize(st));
+        }
+    }
+    for (double* q : {dQ, du, dy0, dy1})
+        if (q) cudaFree(q);
+    for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+    return rc;
 }
 
 long long swedg_launch_count(swedg_handle h) { return h ? h->launches : 0; }

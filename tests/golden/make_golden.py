@@ -46,6 +46,8 @@ CASES = {
     "dam_n3": ["problem", "dambreak", "3", "hyb", "10", "0.0", "0.0625", "0.05", "1"],
     # test_solver.cpp:355-371 positivity failure in element 1
     "positivity": ["positivity"],
+    # bench.hpp volume-kernel cost study: matvec / fluxdiff / skew outputs, n = 6..50
+    "ratio": ["ratio"],
 }
 
 

@@ -54,6 +54,8 @@ def lib(precision: str = "double"):
         _lib.oracle_step_lsrk45.argtypes = [C.POINTER(OracleOps), _dp, _dp, C.c_double, C.c_int, _ip]
         _lib.oracle_rhs_subset.argtypes = [C.POINTER(OracleOps), _dp, _dp, _ip, C.c_int, _ip]
         _lib.oracle_rhs_from_proj_n.argtypes = [C.POINTER(OracleOps), _dp, C.c_int, _dp, _ip, C.c_int, _ip]
+        _lib.oracle_ratio_matvec.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double, _dp]
+        _lib.oracle_ratio_fluxdiff.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, _dp]
         _lib.oracle_project_nodal.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
         _lib.oracle_diag.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                      C.c_double, C.c_double, C.c_int, _dp, _dp, _dp, C.POINTER(C.c_long)]
@@ -222,6 +224,20 @@ def diag(fine, u_modal, *, what, b_modal=None, u_ref=None, t=0.0, g=0.0, vortex=
                             _p(f["map_coeffs"]), _p(u), _p(b), _p(ur), _p(vp), float(t), float(g), int(what),
                             _p(terms), _p(sums), C.byref(mh), C.byref(bad))
     return terms, sums, mh.value, err, bad.value
+
+
+def ratio_kernels(Q, u, g=9.81, nq=None):
+    """bench.hpp kernel_matvec and kernel_fluxdiff(_skew): Q [n][n] as stored ([cols][rows]),
+    u [K][3][n].  Returns (y_dg, y_esdg)."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    K, _, n = u.shape
+    y_dg = np.zeros((K, 3, n))
+    y_es = np.zeros((K, 3, n))
+    L = lib()
+    L.oracle_ratio_matvec(n, K, _p(Q), _p(u), float(g), _p(y_dg))
+    L.oracle_ratio_fluxdiff(n, n if nq is None else int(nq), K, _p(Q), _p(u), float(g), _p(y_es))
+    return y_dg, y_es
 
 
 def case_dict(c) -> dict:

@@ -164,3 +164,20 @@ def test_diagnostics_oracle_bitwise(name):
             assert err == 0
             e = np.r_[np.sqrt(s[:3]), np.sqrt(s[0] + s[1] + s[2])]
             np.testing.assert_array_equal(e, c[tag + key_l2])
+
+
+def test_ratio_oracle_bitwise():
+    """oracle_ratio_* == bench.hpp kernel_matvec / kernel_fluxdiff / kernel_fluxdiff_skew."""
+    from oracle_py import ratio_kernels
+
+    G = load_golden("ratio")
+    for n in G["sizes"]:
+        p = f"n{n}_"
+        dg, es = ratio_kernels(G[p + "Q"], G[p + "u"])
+        np.testing.assert_array_equal(dg, G[p + "y_dg"])
+        np.testing.assert_array_equal(es, G[p + "y_esdg"])
+        nq = int(G[p + "nq"][0])
+        Qz = np.array(G[p + "Q"], copy=True)
+        Qz[nq:, nq:] = 0.0
+        _, sk = ratio_kernels(Qz, G[p + "u"], nq=nq)
+        np.testing.assert_array_equal(sk, G[p + "y_skew"])
