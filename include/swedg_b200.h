@@ -141,6 +141,13 @@ int swedg_get_state(swedg_handle h, double* u, double* res, double* t);
 /* nsteps LSRK45 steps of size dt on the device-resident state (solver.hpp:466-484).
  * Stream-ordered; errors are checked (one device sync) when sync != 0. */
 int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync);
+/* The same steps on a HOST-resident state u_host [K][3][Np] (the reference's
+ * calling pattern: state.u lives on the host between steps).  Each step reads
+ * its input from u_host and writes its result back; the transfers are
+ * pipelined with the compute in `nchunks` element chunks (0 = 16): step n's D2H,
+ * step n+1's H2D (full duplex) and the element-local stage-1 volume kernel
+ * overlap.  u_host should be pinned.  Syncs and checks errors at the end. */
+int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps, int nchunks);
 /* Replay nsteps >= 2 as a captured one-step CUDA graph (default on; off while
  * per-kernel timers are enabled). */
 int swedg_set_graphs(swedg_handle h, int on);

@@ -133,6 +133,7 @@ def lib() -> C.CDLL:
     L.swedg_read_invariants_raw.argtypes = [vp, C.c_int, vp]
     L.swedg_run.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, _dp, _ip, _ip]
     L.swedg_exact_sum.argtypes = [_dp, C.c_size_t, _dp]
+    L.swedg_step_lsrk45_host.argtypes = [vp, _dp, C.c_double, C.c_int, C.c_int]
     L.swedg_ratio_kernels.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.c_int,
                                       _dp, _dp, _dp]
     _lib = L
@@ -150,6 +151,7 @@ EXPORTED = [
     "swedg_set_diagnostics", "swedg_compute_invariants", "swedg_l2_error", "swedg_diag_raw_bytes",
     "swedg_diag_raw", "swedg_diag_from_raw", "swedg_sample_invariants", "swedg_read_invariants",
     "swedg_read_invariants_raw", "swedg_run", "swedg_exact_sum", "swedg_ratio_kernels",
+    "swedg_step_lsrk45_host",
 ]
 
 
@@ -332,6 +334,13 @@ class Handle:
 
     def step(self, dt: float, nsteps: int = 1, sync: bool = True):
         self._check(self._lib.swedg_step_lsrk45(self._h, float(dt), int(nsteps), 1 if sync else 0))
+
+    def step_host(self, u, dt: float, nsteps: int = 1, nchunks: int = 0):
+        """nsteps LSRK45 steps on the host state u ([K][3][Np] float64, C-contiguous, updated
+        in place; pinned memory recommended): every step round-trips through u."""
+        if not (isinstance(u, np.ndarray) and u.dtype == np.float64 and u.flags.c_contiguous):
+            raise ValueError("u must be a C-contiguous float64 array (updated in place)")
+        self._check(self._lib.swedg_step_lsrk45_host(self._h, _p(u), float(dt), int(nsteps), int(nchunks)))
 
     def set_graphs(self, on: bool):
         self._check(self._lib.swedg_set_graphs(self._h, 1 if on else 0))

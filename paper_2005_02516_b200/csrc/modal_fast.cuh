@@ -147,7 +147,7 @@ modal_volume_fast_kernel(ModalVolParams prm) {
                     uq1 = __fma_rn(v, el[C::oU + Np + m], uq1);
                     uq2 = __fma_rn(v, el[C::oU + 2 * Np + m], uq2);
                 }
-                if (!(uq0 > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                if (!(uq0 > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                 const double vx = uq1 / uq0, vy = uq2 / uq0;
                 el[C::oV + i] = g * (uq0 + el[C::oBs + i]) - 0.5 * (vx * vx + vy * vy);
                 el[C::oV + nq + i] = vx;
@@ -190,7 +190,7 @@ modal_volume_fast_kernel(ModalVolParams prm) {
                     }
                 }
                 const double h = (vt0 + 0.5 * (vt1 * vt1 + vt2 * vt2)) / g - el[C::oBs + row];
-                if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                 const double U = h * vt1, V = h * vt2;
                 reinterpret_cast<double2*>(el + C::oA)[row] = make_double2(U, V);
                 reinterpret_cast<double2*>(el + C::oB)[row] = make_double2(U / h, V / h);

@@ -49,6 +49,7 @@ struct ModalVolParams {
     ErrRec* err;
     unsigned stage_id;
     int early_exit;
+    int k_base;         // global id of element 0 of this launch (chunked launches; error reports)
 };
 
 template <int N>
@@ -143,7 +144,7 @@ modal_volume_kernel(ModalVolParams prm) {
                 for (int m = 0; m < Np; ++m) s = A::fma(sVq[i + m * nq], el[S::su + c * Np + m], s);
                 uq[c] = s;
             }
-            if (!(uq[0] > 0.0)) record_error(prm.err, prm.stage_id, 0, base + e);
+            if (!(uq[0] > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + base + e);
             double vx = A::div(uq[1], uq[0]), vy = A::div(uq[2], uq[0]);
             el[S::sv + i] = A::sub(A::mul(g, A::add(uq[0], el[S::sbs + i])),
                                    A::mul(0.5, A::add(A::mul(vx, vx), A::mul(vy, vy))));
@@ -187,7 +188,7 @@ modal_volume_kernel(ModalVolParams prm) {
             }
             double h = A::sub(A::div(A::add(vt[0], A::mul(0.5, A::add(A::mul(vt[1], vt[1]), A::mul(vt[2], vt[2])))), g),
                               el[S::sbs + mi]);
-            if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+            if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
             hi = h;
             Ui = A::mul(h, vt[1]);
             Vi = A::mul(h, vt[2]);

@@ -187,7 +187,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             for (int q = 0; q < 2; ++q) {
                 const int i = q == 0 ? rA : rB;
                 if (i < nq) {
-                    if (valid && !(uq[q][0] > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                    if (valid && !(uq[q][0] > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                     const double inv = 1.0 / uq[q][0];
                     const double vx = uq[q][1] * inv, vy = uq[q][2] * inv;
                     work[W::wV + i] = g * (uq[q][0] + work[W::wBs + i]) - 0.5 * (vx * vx + vy * vy);
@@ -265,7 +265,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 r.g4 = d.y;
                 r.a0 = r.a1 = r.a2 = 0.0;
                 if (q < 2 || lp < 8) {
-                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                     reinterpret_cast<double2*>(work + W::wA)[row] = make_double2(r.U, r.V);
                     reinterpret_cast<double2*>(work + W::wB)[row] = make_double2(r.u, r.v);
                     work[W::wH + row] = h;

@@ -211,7 +211,7 @@ modal_volume_quad_n4_kernel(ModalVolParams prm) {
             for (int q = 0; q < 4; ++q) {
                 const int i = lp + 8 * q;
                 if (i < nq && valid) {
-                    if (!(uq[q][0] > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                    if (!(uq[q][0] > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                     const double inv = 1.0 / uq[q][0];
                     const double vx = uq[q][1] * inv, vy = uq[q][2] * inv;
                     work[Q::wV + i] = g * (uq[q][0] + sb[i]) - 0.5 * (vx * vx + vy * vy);
@@ -289,7 +289,7 @@ modal_volume_quad_n4_kernel(ModalVolParams prm) {
             for (int q = 0; q < 5; ++q) {
                 const int row = lp + 8 * q;
                 const double h = (vt[q][0] + 0.5 * (vt[q][1] * vt[q][1] + vt[q][2] * vt[q][2])) * ig - sb[row];
-                if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                 R[q].U = h * vt[q][1];
                 R[q].V = h * vt[q][2];
                 R[q].u = vt[q][1];

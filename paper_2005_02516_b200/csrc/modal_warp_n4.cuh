@@ -279,7 +279,7 @@ modal_volume_warp_n4_kernel(ModalVolParams prm) {
                     uq1 = __fma_rn(Vr[m], el[W::oU + Np + m], uq1);
                     uq2 = __fma_rn(Vr[m], el[W::oU + 2 * Np + m], uq2);
                 }
-                if (!(uq0 > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                if (!(uq0 > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                 const double inv = 1.0 / uq0;
                 const double vx = uq1 * inv, vy = uq2 * inv;
                 el[W::oV + lane] = g * (uq0 + el[W::oBs + lane]) - 0.5 * (vx * vx + vy * vy);
@@ -351,7 +351,7 @@ modal_volume_warp_n4_kernel(ModalVolParams prm) {
                 if (w == 1 && lane >= 8) break;
                 const int row = w == 0 ? lane : 32 + lane;
                 const double h = w == 0 ? hi : hB, U = w == 0 ? Ui : UB, V = w == 0 ? Vi : VB;
-                if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);
+                if (!(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                 reinterpret_cast<double2*>(el + W::oA)[row] = make_double2(U, V);
                 reinterpret_cast<double2*>(el + W::oB)[row] = w == 0 ? make_double2(ui, vi) : make_double2(uB, vB);
                 el[W::oH + row] = h;

@@ -85,6 +85,10 @@ struct swedg_handle_s {
     DiagRec* drec = nullptr;   // one-shot record
     DiagRec* series = nullptr; // run-loop samples
     int series_cap = 0;
+    // host-state stepping (swedg_step_lsrk45_host): copy streams + per-chunk events
+    cudaStream_t cp_in = nullptr, cp_out = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_out;
+    cudaEvent_t ev_step = nullptr;
     size_t dev_bytes = 0;
     bool bathy_set = false;
     unsigned next_stage = 1;
@@ -238,29 +242,34 @@ struct StageArgs {
     double* du_out;     // rhs mode
     unsigned stage_id;
     bool early_exit;
+    int k0 = 0, k1 = -1;  // volume part: element range [k0, k1) (k1 < 0: all K)
 };
 
 template <int N>
 int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     if (sa.parts & 1) {
     ModalVolParams vp;
-    vp.K = h->K;
+    const int k0 = sa.k0, k1 = sa.k1 < 0 ? h->K : sa.k1;
+    const size_t b = (size_t)k0;
+    const int nh = h->nh, Np = h->Np, nf = h->nf;
+    vp.K = k1 - k0;
     vp.g = h->g;
     vp.ops = h->ops;
-    vp.u = sa.u_in;
-    vp.gf = h->gf;
-    vp.bs = h->bs;
-    vp.src = h->src;
-    vp.trace = h->trace;
-    vp.accf = h->accf;
-    vp.T1 = h->T1;
-    vp.proj = sa.proj;
+    vp.u = sa.u_in + b * 3 * Np;
+    vp.gf = h->gf + b * 4 * nh;
+    vp.bs = h->bs + b * nh;
+    vp.src = h->src + b * 2 * nh;
+    vp.trace = h->trace + b * 3 * nf;
+    vp.accf = h->accf + b * 3 * nf;
+    vp.T1 = h->T1 + b * 3 * Np;
+    vp.proj = sa.proj ? sa.proj + b * 3 * nh : nullptr;
     vp.err = h->err;
     vp.stage_id = sa.stage_id;
     vp.early_exit = sa.early_exit ? 1 : 0;
+    vp.k_base = k0;
     using VC = VolCfg<N>;
     const size_t smem = VolSmem<N>::bytes(VC::E);
-    const int nblk_needed = (h->K + VC::E - 1) / VC::E;
+    const int nblk_needed = (vp.K + VC::E - 1) / VC::E;
     auto launch_vol = [&](void (*kern)(ModalVolParams)) -> int {
         int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, VC::T, smem);
         int grid = std::min(nblk_needed, occ * h->nsm);
@@ -276,19 +285,19 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
             auto kern = modal_volume_pair_n4_kernel;
             const size_t psm = PairN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
-            int grid = std::min((h->K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
+            int grid = std::min((vp.K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
             kern<<<std::max(grid, 1), PairN4::T, psm, h->stream>>>(vp);
         } else if (N == 4 && h->vol_variant == 4) {
             auto kern = modal_volume_quad_n4_kernel;
             const size_t qsm = QuadN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, QuadN4::T, qsm);
-            int grid = std::min((h->K + 4 * QuadN4::WARPS - 1) / (4 * QuadN4::WARPS), occ * h->nsm);
+            int grid = std::min((vp.K + 4 * QuadN4::WARPS - 1) / (4 * QuadN4::WARPS), occ * h->nsm);
             kern<<<std::max(grid, 1), QuadN4::T, qsm, h->stream>>>(vp);
         } else if (N == 4 && h->vol_variant == 3) {
             auto kern = modal_volume_warp_n4_kernel;
             const size_t wsm = WarpN4::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, WarpN4::T, wsm);
-            int grid = std::min((h->K + WarpN4::WARPS - 1) / WarpN4::WARPS, occ * h->nsm);
+            int grid = std::min((vp.K + WarpN4::WARPS - 1) / WarpN4::WARPS, occ * h->nsm);
             kern<<<std::max(grid, 1), WarpN4::T, wsm, h->stream>>>(vp);
         } else if (h->vol_variant == 2) {
             launch_vol(modal_volume_kernel<N, false>);
@@ -297,7 +306,7 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
             auto kern = modal_volume_fast_kernel<N>;
             const size_t fsm = FC::bytes();
             int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, FC::T, fsm);
-            int grid = std::min((h->K + FC::E - 1) / FC::E, occ * h->nsm);
+            int grid = std::min((vp.K + FC::E - 1) / FC::E, occ * h->nsm);
             kern<<<std::max(grid, 1), FC::T, fsm, h->stream>>>(vp);
         }
     }
@@ -807,6 +816,11 @@ int swedg_destroy(swedg_handle h) {
     }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    for (auto e : h->ev_in) cudaEventDestroy(e);
+    for (auto e : h->ev_out) cudaEventDestroy(e);
+    if (h->ev_step) cudaEventDestroy(h->ev_step);
+    if (h->cp_in) cudaStreamDestroy(h->cp_in);
+    if (h->cp_out) cudaStreamDestroy(h->cp_out);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return SWEDG_OK;
@@ -1477,6 +1491,82 @@ int swedg_ratio_kernels(int device, int n, int nq, int K, const double* Q, const
         if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
     return rc;
+}
+
+// The reference's step_lsrk45 on a HOST-resident state (solver.hpp:466-484 called
+// in a loop with state.u on the host): every step's input is read from u_host
+// and its result written back to u_host.  The copies are pipelined with the
+// compute in element chunks: the D2H of step n's chunk c, the H2D of step
+// n+1's chunk c (full duplex) and stage 1's element-local volume kernel on
+// chunk c overlap; the interface/update kernels and stages 2..5 run on the whole
+// mesh.  u_host should be pinned (cudaHostAlloc/cudaHostRegister).
+int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps, int nchunks) {
+    if (!h || !u_host) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    if (nsteps < 0) return fail(h, SWEDG_ERR_INVALID, "nsteps must be >= 0");
+    cudaSetDevice(h->device);
+    const size_t per = (size_t)3 * h->nstate();
+    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED || h->n_halo > 0) {  // unchunked: copy, step, copy
+        for (int n = 0; n < nsteps; ++n) {
+            CUDA_TRY(h, cudaMemcpyAsync(h->u, u_host, per * h->K * 8, cudaMemcpyHostToDevice, h->stream));
+            if (swedg_step_lsrk45(h, dt, 1, 0)) return h->last_code;
+            CUDA_TRY(h, cudaMemcpyAsync(u_host, h->u, per * h->K * 8, cudaMemcpyDeviceToHost, h->stream));
+        }
+        return check_errors(h);
+    }
+    int C = nchunks > 0 ? nchunks : 16;
+    C = std::max(1, std::min(C, std::min(64, h->K)));
+    if (!h->cp_in) {
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_in, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_out, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_step, cudaEventDisableTiming));
+    }
+    while ((int)h->ev_in.size() < C) {
+        cudaEvent_t a, b;
+        CUDA_TRY(h, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        h->ev_in.push_back(a);
+        h->ev_out.push_back(b);
+    }
+    auto lo = [&](int c) { return (int)((long)h->K * c / C); };
+    // the copy streams start after everything already queued on the handle stream
+    CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_step, 0));
+    for (int n = 0; n < nsteps; ++n) {
+        const double t0 = h->t;
+        for (int c = 0; c < C; ++c) {  // H2D of chunk c after the previous step's D2H of it
+            if (n > 0) CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_out[c], 0));
+            const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+            CUDA_TRY(h, cudaMemcpyAsync(h->u + a, u_host + a, (e - a) * 8, cudaMemcpyHostToDevice, h->cp_in));
+            CUDA_TRY(h, cudaEventRecord(h->ev_in[c], h->cp_in));
+        }
+        for (int s = 0; s < 5; ++s) {
+            const unsigned sid = new_stage(h, t0 + Lsrk45::c[s] * dt);
+            if (s == 0) {
+                for (int c = 0; c < C; ++c) {  // element-local volume kernel as the chunks land
+                    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
+                    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, sid, true,
+                                 lo(c), lo(c + 1)};
+                    if (run_stage(h, sa)) return h->last_code;
+                }
+                StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, sid, true};
+                if (run_stage(h, sa)) return h->last_code;
+            } else {
+                StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, sid, true};
+                if (run_stage(h, sa)) return h->last_code;
+            }
+        }
+        h->t = t0 + dt;
+        CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_step, 0));
+        for (int c = 0; c < C; ++c) {  // D2H of the step's result
+            const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+            CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
+            CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
+        }
+    }
+    if (nsteps > 0) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_out[C - 1], 0));
+    return check_errors(h);
 }
 
 long long swedg_launch_count(swedg_handle h) { return h ? h->launches : 0; }

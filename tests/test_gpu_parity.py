@@ -209,3 +209,31 @@ def test_graph_replay_equals_individual_launches_and_reports_step():
         h2.step(dt, 4)
     assert ei.value.elem == 7 and "element 7" in str(ei.value)
     assert abs(ei.value.t - 0.25) < 1e-12
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+@pytest.mark.parametrize("nchunks", [1, 3, 8])
+def test_host_state_stepping_equals_device_steps(mode, nchunks):
+    """swedg_step_lsrk45_host (state round-trips through host memory every step, copies
+    pipelined with chunked stage-1 volume kernels) == device-resident steps, bitwise;
+    errors keep the global element id and stage time across chunks and async steps."""
+    c = load_golden("c1_vortex")
+    m = capi.MODE_PARITY if mode == "parity" else capi.MODE_FAST
+    dt = float(c["dt"][0])
+    h1 = make(c, m)
+    h1.set_state(c["u"])
+    h1.step(dt, 3)
+    u1, _, t1 = h1.get_state()
+    h2 = make(c, m)
+    u = np.array(c["u"], copy=True)
+    h2.set_state(u)  # t = 0
+    h2.step_host(u, dt, 3, nchunks)
+    np.testing.assert_array_equal(u, u1)
+    _, _, t2 = h2.get_state()
+    assert t2 == t1
+    bad = np.array(c["u"], copy=True)
+    bad[400, 0, 0] = -1.0  # element 400 of 512: in the last chunks
+    h2.set_state(bad, None, 0.5)
+    with pytest.raises(capi.PositivityError) as ei:
+        h2.step_host(bad, dt, 2, nchunks)
+    assert ei.value.elem == 400 and abs(ei.value.t - 0.5) < 1e-12
