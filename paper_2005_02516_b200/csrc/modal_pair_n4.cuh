@@ -23,6 +23,38 @@
 
 namespace swedg {
 
+// One stacked row's state in the flux loops.  The EC-flux accumulation is
+// factored so a pair costs 17 FP64 instructions instead of 23: with
+// T = qx sU + qy sV (the mass-flux term, sU = hu_i + hu_j, sV = hv_i + hv_j),
+//   sum_j qx F1x + qy F1y = u_i sum_j T + sum_j u_j T + gh4_i sum_j qx h_j
+//   sum_j qx F2x + qy F2y = v_i sum_j T + sum_j v_j T + gh4_i sum_j qy h_j
+// (F1x = sU su + p4, F1y = sV su, F2x = sU sv, F2y = sV sv + p4, su = u_i + u_j,
+// p4 = gh4_i h_j), so the loops carry a0 = sum T, a1 = sum u_j T, a2 = sum v_j T,
+// b1 = sum qx h_j, b2 = sum qy h_j and row_finish adds the row-constant parts.
+struct Row6 {
+    double U, V, g1, g2, g3, g4;
+    double a0, a1, a2, b1, b2;
+};
+
+__device__ __forceinline__ void pair6(Row6& r, const double2 q, const double2 A, const double2 B, const double g1j,
+                                      const double g2j, const double g3j, const double g4j, const double hj) {
+    const double qx = __fma_rn(q.x, r.g1 + g1j, q.y * (r.g2 + g2j));
+    const double qy = __fma_rn(q.x, r.g3 + g3j, q.y * (r.g4 + g4j));
+    const double sU = r.U + A.x, sV = r.V + A.y;
+    const double T = __fma_rn(qx, sU, qy * sV);
+    r.a0 += T;
+    r.a1 = __fma_rn(B.x, T, r.a1);
+    r.a2 = __fma_rn(B.y, T, r.a2);
+    r.b1 = __fma_rn(qx, hj, r.b1);
+    r.b2 = __fma_rn(qy, hj, r.b2);
+}
+
+// row-constant parts of the factored accumulation (u_i, v_i, gh4_i = 2 g h_i)
+__device__ __forceinline__ void row_finish(Row6& r, const double ui, const double vi, const double gh4) {
+    r.a1 = __fma_rn(gh4, r.b1, __fma_rn(ui, r.a0, r.a1));
+    r.a2 = __fma_rn(gh4, r.b2, __fma_rn(vi, r.a0, r.a2));
+}
+
 struct PairN4 {
     static constexpr int Np = 15, nq = 25, nf = 15, nh = 40;
     static constexpr int WARPS = 16, T = WARPS * 32;
@@ -219,7 +251,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
         }
         __syncwarp();
         // ---- projected states at rows rA, rB, rC (rC only lanes l' < 8 store)
-        Row5 RA, RB, RC;
+        Row6 RA, RB, RC;
         {
             double vt[3][3] = {};
             {  // rows rA (doubles 0..14) and rB (15..29)
@@ -251,23 +283,20 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                     vt[2][2] = __fma_rn(c, work[W::wVh + 2 * Np + m], vt[2][2]);
                 }
             }
-            auto finish = [&](Row5& r, const int q, const int row) {
+            auto finish = [&](Row6& r, const int q, const int row) {
                 const double h = (vt[q][0] + 0.5 * (vt[q][1] * vt[q][1] + vt[q][2] * vt[q][2])) * ig - work[W::wBs + row];
                 r.U = h * vt[q][1];
                 r.V = h * vt[q][2];
-                r.u = vt[q][1];
-                r.v = vt[q][2];
-                r.gh4 = g2 * h;
                 const double2 c = nC[row], d = nD[row];
                 r.g1 = c.x;
                 r.g2 = c.y;
                 r.g3 = d.x;
                 r.g4 = d.y;
-                r.a0 = r.a1 = r.a2 = 0.0;
+                r.a0 = r.a1 = r.a2 = r.b1 = r.b2 = 0.0;
                 if (q < 2 || lp < 8) {
                     if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
                     reinterpret_cast<double2*>(work + W::wA)[row] = make_double2(r.U, r.V);
-                    reinterpret_cast<double2*>(work + W::wB)[row] = make_double2(r.u, r.v);
+                    reinterpret_cast<double2*>(work + W::wB)[row] = make_double2(vt[q][1], vt[q][2]);
                     work[W::wH + row] = h;
                     if (valid && row >= nq) {
                         double* tr = prm.trace + (size_t)k * 3 * nf + (row - nq);
@@ -299,13 +328,19 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                     const int j = par + 2 * (s0 + t);
                     if (s0 + t < 13 && j < nq) {
                         const double2 C = nC[j], D = nD[j];
-                        pair5(RC, qc[t], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
+                        pair6(RC, qc[t], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
                     }
                 }
             }
             RC.a0 += __shfl_xor_sync(0xffffffffu, RC.a0, 8);
             RC.a1 += __shfl_xor_sync(0xffffffffu, RC.a1, 8);
             RC.a2 += __shfl_xor_sync(0xffffffffu, RC.a2, 8);
+            RC.b1 += __shfl_xor_sync(0xffffffffu, RC.b1, 8);
+            RC.b2 += __shfl_xor_sync(0xffffffffu, RC.b2, 8);
+            {
+                const double2 uv = nB[rC];
+                row_finish(RC, uv.x, uv.y, g2 * nH[rC]);
+            }
             if (valid && lp < 8) {
                 double* af = prm.accf + (size_t)k * 3 * nf + (rC - nq);
                 af[0] = 2.0 * RC.a0;
@@ -324,17 +359,22 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 const int j = j0 + p;
                 const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
                 const double hj = nH[j];
-                pair5(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
-                pair5(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
+                pair6(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
+                pair6(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
             }
         }
         {
             const double2 qa = tmem_ld4(tbase + W::tA + 4 * 24), qb = tmem_ld4(tbase + W::tB + 4 * 24);
             const double2 A = nA[24], B = nB[24], C = nC[24], D = nD[24];
-            pair5(RA, qa, A, B, C.x, C.y, D.x, D.y, nH[24]);
-            pair5(RB, qb, A, B, C.x, C.y, D.x, D.y, nH[24]);
+            pair6(RA, qa, A, B, C.x, C.y, D.x, D.y, nH[24]);
+            pair6(RB, qb, A, B, C.x, C.y, D.x, D.y, nH[24]);
         }
         // rows 25..31 (rB for l' >= 9) are complete surface rows
+        const bool bvol = rB < nq;
+        if (!bvol) {
+            const double2 uv = nB[rB];
+            row_finish(RB, uv.x, uv.y, g2 * nH[rB]);
+        }
         if (valid && rB >= nq) {
             double* af = prm.accf + (size_t)k * 3 * nf + (rB - nq);
             af[0] = 2.0 * RB.a0;
@@ -342,7 +382,6 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             af[2 * nf] = RB.a2;
         }
         // ---- loop C: volume rows rA (all), rB (l' <= 8) x surface columns 25..39
-        const bool bvol = rB < nq;
 #pragma unroll 1
         for (int j0 = nq; j0 < nh; j0 += 4) {
             double2 qa[4], qb[4];
@@ -354,10 +393,18 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 if (j < nh) {
                     const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
                     const double hj = nH[j];
-                    pair5(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
-                    if (bvol) pair5(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
+                    pair6(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
+                    if (bvol) pair6(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
                 }
             }
+        }
+        {
+            const double2 uv = nB[rA];
+            row_finish(RA, uv.x, uv.y, g2 * nH[rA]);
+        }
+        if (bvol) {
+            const double2 uv = nB[rB];
+            row_finish(RB, uv.x, uv.y, g2 * nH[rB]);
         }
         // ---- stacked = src - acc on volume rows, then T1 = Vq^T stacked
         {
@@ -366,7 +413,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int row = q == 0 ? rA : rB;
-                const Row5& r = q == 0 ? RA : RB;
+                const Row6& r = q == 0 ? RA : RB;
                 if (row < nq) {
                     const double mgh = -g * nH[row];
                     stk[row] = -2.0 * r.a0;
