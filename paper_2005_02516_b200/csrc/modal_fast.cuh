@@ -40,14 +40,17 @@ struct VolFastCfg {
     static constexpr int stride = ((len + 13) / 16) * 16 + 2;  // == 2 (mod 16): 16 B bank shift
     static constexpr int ops_len = ((nq * Np + nf * Np + Np * nq + 1) / 2) * 2 + 2 * nh * nh;
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)E * stride); }
-    static_assert(X * G * 3 <= 6 * Np, "partials must fit the scratch region");
+    static_assert(X * G * 5 <= 6 * Np + 3 * nq, "partials must fit the scratch region");
 };
 
 // Two-row EC flux-differencing update for one column j (reassociated form:
-// p = g/2 h_i h_j, qx/qy carry the 1/4, acc0 carries a final factor 2).
+// p = g/2 h_i h_j, qx/qy carry the 1/4, acc0 carries a final factor 2), with the
+// factored accumulation of modal_pair_n4.cuh (Row6): a0 = sum T, a1 = sum u_j T,
+// a2 = sum v_j T, b1 = sum qx h_j, b2 = sum qy h_j; finish_row adds the
+// row-constant parts u_i a0 + gh4_i b1 and v_i a0 + gh4_i b2.
 struct RowState {
     double h, U, V, u, v, g1, g2, g3, g4, gh4;
-    double a0, a1, a2;
+    double a0, a1, a2, b1, b2;
 };
 
 __device__ __forceinline__ void pair_update(RowState& r, const double2 q, const double2 A, const double2 B,
@@ -55,16 +58,17 @@ __device__ __forceinline__ void pair_update(RowState& r, const double2 q, const 
     const double qx = __fma_rn(q.x, r.g1 + Cg.x, q.y * (r.g2 + Cg.y));
     const double qy = __fma_rn(q.x, r.g3 + Dg.x, q.y * (r.g4 + Dg.y));
     const double sU = r.U + A.x, sV = r.V + A.y;
-    const double su = r.u + B.x, sv = r.v + B.y;
-    const double p4 = r.gh4 * hj;
-    const double F1x = __fma_rn(sU, su, p4), F2x = sU * sv;
-    const double F1y = sV * su, F2y = __fma_rn(sV, sv, p4);
-    r.a0 = __fma_rn(qx, sU, r.a0);
-    r.a0 = __fma_rn(qy, sV, r.a0);
-    r.a1 = __fma_rn(qx, F1x, r.a1);
-    r.a1 = __fma_rn(qy, F1y, r.a1);
-    r.a2 = __fma_rn(qx, F2x, r.a2);
-    r.a2 = __fma_rn(qy, F2y, r.a2);
+    const double T = __fma_rn(qx, sU, qy * sV);
+    r.a0 += T;
+    r.a1 = __fma_rn(B.x, T, r.a1);
+    r.a2 = __fma_rn(B.y, T, r.a2);
+    r.b1 = __fma_rn(qx, hj, r.b1);
+    r.b2 = __fma_rn(qy, hj, r.b2);
+}
+
+__device__ __forceinline__ void finish_row(RowState& r) {
+    r.a1 = __fma_rn(r.gh4, r.b1, __fma_rn(r.u, r.a0, r.a1));
+    r.a2 = __fma_rn(r.gh4, r.b2, __fma_rn(r.v, r.a0, r.a2));
 }
 
 template <int N>
@@ -212,8 +216,8 @@ modal_volume_fast_kernel(ModalVolParams prm) {
         __syncthreads();
         // ---- flux differencing
         RowState A, B;
-        A.a0 = A.a1 = A.a2 = 0.0;
-        B.a0 = B.a1 = B.a2 = 0.0;
+        A.a0 = A.a1 = A.a2 = A.b1 = A.b2 = 0.0;
+        B.a0 = B.a1 = B.a2 = B.b1 = B.b2 = 0.0;
         if (act) {
             load_row<N>(A, el, ra, g);
             load_row<N>(B, el, rb, g);
@@ -232,12 +236,14 @@ modal_volume_fast_kernel(ModalVolParams prm) {
             }
             // surface rows are complete after pass 1
             if (ra >= nq) {
+                finish_row(A);
                 double* af = prm.accf + (size_t)k * 3 * nf + (ra - nq);
                 af[0] = 2.0 * A.a0;
                 af[nf] = A.a1;
                 af[2 * nf] = A.a2;
             }
             if (rb >= nq) {
+                finish_row(B);
                 double* af = prm.accf + (size_t)k * 3 * nf + (rb - nq);
                 af[0] = 2.0 * B.a0;
                 af[nf] = B.a1;
@@ -248,6 +254,7 @@ modal_volume_fast_kernel(ModalVolParams prm) {
 #pragma unroll 5
                 for (int j = nq; j < nh; ++j)
                     pair_update(A, sQP[j * nh + ra], nA[j], nB[j], nC[j], nD[j], nH[j]);
+                finish_row(A);
             }
             if constexpr (X > 0) {
                 // the X upper-half volume rows: column groups spread over all threads
@@ -256,7 +263,7 @@ modal_volume_fast_kernel(ModalVolParams prm) {
                     const int row = R + x;
                     if (grp > 0) {  // helper: fresh partial for row R+x
                         load_row<N>(B, el, row, g);
-                        B.a0 = B.a1 = B.a2 = 0.0;
+                        B.a0 = B.a1 = B.a2 = B.b1 = B.b2 = 0.0;
                     }
                     for (int j = nq + grp; j < nh; j += G)
                         pair_update(B, sQP[j * nh + row], nA[j], nB[j], nC[j], nD[j], nH[j]);
@@ -268,18 +275,23 @@ modal_volume_fast_kernel(ModalVolParams prm) {
             double* part = el + C::oU;
             if (act && t < G * X && t >= X) {
                 const int x = t % X, grp = t / X;
-                part[(x * G + grp) * 3 + 0] = B.a0;
-                part[(x * G + grp) * 3 + 1] = B.a1;
-                part[(x * G + grp) * 3 + 2] = B.a2;
+                part[(x * G + grp) * 5 + 0] = B.a0;
+                part[(x * G + grp) * 5 + 1] = B.a1;
+                part[(x * G + grp) * 5 + 2] = B.a2;
+                part[(x * G + grp) * 5 + 3] = B.b1;
+                part[(x * G + grp) * 5 + 4] = B.b2;
             }
             __syncthreads();
             if (act && t < X) {
 #pragma unroll
                 for (int grp = 1; grp < G; ++grp) {
-                    B.a0 += part[(t * G + grp) * 3 + 0];
-                    B.a1 += part[(t * G + grp) * 3 + 1];
-                    B.a2 += part[(t * G + grp) * 3 + 2];
+                    B.a0 += part[(t * G + grp) * 5 + 0];
+                    B.a1 += part[(t * G + grp) * 5 + 1];
+                    B.a2 += part[(t * G + grp) * 5 + 2];
+                    B.b1 += part[(t * G + grp) * 5 + 3];
+                    B.b2 += part[(t * G + grp) * 5 + 4];
                 }
+                finish_row(B);
             }
             __syncthreads();  // partials consumed before the stacked rows overwrite them
         }

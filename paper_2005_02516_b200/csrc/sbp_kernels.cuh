@@ -153,24 +153,26 @@ sbp_rhs_kernel(SbpParams prm) {
             acc2 = A::add(acc2, A::mul(2.0, A::add(A::mul(qx, fx2), A::mul(qy, fy2))));
         }
     } else {
+        // factored accumulation (modal_pair_n4.cuh Row6): T = qx sU + qy sV,
+        // acc1 = u_i sum T + sum u_j T + gh4_i sum qx h_j (and likewise acc2)
         const double gh4i = 2.0 * g * hi;
+        double b1 = 0.0, b2 = 0.0;
 #pragma unroll 4
         for (int j = 0; j < nq; ++j) {
             const double ax = sQA[mi + j * nq], bx = sQB[mi + j * nq];
             const double qx = __fma_rn(ax, g1i + G1[j], bx * (g2i + G2[j]));
             const double qy = __fma_rn(ax, g3i + G3[j], bx * (g4i + G4[j]));
             const double sU = Ui + HU[j], sV = Vi + HV[j];
-            const double su = ui + Uv[j], sv = vi + Vv[j];
-            const double p4 = gh4i * Hh[j];
-            const double F1x = __fma_rn(sU, su, p4), F2x = sU * sv;
-            const double F1y = sV * su, F2y = __fma_rn(sV, sv, p4);
-            acc0 = __fma_rn(qx, sU, acc0);
-            acc0 = __fma_rn(qy, sV, acc0);
-            acc1 = __fma_rn(qx, F1x, acc1);
-            acc1 = __fma_rn(qy, F1y, acc1);
-            acc2 = __fma_rn(qx, F2x, acc2);
-            acc2 = __fma_rn(qy, F2y, acc2);
+            const double T = __fma_rn(qx, sU, qy * sV);
+            const double hj = Hh[j];
+            acc0 += T;
+            acc1 = __fma_rn(Uv[j], T, acc1);
+            acc2 = __fma_rn(Vv[j], T, acc2);
+            b1 = __fma_rn(qx, hj, b1);
+            b2 = __fma_rn(qy, hj, b2);
         }
+        acc1 = __fma_rn(gh4i, b1, __fma_rn(ui, acc0, acc1));
+        acc2 = __fma_rn(gh4i, b2, __fma_rn(vi, acc0, acc2));
         acc0 *= 2.0;
     }
     // surface term: slot i with face_index[i] == mi (unique per node)
