@@ -385,9 +385,9 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
     using C = SbpCfg<N>;
     const size_t smem = SbpSmem<N>::bytes(C::E);
     const int grid = (h->K + C::E - 1) / C::E;
-    auto go = [&](void (*kern)(SbpParams)) {
-        kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, C::T, smem);
-        kern<<<grid, C::T, smem, h->stream>>>(sp);
+    auto go = [&](void (*kern)(SbpParams)) {  // persistent: resident CTAs x SMs
+        const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, C::T, smem);
+        kern<<<std::max(1, std::min(grid, occ * h->nsm)), C::T, smem, h->stream>>>(sp);
     };
     {
         KTimer kt(h, 0);
@@ -781,7 +781,18 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
         for (size_t k = 0; k < K; ++k)
             for (int i = 0; i < nq; ++i) minv[k * nq + i] = 1.0 / (d->M_diag[i] * d->J_vol[k * nq + i]);  // :357
         if (dalloc(h, &h->Minv, K * nq) || upload(h, h->Minv, minv.data(), K * nq)) return bail(h->last_code);
-        if (dalloc(h, &h->fidx, nf) || upload(h, h->fidx, d->face_index, nf)) return bail(h->last_code);
+        // face_index (nf) followed by its inverse: the surface slot of each node (-1: interior)
+        std::vector<int> fx(d->face_index, d->face_index + nf);
+        fx.resize(nf + nq, -1);
+        for (int i = 0; i < nf; ++i) {
+            const int v = d->face_index[i];
+            if (v < 0 || v >= nq || fx[nf + v] != -1) {
+                fail(h, SWEDG_ERR_INVALID, "face_index must map surface slots to distinct volume nodes");
+                return bail(SWEDG_ERR_INVALID);
+            }
+            fx[nf + v] = i;
+        }
+        if (dalloc(h, &h->fidx, fx.size()) || upload(h, h->fidx, fx.data(), fx.size())) return bail(h->last_code);
         if (dalloc(h, &h->src, K * 2 * nq)) return bail(h->last_code);
     }
     const size_t ns = K * 3 * h->nstate();
