@@ -55,6 +55,29 @@ __device__ __forceinline__ void row_finish(Row6& r, const double ui, const doubl
     r.a2 = __fma_rn(gh4, r.b2, __fma_rn(vi, r.a0, r.a2));
 }
 
+// Fused stage launch (opt-in, SWEDG_FUSION=1): the interface/lift/M^-1/RK-update
+// phase of stage s-1 (the arithmetic of modal_surface_kernel<4,false>) followed,
+// for the same element pair in the same warp, by the projection + volume phase of
+// stage s; the updated u feeds the projection from shared memory and a step needs
+// 6 launches instead of 10.  Traces are double-buffered by stage parity.  The
+// hoped-for overlap of the memory-bound interface phase with other warps' FP64
+// work does not happen (measured 2 % slower at C4): the volume phase needs every
+// warp slot to keep the FP64 pipe at 65 %, and the warps stay phase-locked.
+struct PairStageParams {
+    ModalVolParams v;          // volume phase, stage s (v.u read only when !do_surface)
+    int do_surface, do_volume;
+    int lf;
+    const double* trace_in;    // [K][3][nf] traces of stage s-1
+    const double* surf;        // [K][3][nf]: w*sJ, nx, ny
+    const int* nbr;            // [K][3]
+    const int* perm;           // [K][nf]
+    const double* Mpk;         // [K][120] packed symmetric M_h^{-1}
+    double* u;                 // state, updated by the interface phase
+    double* res;               // LSRK register
+    double rk_a, rk_b, dt;     // stage s-1 coefficients
+    unsigned stage_prev;       // stage id of s-1 (non-finite RHS reports)
+};
+
 struct PairN4 {
     static constexpr int Np = 15, nq = 25, nf = 15, nh = 40;
     static constexpr int WARPS = 16, T = WARPS * 32;
@@ -76,20 +99,25 @@ struct PairN4 {
     static constexpr int stage_stride = 246;  // staging per element: u[45](+1) | gf[160] | b[40]
     static constexpr int sU = 0, sG = 46, sB = 206;
     static constexpr int per_warp = 2 * work_stride + 2 * stage_stride;
-    static constexpr int ops_len = 376;       // Vq (25 x 15, col-major) for the lift, +1 pad
+    static constexpr int ops_len = 376 + 226; // Vq (25 x 15) for the volume lift, Vf (15 x 15) for the surface lift
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
 };
 
+// S = true: the fused interface+volume instantiation (ps.do_surface / ps.do_volume
+// select the phases); S = false: the volume-only kernel of the split stage.
+template <bool S>
 __global__ void __launch_bounds__(PairN4::T, 1)
-modal_volume_pair_n4_kernel(ModalVolParams prm) {
+modal_volume_pair_n4_kernel(PairStageParams ps) {
     using W = PairN4;
     using O = ModalOps<4>;
-    constexpr int Np = W::Np, nq = W::nq, nf = W::nf, nh = W::nh;
+    constexpr int Np = W::Np, nq = W::nq, nf = W::nf, nh = W::nh, npf = 5;
+    const ModalVolParams& prm = ps.v;
     if (prm.early_exit && error_pending(prm.err)) return;
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
-    double* sVq = smem;  // 25 x 15
+    double* sVq = smem;         // 25 x 15
+    double* sVf = smem + 376;   // 15 x 15
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int half = lane >> 4, lp = lane & 15;
     double* wbase = smem + W::ops_len + warp * W::per_warp;
@@ -103,6 +131,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
 
     // ---- CTA setup
     for (int x = threadIdx.x; x < nq * Np; x += W::T) sVq[x] = prm.ops[O::Vq + x];
+    for (int x = threadIdx.x; x < nf * Np; x += W::T) sVf[x] = prm.ops[O::Vf + x];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_addr_u32(&tmem_base_sh)),
@@ -146,12 +175,16 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
     const int npairs = (prm.K + 1) / 2;
     const int gw = blockIdx.x * W::WARPS + warp, nw = gridDim.x * W::WARPS;
 
+    const bool do_surface = S && ps.do_surface;
+    const bool do_volume = !S || ps.do_volume;
+    const bool with_u = !do_surface;  // otherwise u comes from the interface phase
     auto issue = [&](int pr) {
         const int k0 = 2 * pr;
-        if (k0 + 1 < prm.K) {
+        if (!do_volume) {
+        } else if (k0 + 1 < prm.K) {
             // u: 2 x 45 doubles (8 B granules: element blocks are 246 apart)
             const double* gu = prm.u + (size_t)k0 * 3 * Np;
-            for (int x = lane; x < 90; x += 32) {
+            for (int x = lane; with_u && x < 90; x += 32) {
                 const int e = x / 45, r = x - e * 45;
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sU + r)),
                              "l"(gu + x)
@@ -169,7 +202,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 cp_async16(stage + e * W::stage_stride + W::sB + r, gb + 2 * x);
             }
         } else if (k0 < prm.K) {  // odd K: last element alone
-            for (int r = lane; r < 45; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
+            for (int r = lane; with_u && r < 45; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
             for (int r = lane; r < 160; r += 32) stage[W::sG + r] = prm.gf[(size_t)k0 * 160 + r];
             for (int r = lane; r < 40; r += 32) stage[W::sB + r] = prm.bs[(size_t)k0 * 40 + r];
         }
@@ -183,9 +216,9 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
         cp_async_wait_all();
         __syncwarp();
         // ---- park: staging -> work (u, b, g pairs), freeing the staging for the next pair
-        {
+        if (do_volume) {
             const double* st = stage + half * W::stage_stride;
-            for (int r = lp; r < 45; r += 16) work[W::wU + r] = st[W::sU + r];
+            for (int r = lp; with_u && r < 45; r += 16) work[W::wU + r] = st[W::sU + r];
             for (int r = lp; r < 40; r += 16) {
                 work[W::wBs + r] = st[W::sB + r];
                 reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(st[W::sG + r], st[W::sG + nh + r]);
@@ -195,6 +228,123 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
         }
         __syncwarp();
         if (pr + nw < npairs) issue(pr + nw);
+
+        // ---- interface phase of stage s-1 (modal_surface_kernel<4,false> arithmetic):
+        //      lane l' < 15 = surface slot l' and modal coefficient l' of its element
+        if (do_surface) {
+            const double gS = prm.g;
+            const int s_ = lp < nf ? lp : nf - 1;
+            const bool act = valid && lp < nf;
+            // front-load every independent global read of the lane
+            double ui[3] = {1.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, t1r[3] = {0.0, 0.0, 0.0};
+            double ur[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0};
+            double m = 0.0, nxi = 0.0, nyi = 0.0, srx = 0.0, sry = 0.0;
+            int nb = -1, jn = 0;
+            if (act) {
+                const size_t ot = (size_t)k * 3 * nf + s_;
+                const size_t om = (size_t)k * 3 * Np + s_;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    ui[c] = ps.trace_in[ot + c * nf];
+                    acc[c] = prm.accf[ot + c * nf];
+                    t1r[c] = prm.T1[om + c * Np];
+                    ur[c] = ps.u[om + c * Np];
+                    rr[c] = ps.res[om + c * Np];
+                }
+                m = ps.surf[ot];
+                nxi = ps.surf[ot + nf];
+                nyi = ps.surf[ot + 2 * nf];
+                srx = prm.src[(size_t)k * 2 * nh + nq + s_];
+                sry = prm.src[(size_t)k * 2 * nh + nh + nq + s_];
+                nb = ps.nbr[(size_t)k * 3 + s_ / npf];
+                jn = ps.perm[(size_t)k * nf + s_];
+            }
+            // packed M_h^{-1} of the pair (2 x 120 contiguous doubles) -> work[wV..]
+            {
+                const int k0 = 2 * pr;
+                const int ne = k0 + 1 < prm.K ? 2 : 1;
+                const double* gm = ps.Mpk + (size_t)k0 * 120;
+                double* w0 = wbase;
+                for (int x = lane; x < ne * 120; x += 32) {
+                    const int e = x >= 120, r = x - 120 * e;
+                    w0[e * W::work_stride + W::wV + r] = gm[x];
+                }
+            }
+            double up[3] = {ui[0], ui[1], ui[2]};
+            if (act) {
+                if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
+                    const double un = ui[1] * nxi + ui[2] * nyi;
+                    up[1] = ui[1] - 2.0 * un * nxi;
+                    up[2] = ui[2] - 2.0 * un * nyi;
+                } else {
+                    const double* tn = ps.trace_in + (size_t)nb * 3 * nf + jn;
+                    up[0] = tn[0];
+                    up[1] = tn[nf];
+                    up[2] = tn[2 * nf];
+                }
+                const double Bx = m * nxi, By = m * nyi;
+                {  // ec_flux_xy(u+, u)
+                    const double uxa = up[1] / up[0], uya = up[2] / up[0];
+                    const double uxb = ui[1] / ui[0], uyb = ui[2] / ui[0];
+                    const double h_avg = 0.5 * (up[0] + ui[0]);
+                    const double p = gS * h_avg * h_avg - 0.25 * gS * (up[0] * up[0] + ui[0] * ui[0]);
+                    const double ux = 0.5 * (uxa + uxb), uy = 0.5 * (uya + uyb);
+                    const double hu = 0.5 * (up[1] + ui[1]), hv = 0.5 * (up[2] + ui[2]);
+                    const double fx[3] = {hu, hu * ux + p, hu * uy};
+                    const double fy[3] = {hv, hv * ux, hv * uy + p};
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[c] = acc[c] + (Bx * fx[c] + By * fy[c]);
+                }
+                if (ps.lf) {  // lf_penalty(u, u+) (swe.hpp:87-99)
+                    const double wl = fabs((ui[1] * nxi + ui[2] * nyi) / ui[0]) + sqrt(gS * ui[0]);
+                    const double wr = fabs((up[1] * nxi + up[2] * nyi) / up[0]) + sqrt(gS * up[0]);
+                    const double lam = (wl < wr) ? wr : wl;
+                    const double hl = 0.5 * lam;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[c] = acc[c] - m * (hl * (up[c] - ui[c]));
+                }
+                const double mgh = -gS * ui[0];
+                work[W::wA + s_] = 0.0 - acc[0];
+                work[W::wA + nf + s_] = mgh * srx - acc[1];
+                work[W::wA + 2 * nf + s_] = mgh * sry - acc[2];
+            }
+            __syncwarp();
+            // modal = T1 + Vf^T stacked_surface (solver.hpp:285-286)
+            if (act) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double t2 = 0.0;
+#pragma unroll
+                    for (int i = 0; i < nf; ++i) t2 = __fma_rn(sVf[i + s_ * nf], work[W::wA + c * nf + i], t2);
+                    work[W::wB + c * Np + s_] = t1r[c] + t2;
+                }
+            }
+            __syncwarp();
+            // du = M_h^{-1} modal; finiteness; LSRK45 register update
+            if (act) {
+                double du[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int mm = 0; mm < Np; ++mm) {
+                    const int a = s_ < mm ? s_ : mm, b = s_ < mm ? mm : s_;
+                    const double mv = work[W::wV + a * Np - a * (a - 1) / 2 + (b - a)];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) du[c] = __fma_rn(mv, work[W::wB + c * Np + mm], du[c]);
+                }
+                if (!(isfinite(du[0]) && isfinite(du[1]) && isfinite(du[2])))
+                    record_error(prm.err, ps.stage_prev, 1, prm.k_base + k);
+                const size_t om = (size_t)k * 3 * Np + s_;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double r = __fma_rn(ps.rk_a, rr[c], ps.dt * du[c]);
+                    const double un = __fma_rn(ps.rk_b, r, ur[c]);
+                    ps.res[om + c * Np] = r;
+                    ps.u[om + c * Np] = un;
+                    work[W::wU + c * Np + s_] = un;
+                }
+            }
+            __syncwarp();
+        }
+        if (!do_volume) continue;
 
         // ---- entropy variables at volume points rA (all) and rB (< 25)
         {

@@ -70,6 +70,12 @@ struct swedg_handle_s {
     double* du = nullptr;    // host-API scratch rhs
     double* proj = nullptr;  // host-API scratch projection
     double* trace = nullptr; // [K][3][nf]
+    double* trace2 = nullptr; // second trace buffer (fused stage chain: traces double-buffered by stage parity)
+    // FAST N=4 single rank: fused interface(s-1) + volume(s) launches, opt-in (env
+    // SWEDG_FUSION=1).  Measured 2 % slower than the split launches at C4 (39.6 vs
+    // 38.8 ms/step): the interface phase takes warp slots the FP64-latency-bound
+    // volume phase needs, and the warps stay phase-locked, so nothing overlaps.
+    bool fusion = false;
     double* accf = nullptr;  // [K][3][nf]
     double* T1 = nullptr;    // [K][3][Np]
     ErrRec* err = nullptr;
@@ -105,6 +111,7 @@ struct swedg_handle_s {
     cudaStream_t graph_stream = nullptr;
     int graph_mode = -1, graph_penalty = -1;
     unsigned graph_base = 0;
+    long long graph_nodes = 11;  // kernels in the captured step
     bool use_graphs = true;
     // per-kernel-class event timers
     bool timers = false;
@@ -233,6 +240,14 @@ int kernel_occupancy(const void* kern, int device, int threads, size_t smem) {
     return occ;
 }
 
+void launch_pair(swedg_handle h, const PairStageParams& ps) {
+    auto kern = ps.do_surface ? modal_volume_pair_n4_kernel<true> : modal_volume_pair_n4_kernel<false>;
+    const size_t psm = PairN4::bytes();
+    const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
+    const int grid = std::min((ps.v.K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
+    kern<<<std::max(grid, 1), PairN4::T, psm, h->stream>>>(ps);
+}
+
 struct StageArgs {
     const double* u_in;
     int parts = 3;  // bit 0: volume kernel, bit 1: surface/update kernel
@@ -282,11 +297,11 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         if (h->mode == SWEDG_MODE_PARITY) {
             launch_vol(modal_volume_kernel<N, true>);
         } else if (N == 4 && h->vol_variant == 0) {
-            auto kern = modal_volume_pair_n4_kernel;
-            const size_t psm = PairN4::bytes();
-            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
-            int grid = std::min((vp.K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
-            kern<<<std::max(grid, 1), PairN4::T, psm, h->stream>>>(vp);
+            PairStageParams ps{};
+            ps.v = vp;
+            ps.do_surface = 0;
+            ps.do_volume = 1;
+            launch_pair(h, ps);
         } else if (N == 4 && h->vol_variant == 4) {
             auto kern = modal_volume_quad_n4_kernel;
             const size_t qsm = QuadN4::bytes();
@@ -422,6 +437,107 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+int run_stage(swedg_handle h, const StageArgs& sa);
+
+// FAST N=4 single-rank fused chain (modal_pair_n4.cuh PairStageParams).
+bool fused_path(swedg_handle h) {
+    return h->fusion && h->mode == SWEDG_MODE_FAST && h->scheme == SWEDG_SCHEME_HYBRIDIZED && h->N == 4 &&
+           h->vol_variant == 0 && h->n_halo == 0 && !h->timers;
+}
+
+int ensure_trace2(swedg_handle h) {
+    if (!h->trace2 && dalloc(h, &h->trace2, (size_t)h->K * 3 * h->nf)) return h->last_code;
+    return SWEDG_OK;
+}
+
+// Stages 1..4 as fused launches [interface(s-1) + volume(s)] and the final
+// interface/update of stage 4, after stage 0's volume kernel wrote its traces to
+// h->trace (buffer 0).  Stage s writes traces to buffer s % 2.
+int run_fused_tail(swedg_handle h, const unsigned* ids, double dt) {
+    if (ensure_trace2(h)) return h->last_code;
+    double* buf[2] = {h->trace, h->trace2};
+    for (int s = 1; s < 5; ++s) {
+        PairStageParams ps{};
+        ModalVolParams& vp = ps.v;
+        vp.K = h->K;
+        vp.g = h->g;
+        vp.ops = h->ops;
+        vp.u = h->u;
+        vp.gf = h->gf;
+        vp.bs = h->bs;
+        vp.src = h->src;
+        vp.trace = buf[s & 1];
+        vp.accf = h->accf;
+        vp.T1 = h->T1;
+        vp.proj = nullptr;
+        vp.err = h->err;
+        vp.stage_id = ids[s];
+        vp.early_exit = 1;
+        vp.k_base = 0;
+        ps.do_surface = 1;
+        ps.do_volume = 1;
+        ps.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
+        ps.trace_in = buf[(s - 1) & 1];
+        ps.surf = h->surf;
+        ps.nbr = h->nbr;
+        ps.perm = h->perm;
+        ps.Mpk = h->Mpk;
+        ps.u = h->u;
+        ps.res = h->res;
+        ps.rk_a = Lsrk45::a[s - 1];
+        ps.rk_b = Lsrk45::b[s - 1];
+        ps.dt = dt;
+        ps.stage_prev = ids[s - 1];
+        launch_pair(h, ps);
+        h->launches++;
+    }
+    // interface + update of stage 4 (reads buffer 0)
+    ModalSurfParams sp;
+    sp.K = h->K;
+    sp.g = h->g;
+    sp.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
+    sp.ops = h->ops;
+    sp.trace = buf[0];
+    sp.accf = h->accf;
+    sp.T1 = h->T1;
+    sp.surf = h->surf;
+    sp.src = h->src;
+    sp.nbr = h->nbr;
+    sp.perm = h->perm;
+    sp.Minv = h->Minv;
+    sp.Mpk = h->Mpk;
+    sp.du = nullptr;
+    sp.u = h->u;
+    sp.res = h->res;
+    sp.rk_a = Lsrk45::a[4];
+    sp.rk_b = Lsrk45::b[4];
+    sp.dt = dt;
+    sp.rk_mode = 1;
+    sp.err = h->err;
+    sp.stage_id = ids[4];
+    sp.early_exit = 1;
+    using SC = SurfCfg<4>;
+    modal_surface_kernel<4, false><<<(h->K + SC::E - 1) / SC::E, SC::T, 0, h->stream>>>(sp);
+    h->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+// One LSRK45 step on the resident state: 6 launches on the fused path, else 10.
+int run_step(swedg_handle h, const unsigned* ids, double dt) {
+    if (fused_path(h)) {
+        StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, ids[0], true};
+        if (run_stage(h, sa)) return h->last_code;
+        return run_fused_tail(h, ids, dt);
+    }
+    for (int s = 0; s < 5; ++s) {
+        StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
+        if (run_stage(h, sa)) return h->last_code;
+    }
     return SWEDG_OK;
 }
 
@@ -676,6 +792,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->n_halo = d->n_halo;
     h->g = d->g;
     h->device = d->device;
+    if (const char* v = std::getenv("SWEDG_FUSION")) h->fusion = std::string(v) == "1";
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
         h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : (sv == "quad" ? 4 : 0)));
@@ -818,7 +935,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
-                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ};
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& p : h->ev_pending) {
@@ -1071,18 +1188,22 @@ int capture_step_graph(swedg_handle h, double dt) {
         cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
     }
+    if (fused_path(h) && ensure_trace2(h)) return h->last_code;  // no allocation inside a capture
     h->graph_base = h->next_stage;
     h->next_stage += 5;
     CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     int rc = SWEDG_OK;
     const long long l0 = h->launches;
-    for (int s = 0; s < 5 && rc == SWEDG_OK; ++s) {
-        StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, h->graph_base + s, true};
-        rc = run_stage(h, sa);
+    {
+        const unsigned ids[5] = {h->graph_base, h->graph_base + 1, h->graph_base + 2, h->graph_base + 3,
+                                 h->graph_base + 4};
+        rc = run_step(h, ids, dt);
     }
     step_counter_kernel<<<1, 1, 0, h->stream>>>(h->err);
+    h->launches++;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    h->graph_nodes = h->launches - l0;
     h->launches = l0;  // captured, not launched
     if (rc != SWEDG_OK) {
         if (graph) cudaGraphDestroy(graph);
@@ -1120,7 +1241,7 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
             const double t0 = h->t;
             for (int s = 0; s < 5; ++s) new_stage(h, t0 + Lsrk45::c[s] * dt);
             CUDA_TRY(h, cudaGraphLaunch(h->graph_exec, h->stream));
-            h->launches += 11;
+            h->launches += h->graph_nodes;
             h->t = t0 + dt;
         }
         // individually launched stages carry their own ids: offset back to 0
@@ -1131,11 +1252,9 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
     }
     for (int n = 0; n < nsteps; ++n) {
         const double t0 = h->t;
-        for (int s = 0; s < 5; ++s) {
-            const unsigned sid = new_stage(h, t0 + Lsrk45::c[s] * dt);
-            StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, sid, true};
-            if (run_stage(h, sa)) return h->last_code;
-        }
+        unsigned ids[5];
+        for (int s = 0; s < 5; ++s) ids[s] = new_stage(h, t0 + Lsrk45::c[s] * dt);
+        if (run_step(h, ids, dt)) return h->last_code;
         h->t = t0 + dt;
     }
     if (sync) return check_errors(h);
@@ -1551,19 +1670,19 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
             CUDA_TRY(h, cudaMemcpyAsync(h->u + a, u_host + a, (e - a) * 8, cudaMemcpyHostToDevice, h->cp_in));
             CUDA_TRY(h, cudaEventRecord(h->ev_in[c], h->cp_in));
         }
-        for (int s = 0; s < 5; ++s) {
-            const unsigned sid = new_stage(h, t0 + Lsrk45::c[s] * dt);
-            if (s == 0) {
-                for (int c = 0; c < C; ++c) {  // element-local volume kernel as the chunks land
-                    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
-                    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, sid, true,
-                                 lo(c), lo(c + 1)};
-                    if (run_stage(h, sa)) return h->last_code;
-                }
-                StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, sid, true};
-                if (run_stage(h, sa)) return h->last_code;
-            } else {
-                StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, sid, true};
+        unsigned ids[5];
+        for (int s = 0; s < 5; ++s) ids[s] = new_stage(h, t0 + Lsrk45::c[s] * dt);
+        for (int c = 0; c < C; ++c) {  // element-local stage-0 volume kernel as the chunks land
+            CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
+            StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, ids[0], true,
+                         lo(c), lo(c + 1)};
+            if (run_stage(h, sa)) return h->last_code;
+        }
+        if (fused_path(h)) {
+            if (run_fused_tail(h, ids, dt)) return h->last_code;
+        } else {
+            for (int s = 0; s < 5; ++s) {
+                StageArgs sa{h->u, s == 0 ? 2 : 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
                 if (run_stage(h, sa)) return h->last_code;
             }
         }

@@ -237,3 +237,28 @@ def test_host_state_stepping_equals_device_steps(mode, nchunks):
     with pytest.raises(capi.PositivityError) as ei:
         h2.step_host(bad, dt, 2, nchunks)
     assert ei.value.elem == 400 and abs(ei.value.t - 0.5) < 1e-12
+
+
+def test_fused_stage_chain_matches_split_launches():
+    """FAST N=4: the fused [interface(s-1) + volume(s)] launch chain (6 launches per step,
+    double-buffered traces) == the split 10-launch step, to rounding (the same arithmetic;
+    FMA contraction may differ between the two kernels)."""
+    import os
+    c = load_golden("modal_n4_warp")
+    dt = 0.004
+    out = {}
+    for fused in ("1", "0"):
+        os.environ["SWEDG_FUSION"] = fused
+        try:
+            h = make(c, capi.MODE_FAST)
+        finally:
+            os.environ.pop("SWEDG_FUSION", None)
+        h.set_state(c["u"])
+        h.step(dt, 3)           # graph replay
+        h.step(dt, 1)           # individual launches
+        u = np.array(c["u"], copy=True)
+        h.step_host(u, dt, 2)   # host-state path
+        out[fused] = (h.get_state()[0], u)
+        h.close()
+    assert rel(out["1"][0], out["0"][0]) <= 1e-13
+    assert rel(out["1"][1], out["0"][1]) <= 1e-13
