@@ -43,13 +43,23 @@ typedef struct {
 } swedg_case_config;
 
 int swedg_case_build(const swedg_case_config* cfg, swedg_case* out);
+/* The problem's state, bathymetry and operators on a caller-supplied mesh (the
+ * read_mesh_text format, mesh.hpp:462-493): verts[nv][2], tris[ne][3] (counter-
+ * clockwise), wall_faces[nw][2] = (element, face) records, domain = {xc, yc, Lx,
+ * Ly} (periodic matching of open boundary faces, mesh.hpp:210-247).  Elements
+ * are straight-sided at degree N (cfg->warp != 0 warps them like warp_mesh);
+ * cfg->nx, ny, strips are ignored. */
+int swedg_case_build_mesh(const swedg_case_config* cfg, const double* verts, int nv, const int* tris, int ne,
+                          const int* wall_faces, int nw, const double* domain, int periodic_x, int periodic_y,
+                          swedg_case* out);
 int swedg_case_destroy(swedg_case c);
 const char* swedg_case_error(void);
 /* Fill every operator/geometry/connectivity pointer and size of *d (penalty,
  * mode and device are left for the caller). */
 int swedg_case_fill_desc(swedg_case c, swedg_desc* d);
 /* Named host arrays: "u0" [K][3][n], "b" [K][n], "xy_vol" [K][2][nq], "map_coeffs" [K][2][Np],
- * "J_vol" [K][nq], "volq_w" [nq], "Vq" ... ; returns element count via *n. */
+ * "map_nodes" [K][2][Np], "J_vol" [K][nq], "volq_w" [nq], "Vq" ..., "fine_w/V/Vr/Vs" (FineQuad),
+ * "lattice_V" (basis at the mapping lattice, Np x Np); returns element count via *n. */
 const double* swedg_case_array(swedg_case c, const char* name, size_t* n);
 const int* swedg_case_iarray(swedg_case c, const char* name, size_t* n);
 double swedg_case_dt(swedg_case c);

@@ -18,6 +18,8 @@
 #include <fstream>
 #include <iostream>
 #include <random>
+#include <sstream>
+#include <iterator>
 #include <string>
 #include <vector>
 
@@ -515,6 +517,69 @@ int cmd_ratio(const std::string& path) {
     return 0;
 }
 
+// Output formats (diagnostics.hpp:272-375, mesh.hpp:462-493): the reference's own
+// writers' bytes for small cases, with the inputs they were written from.
+std::vector<int> file_bytes(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    std::string s((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    return std::vector<int>(s.begin(), s.end());
+}
+
+int cmd_io(const std::string& path, const std::string& tmpdir) {
+    Writer w(path);
+    auto text = [&](const std::string& name, const std::string& s) {
+        std::vector<int> v(s.begin(), s.end());
+        w.i32(name, {v.size()}, v.data());
+    };
+    {  // mesh text: the unwarped 8 x 8 lake mesh and a 6 x 6 dam-break mesh (wall faces)
+        Mesh lake = uniform_tri_mesh(8, 8, {0.0, 0.0, 2.0, 2.0});
+        std::ostringstream a;
+        write_mesh_text(lake, a);
+        text("mesh_lake_text", a.str());
+        RunConfig cfg;
+        cfg.problem = ProblemId::DamBreak;
+        cfg.degree = 2;
+        cfg.nx = cfg.ny = 6;
+        Case c = build_case(cfg);
+        std::ostringstream b;
+        write_mesh_text(c.mesh, b);
+        text("mesh_dam_text", b.str());
+    }
+    {  // run() output files of a small vortex case
+        RunConfig cfg;
+        cfg.problem = ProblemId::Vortex;
+        cfg.degree = 2;
+        cfg.nx = cfg.ny = 4;
+        cfg.tfinal = 0.05;
+        cfg.out_dir = tmpdir;
+        Case c = build_case(cfg);
+        w.mats("vtk_map_nodes", c.mesh.map_nodes);
+        w.mats("u0", c.hstate.u);
+        w.vecs("b", c.hstate.b);
+        RunResult r = run(c);
+        w.mats("u_final", c.hstate.u);
+        w.scalar("t_final", c.time());
+        std::vector<double> inv;
+        for (auto& s : r.series) inv.insert(inv.end(), {s.t, s.mass, s.momentum_x, s.momentum_y, s.entropy, s.min_h});
+        w.f64("series", {r.series.size(), 6}, inv.data());
+        double er[6] = {(double)r.error.N, r.error.h_mesh, r.error.err_h, r.error.err_hu, r.error.err_hv,
+                        r.error.combined};
+        w.f64("error", {6}, er);
+        std::ostringstream tag;
+        tag << c.time();
+        text("final_name", "solution_" + tag.str() + ".vtk");
+        auto put = [&](const std::string& name, const std::string& file) {
+            std::vector<int> v = file_bytes(tmpdir + "/" + file);
+            w.i32(name, {v.size()}, v.data());
+        };
+        put("vtk0_text", "solution_0.vtk");
+        put("vtk1_text", "solution_" + tag.str() + ".vtk");
+        put("invariants_csv", "invariants.csv");
+        put("errors_csv", "errors.csv");
+    }
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -529,6 +594,7 @@ int main(int argc, char** argv) {
         if (cmd == "ops") return cmd_ops(out);
         if (cmd == "positivity") return cmd_positivity(out);
         if (cmd == "ratio") return cmd_ratio(out);
+        if (cmd == "io" && argc == 4) return cmd_io(out, argv[3]);
         if (cmd == "modal" && argc == 11)
             return cmd_modal(out, std::atoi(argv[3]), std::atoi(argv[4]), std::atof(argv[5]),
                              std::atoi(argv[6]) != 0, static_cast<unsigned>(std::atoi(argv[7])),

@@ -548,6 +548,8 @@ def _setup_lib():
         L.swedg_case_min_edge.argtypes = [vp]
         L.swedg_case_min_edge.restype = C.c_double
         L.swedg_case_K.argtypes = [vp]
+        L.swedg_case_build_mesh.argtypes = [C.POINTER(_CaseCfg), _dp, C.c_int, _ip, C.c_int, _ip, C.c_int, _dp,
+                                            C.c_int, C.c_int, C.POINTER(vp)]
         L._setup_bound = True
     return L
 
@@ -556,10 +558,13 @@ class Case:
     """A problem built by the native setup (lake / vortex / dambreak / smooth)."""
 
     def __init__(self, problem="smooth", *, scheme=SCHEME_HYBRIDIZED, N=4, nx=16, ny=None,
-                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0):
+                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0, mesh=None):
         """strips > 1: rank `strip`'s y-strip of a global nx x (ny*strips) periodic mesh on
         [-Lx/2,Lx/2] x [-strips*Ly/2, strips*Ly/2] (weak scaling); its 2 halo rows follow the
-        K owned elements (below: slots K..K+2nx, above: K+2nx..K+4nx)."""
+        K owned elements (below: slots K..K+2nx, above: K+2nx..K+4nx).
+        mesh: a caller-supplied mesh instead (dict with verts [nv][2], tris [ne][3],
+        wall_faces [nw][2], domain (xc, yc, Lx, Ly), periodic_x, periodic_y; e.g. from
+        io.read_mesh_text) — swedg_case_build_mesh."""
         L = _setup_lib()
         cfg = _CaseCfg()
         cfg.problem = PROBLEMS[problem] if isinstance(problem, str) else int(problem)
@@ -567,11 +572,21 @@ class Case:
         cfg.warp, cfg.cfl, cfg.g, cfg.seed, cfg.threads = warp, cfl, g, seed, threads
         cfg.strips, cfg.strip = strips, strip
         h = C.c_void_p()
-        rc = L.swedg_case_build(C.byref(cfg), C.byref(h))
+        if mesh is None:
+            rc = L.swedg_case_build(C.byref(cfg), C.byref(h))
+        else:
+            v = _f64(mesh["verts"]).reshape(-1, 2)
+            t = _i32(mesh["tris"]).reshape(-1, 3)
+            w = _i32(mesh.get("wall_faces", np.zeros((0, 2)))).reshape(-1, 2)
+            dom = _f64(mesh["domain"])
+            rc = L.swedg_case_build_mesh(C.byref(cfg), _p(v), len(v), _pi(t), len(t), _pi(w) if len(w) else None,
+                                         len(w), _p(dom), int(mesh.get("periodic_x", 0)),
+                                         int(mesh.get("periodic_y", 0)), C.byref(h))
         if rc != SWEDG_OK:
             raise _err_class(rc)(rc, "swedg_case_build: " + L.swedg_case_error().decode())
         self._c, self._lib = h, L
         self.scheme, self.N = scheme, N
+        self.problem = problem if isinstance(problem, str) else None
         self.desc = _Desc()
         L.swedg_case_fill_desc(self._c, C.byref(self.desc))
         d = self.desc

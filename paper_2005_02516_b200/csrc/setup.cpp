@@ -822,7 +822,11 @@ struct swedg_case_s {
     std::vector<int> nbr, nbr_face, face_type, perm;
     std::vector<double> u0, b, xy_vol, xy_surf, map_coeffs, volq_w, shift;
     std::vector<double> fine_w, fine_V, fine_Vr, fine_Vs;  // FineQuad (diagnostics.hpp:142-153)
+    std::vector<double> lattice_V;                        // basis at the mapping lattice (LatticeInterp, VTK output)
     bool periodic_x = true, periodic_y = true;
+    // external mesh (swedg_case_build_mesh): replaces the problem's structured mesh
+    bool ext = false;
+    Mesh ext_mesh;
     int n_halo = 0;
 };
 
@@ -1039,8 +1043,11 @@ void build_case(swedg_case_s& c) {
     }
     const bool dam = cfg.problem == SWEDG_PROBLEM_DAMBREAK;
     const int P = cfg.strips > 1 ? cfg.strips : 1;
-    c.periodic_x = c.periodic_y = !dam;
-    if (P > 1 && cfg.strip == -1) {  // the whole global strip mesh in one piece (reference for tests)
+    if (!c.ext) c.periodic_x = c.periodic_y = !dam;
+    if (c.ext) {  // read_mesh_text-style input: straight-sided, caller's walls and periodicity
+        if (P > 1) throw std::invalid_argument("strip partitions need the structured mesh");
+        c.mesh = c.ext_mesh;
+    } else if (P > 1 && cfg.strip == -1) {  // the whole global strip mesh in one piece (reference for tests)
         if (dam) throw std::invalid_argument("strip partitions need a periodic problem");
         dom.Ly *= P;
         c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny * P, dom, false);
@@ -1054,9 +1061,11 @@ void build_case(swedg_case_s& c) {
     } else {
         c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny, dom, dam);
     }
-    if (dam) snap_vertices_to_curve(c.mesh, qc);
+    if (dam && !c.ext) snap_vertices_to_curve(c.mesh, qc);
     set_mapping_degree(c.mesh, cfg.N, threads);
-    if (dam) {
+    if (c.ext) {
+        if (cfg.warp != 0.0) warp_mesh(c.mesh, cfg.warp, threads);
+    } else if (dam) {
         auto dam_faces = faces_on_curve(c.mesh, qc);
         if (dam_faces.empty()) throw std::runtime_error("mesh has no faces on the dam curve");
         bool tagged = false;
@@ -1110,6 +1119,7 @@ void build_case(swedg_case_s& c) {
     const int Np = R.Np, nq = R.nq;
     std::vector<double> lx, ly;
     map_lattice(cfg.N, lx, ly);
+    c.lattice_V = flat(vandermonde(cfg.N, lx, ly));
     LU li(vandermonde(cfg.N, lx, ly));
     double a1 = 0, a2 = 0, a3 = 0;
     if (cfg.problem == SWEDG_PROBLEM_SMOOTH) {
@@ -1178,7 +1188,7 @@ void build_case(swedg_case_s& c) {
             }
         }
     });
-    if (dam) {
+    if (dam) {  // h = 10 upstream of the dam curve, 5 downstream (run.hpp:190-205)
         const double sqrt2 = std::sqrt(2.0);
         for (long k = 0; k < K; ++k) {
             double cx = 0, cy = 0;
@@ -1260,6 +1270,52 @@ int swedg_case_fill_desc(swedg_case c, swedg_desc* d) {
     return SWEDG_OK;
 }
 
+int swedg_case_build_mesh(const swedg_case_config* cfg, const double* verts, int nv, const int* tris, int ne,
+                          const int* wall_faces, int nw, const double* domain, int periodic_x, int periodic_y,
+                          swedg_case* out) {
+    if (!cfg || !out || !verts || !tris || !domain || nv < 3 || ne < 1 || nw < 0 || (nw > 0 && !wall_faces))
+        return SWEDG_ERR_INVALID;
+    *out = nullptr;
+    auto* c = new swedg_case_s();
+    c->cfg = *cfg;
+    c->ext = true;
+    c->periodic_x = periodic_x != 0;
+    c->periodic_y = periodic_y != 0;
+    Mesh& m = c->ext_mesh;
+    m.dom = {domain[0], domain[1], domain[2], domain[3]};
+    m.verts.resize(nv);
+    for (int i = 0; i < nv; ++i) m.verts[i] = {verts[2 * i], verts[2 * i + 1]};
+    m.tris.resize(ne);
+    for (int e = 0; e < ne; ++e) {
+        for (int f = 0; f < 3; ++f) {
+            const int v = tris[3 * e + f];
+            if (v < 0 || v >= nv) {
+                g_case_error = "vertex index out of range in element " + std::to_string(e);
+                delete c;
+                return SWEDG_ERR_INVALID;
+            }
+            m.tris[e][f] = v;
+        }
+    }
+    for (int w = 0; w < nw; ++w) {
+        if (wall_faces[2 * w] < 0 || wall_faces[2 * w] >= ne || wall_faces[2 * w + 1] < 0 || wall_faces[2 * w + 1] > 2) {
+            g_case_error = "bad wallface record";
+            delete c;
+            return SWEDG_ERR_INVALID;
+        }
+        m.wall_faces.push_back({wall_faces[2 * w], wall_faces[2 * w + 1]});
+    }
+    try {
+        build_case(*c);
+    } catch (const std::exception& e) {
+        g_case_error = e.what();
+        delete c;
+        return SWEDG_ERR_INVALID;
+    }
+    *out = c;
+    return SWEDG_OK;
+}
+
 const double* swedg_case_array(swedg_case c, const char* name, size_t* n) {
     if (!c || !name) return nullptr;
     const std::vector<double>* v = nullptr;
@@ -1289,6 +1345,7 @@ const double* swedg_case_array(swedg_case c, const char* name, size_t* n) {
     else if (s == "fine_V") v = &c->fine_V;
     else if (s == "fine_Vr") v = &c->fine_Vr;
     else if (s == "fine_Vs") v = &c->fine_Vs;
+    else if (s == "lattice_V") v = &c->lattice_V;
     if (!v) return nullptr;
     if (n) *n = v->size();
     return v->data();

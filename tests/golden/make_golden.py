@@ -16,6 +16,7 @@ import os
 import struct
 import subprocess
 import sys
+import tempfile
 
 import numpy as np
 
@@ -48,6 +49,8 @@ CASES = {
     "positivity": ["positivity"],
     # bench.hpp volume-kernel cost study: matvec / fluxdiff / skew outputs, n = 6..50
     "ratio": ["ratio"],
+    # output formats: mesh text (lake, dam) and run()'s CSV / VTK files of a small vortex run
+    "io": ["io", "@TMP"],
 }
 
 
@@ -82,8 +85,9 @@ def main(argv: list[str]) -> int:
         if only and name not in only:
             continue
         raw = os.path.join(REPO, "oracle", "_ref", name + ".bin")
-        cmd = [DUMP, args[0], raw] + args[1:]
-        subprocess.run(cmd, check=True)
+        with tempfile.TemporaryDirectory() as tmp:  # "@TMP": a scratch output directory
+            cmd = [DUMP, args[0], raw] + [tmp if a == "@TMP" else a for a in args[1:]]
+            subprocess.run(cmd, check=True)
         recs = read_records(raw)
         dst = os.path.join(HERE, name + ".npz")
         np.savez_compressed(dst, **recs)

@@ -165,3 +165,23 @@ def test_invariants_c4_sample_k1d256():
     np.testing.assert_array_equal([inv[f] for f in capi.INVARIANT_FIELDS[1:5]], fsums(terms, 4))
     assert inv["min_h"] == mh
     h.close()
+
+
+def test_python_run_writes_reference_output_files(tmp_path):
+    """paper_2005_02516_b200.run.run (run.hpp:226-284 with out_dir) on the small vortex of
+    tests/golden/io.npz, PARITY: both VTK files byte-identical to the reference's, the CSV
+    files equal to within the reference's summation rounding."""
+    from paper_2005_02516_b200 import run as srun
+
+    G = load_golden("io")
+    text = lambda a: bytes(np.asarray(a).astype(np.uint8)).decode()  # noqa: E731
+    c = capi.Case("vortex", N=2, nx=4)
+    res = srun.run(c, tfinal=0.05, mode=capi.MODE_PARITY, out_dir=str(tmp_path))
+    assert (tmp_path / "solution_0.vtk").read_text() == text(G["vtk0_text"])
+    assert (tmp_path / text(G["final_name"])).read_text() == text(G["vtk1_text"])
+    np.testing.assert_array_equal(res["u"], G["u_final"])
+    got = np.loadtxt(tmp_path / "invariants.csv", delimiter=",", skiprows=1).reshape(-1, 6)
+    np.testing.assert_array_equal(got[:, 0], G["series"][:, 0])
+    np.testing.assert_allclose(got[:, 1:], G["series"][:, 1:], rtol=1e-13, atol=1e-15)
+    e = np.genfromtxt(tmp_path / "errors.csv", delimiter=",", skip_header=1)
+    np.testing.assert_allclose(e[:6], G["error"], rtol=1e-11)
