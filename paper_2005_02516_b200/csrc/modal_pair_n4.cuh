@@ -385,18 +385,25 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
             tmem_ld32d(tbase + W::tP, Pa);            // doubles 0..15
             tmem_ld16d(tbase + W::tP + 32, Pb);       // doubles 16..23
             Pb[8] = tmem_ld2d(tbase + W::tP + 48);    // double 24 (last allocated columns)
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            // two partial sums per output (even / odd i): 6 independent FMA chains
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
-            for (int i = 0; i < nq; ++i) {
+            for (int i = 0; i < nq; i += 2) {
                 const double p = i < 16 ? Pa[i] : Pb[i - 16];
                 s0 = __fma_rn(p, work[W::wV + i], s0);
                 s1 = __fma_rn(p, work[W::wV + nq + i], s1);
                 s2 = __fma_rn(p, work[W::wV + 2 * nq + i], s2);
+                if (i + 1 < nq) {
+                    const double q = i + 1 < 16 ? Pa[i + 1] : Pb[i + 1 - 16];
+                    e0 = __fma_rn(q, work[W::wV + i + 1], e0);
+                    e1 = __fma_rn(q, work[W::wV + nq + i + 1], e1);
+                    e2 = __fma_rn(q, work[W::wV + 2 * nq + i + 1], e2);
+                }
             }
             if (lp < Np) {
-                work[W::wVh + lp] = s0;
-                work[W::wVh + Np + lp] = s1;
-                work[W::wVh + 2 * Np + lp] = s2;
+                work[W::wVh + lp] = s0 + e0;
+                work[W::wVh + Np + lp] = s1 + e1;
+                work[W::wVh + 2 * Np + lp] = s2 + e2;
             }
         }
         __syncwarp();
@@ -576,14 +583,23 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         {
             const double* stk = work + W::wU;
             const int m = lp < Np ? lp : Np - 1;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
-            for (int i = 0; i < nq; ++i) {
+            for (int i = 0; i < nq; i += 2) {
                 const double v = sVq[i + m * nq];
                 s0 = __fma_rn(v, stk[i], s0);
                 s1 = __fma_rn(v, stk[nq + i], s1);
                 s2 = __fma_rn(v, stk[2 * nq + i], s2);
+                if (i + 1 < nq) {
+                    const double w = sVq[i + 1 + m * nq];
+                    e0 = __fma_rn(w, stk[i + 1], e0);
+                    e1 = __fma_rn(w, stk[nq + i + 1], e1);
+                    e2 = __fma_rn(w, stk[2 * nq + i + 1], e2);
+                }
             }
+            s0 += e0;
+            s1 += e1;
+            s2 += e2;
             if (valid && lp < Np) {
                 double* out = prm.T1 + (size_t)k * 3 * Np;
                 out[lp] = s0;
