@@ -162,6 +162,12 @@ int swedg_rhs_device(swedg_handle h, const double* u_dev, double* du_dev, double
  * runs the fused surface + lift + M^-1 + register update.  Stream-ordered. */
 int swedg_stage_volume(swedg_handle h, int stage, double dt);
 int swedg_stage_surface(swedg_handle h, int stage, double dt);
+/* swedg_stage_volume on the element range [k0, k1) only, so boundary elements can
+ * be computed first and their traces exchanged while the interior runs (the
+ * projection + volume kernel is element-local).  The range starting at k0 == 0
+ * opens the stage; the ranges of one stage must cover [0, K) before
+ * swedg_stage_surface. */
+int swedg_stage_volume_range(swedg_handle h, int stage, double dt, int k0, int k1);
 int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo);
 /* Check the device error record (syncs the stream). */
 int swedg_check(swedg_handle h);

@@ -1278,6 +1278,18 @@ int swedg_stage_volume(swedg_handle h, int stage, double dt) {
     return run_stage(h, sa);
 }
 
+int swedg_stage_volume_range(swedg_handle h, int stage, double dt, int k0, int k1) {
+    if (!h || stage < 0 || stage > 4 || k0 < 0 || k1 < k0 || k1 > h->K) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
+        return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
+    cudaSetDevice(h->device);
+    if (k0 == 0) h->stage_cur = new_stage(h, h->t + Lsrk45::c[stage] * dt);  // first range opens the stage
+    if (k1 == k0) return SWEDG_OK;
+    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true, k0, k1};
+    return run_stage(h, sa);
+}
+
 int swedg_stage_surface(swedg_handle h, int stage, double dt) {
     if (!h || stage < 0 || stage > 4) return SWEDG_ERR_INVALID;
     if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");

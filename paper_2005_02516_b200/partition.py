@@ -80,6 +80,32 @@ def exchange(trace, plan: StripHalo, group=None) -> None:
         r.wait()
 
 
+def stage_overlapped(h, stage: int, dt: float, trace, plan: StripHalo, stream, comm_stream, group=None,
+                     exchange_fn=None) -> None:
+    """One LSRK45 stage with the halo exchange overlapped with interior volume work:
+    the volume kernel runs first on the two boundary rows (the elements whose traces
+    the neighbours need), the exchange of those traces starts on `comm_stream`, the
+    interior volume kernel runs on `stream` meanwhile, and the surface kernel waits
+    for the exchange.  `exchange_fn(trace, plan)` defaults to `exchange` (NCCL/gloo
+    point-to-point)."""
+    import torch
+
+    K, row = plan.K, plan.row
+    ex = exchange_fn or (lambda t, p: exchange(t, p, group))
+    h.stage_volume_range(stage, dt, 0, row)            # first row  -> previous rank
+    h.stage_volume_range(stage, dt, K - row, K)        # last row   -> next rank
+    boundary_done = torch.cuda.Event()
+    boundary_done.record(stream)
+    with torch.cuda.stream(comm_stream):
+        comm_stream.wait_event(boundary_done)
+        ex(trace, plan)
+        halos_in = torch.cuda.Event()
+        halos_in.record(comm_stream)
+    h.stage_volume_range(stage, dt, row, K - row)      # interior, concurrent with the exchange
+    stream.wait_event(halos_in)
+    h.stage_surface(stage, dt)
+
+
 def copy_halos_local(traces, plans) -> None:
     """Single-process stand-in for `exchange` over P logical partitions (device copies)."""
     P = len(plans)

@@ -144,3 +144,70 @@ def test_logical_partitions_on_one_gpu_equal_global(P):
         u, _, t = h.get_state()
         np.testing.assert_array_equal(u, ug[owned_slice(r)])
         assert t == 2 * dt
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_boundary_first_volume_ranges_equal_global(P):
+    """The overlapped schedule (partition.stage_overlapped): boundary rows' volume kernel,
+    halo exchange, interior volume kernel, surface kernel — with logical partitions on
+    one GPU — bit-for-bit the unpartitioned steps."""
+    from paper_2005_02516_b200.partition import trace_tensor
+
+    g = capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
+    hg = g.handle(mode=capi.MODE_FAST)
+    hg.set_state(g.u0())
+    dt = 1e-3
+    hg.step(dt, 2)
+    ug, _, _ = hg.get_state()
+    cases = [capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, strips=P, strip=r, threads=1) for r in range(P)]
+    hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
+    for h, c in zip(hs, cases):
+        h.set_state(c.u0())
+    plans = [StripHalo(P, r, NX, c.K) for r, c in enumerate(cases)]
+    traces = [trace_tensor(h) for h in hs]
+    for _ in range(2):
+        for s in range(5):
+            for h, pl in zip(hs, plans):
+                h.stage_volume_range(s, dt, 0, pl.row)
+                h.stage_volume_range(s, dt, pl.K - pl.row, pl.K)
+            torch.cuda.synchronize()
+            copy_halos_local(traces, plans)
+            for h, pl in zip(hs, plans):
+                h.stage_volume_range(s, dt, pl.row, pl.K - pl.row)
+            torch.cuda.synchronize()
+            for h in hs:
+                h.stage_surface(s, dt)
+    for h in hs:
+        h.check()
+    for r, h in enumerate(hs):
+        u, _, t = h.get_state()
+        np.testing.assert_array_equal(u, ug[owned_slice(r)])
+
+
+@pytest.mark.gpu
+def test_stage_overlapped_single_rank_equals_step():
+    """partition.stage_overlapped on one rank (no neighbours: the exchange is empty) with
+    separate compute and comm streams == swedg_step_lsrk45, bitwise."""
+    from paper_2005_02516_b200.partition import stage_overlapped, trace_tensor
+
+    c = capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, threads=1)
+    dt = 1e-3
+    h1 = c.handle(mode=capi.MODE_FAST)
+    h1.set_state(c.u0())
+    h1.step(dt, 2)
+    u1, _, _ = h1.get_state()
+    h2 = c.handle(mode=capi.MODE_FAST)
+    stream, comm = torch.cuda.Stream(), torch.cuda.Stream()
+    h2.set_stream(stream.cuda_stream)
+    h2.set_state(c.u0())
+    plan = StripHalo(1, 0, NX, c.K)
+    trace = trace_tensor(h2)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            for s in range(5):
+                stage_overlapped(h2, s, dt, trace, plan, stream, comm)
+    torch.cuda.synchronize()
+    h2.check()
+    u2, _, _ = h2.get_state()
+    np.testing.assert_array_equal(u1, u2)
