@@ -338,6 +338,7 @@ struct ModalSurfParams {
     ErrRec* err;
     unsigned stage_id;
     int early_exit;
+    int k_begin;          // first element of this launch (K = one past the last)
 };
 
 template <int N>
@@ -367,11 +368,11 @@ modal_surface_kernel(ModalSurfParams prm) {
     const int tid = threadIdx.x;
     for (int x = tid; x < nf * Np; x += T) sVf[x] = prm.ops[O::Vf + x];
     const int e = tid / L, s = tid % L;
-    const int k = blockIdx.x * E + e;
+    const int k = prm.k_begin + blockIdx.x * E + e;  // elements [k_begin, K)
     const bool act = k < prm.K;
     const double g = prm.g;
     if constexpr (!P) {  // packed M_h^{-1} of the block's elements: one contiguous coalesced copy
-        const int k0 = blockIdx.x * E, ne = min(E, prm.K - k0);
+        const int k0 = prm.k_begin + blockIdx.x * E, ne = min(E, prm.K - k0);
         const double* src = prm.Mpk + (size_t)k0 * NPK;
         for (int x = tid; x < ne * NPK; x += T) sMpk[x] = src[x];
     }

@@ -356,8 +356,12 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     sp.err = h->err;
     sp.stage_id = sa.stage_id;
     sp.early_exit = sa.early_exit ? 1 : 0;
+    // surface-only calls may cover an element range [k0, k1) (chunked host-state stepping)
+    sp.k_begin = sa.parts == 2 ? sa.k0 : 0;
+    if (sa.parts == 2 && sa.k1 >= 0) sp.K = sa.k1;
     using SC = SurfCfg<N>;
-    const int grid = (h->K + SC::E - 1) / SC::E;
+    const int grid = (sp.K - sp.k_begin + SC::E - 1) / SC::E;
+    if (grid <= 0) return SWEDG_OK;
     {
         KTimer kt(h, 1);
         if (h->mode == SWEDG_MODE_PARITY)
@@ -519,6 +523,7 @@ int run_fused_tail(swedg_handle h, const unsigned* ids, double dt) {
     sp.err = h->err;
     sp.stage_id = ids[4];
     sp.early_exit = 1;
+    sp.k_begin = 0;
     using SC = SurfCfg<4>;
     modal_surface_kernel<4, false><<<(h->K + SC::E - 1) / SC::E, SC::T, 0, h->stream>>>(sp);
     h->launches++;
@@ -1692,20 +1697,32 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
         }
         if (fused_path(h)) {
             if (run_fused_tail(h, ids, dt)) return h->last_code;
+            CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
+            CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_step, 0));
+            for (int c = 0; c < C; ++c) {  // D2H of the step's result
+                const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+                CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
+                CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
+            }
         } else {
-            for (int s = 0; s < 5; ++s) {
+            for (int s = 0; s < 4; ++s) {
                 StageArgs sa{h->u, s == 0 ? 2 : 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
                 if (run_stage(h, sa)) return h->last_code;
             }
+            StageArgs sv{h->u, 1, nullptr, true, Lsrk45::a[4], Lsrk45::b[4], dt, nullptr, ids[4], true};
+            if (run_stage(h, sv)) return h->last_code;
+            for (int c = 0; c < C; ++c) {  // last interface/update kernel by chunk, each chunk's D2H right after
+                StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[4], Lsrk45::b[4], dt, nullptr, ids[4], true,
+                             lo(c), lo(c + 1)};
+                if (run_stage(h, ss)) return h->last_code;
+                CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
+                CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_step, 0));
+                const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+                CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
+                CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
+            }
         }
         h->t = t0 + dt;
-        CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
-        CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_step, 0));
-        for (int c = 0; c < C; ++c) {  // D2H of the step's result
-            const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
-            CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
-            CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
-        }
     }
     if (nsteps > 0) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_out[C - 1], 0));
     return check_errors(h);
