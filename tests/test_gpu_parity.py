@@ -17,7 +17,7 @@ import math
 import numpy as np
 import pytest
 
-from oracle_py import Oracle, load_golden
+from oracle_py import Oracle, case_dict, load_golden
 
 pytestmark = pytest.mark.gpu
 
@@ -262,3 +262,34 @@ def test_fused_stage_chain_matches_split_launches():
         h.close()
     assert rel(out["1"][0], out["0"][0]) <= 1e-13
     assert rel(out["1"][1], out["0"][1]) <= 1e-13
+
+
+@pytest.mark.parametrize("N", [3, 4])
+def test_odd_element_count_imported_mesh(N):
+    """Odd K (a pentagon fan of 5 triangles, wall boundary, imported through
+    swedg_case_build_mesh): exercises the pair kernel's single-element tail and the
+    chunked paths; PARITY bitwise against the C oracle, FAST within tolerance, and a
+    few LSRK45 steps (graph replay + host-state path) agree with the oracle's steps."""
+    import math as m
+    verts = [[0.0, 0.0]] + [[0.6 * m.cos(2 * m.pi * i / 5), 0.6 * m.sin(2 * m.pi * i / 5)] for i in range(5)]
+    tris = [[0, 1 + i, 1 + (i + 1) % 5] for i in range(5)]
+    c = capi.Case("smooth", N=N, mesh=dict(verts=verts, tris=tris, domain=(0.0, 0.0, 2.0, 2.0)))
+    assert c.K == 5
+    cd = case_dict(c)
+    u = c.u0()
+    ref, err, _ = Oracle(cd).rhs(u)
+    assert err == 0
+    hp = c.handle(mode=capi.MODE_PARITY)
+    np.testing.assert_array_equal(hp.rhs(u), ref)
+    hf = c.handle(mode=capi.MODE_FAST)
+    assert_fast_rhs(hf.rhs(u), ref, cd, u)
+    dt = 0.5 * c.dt
+    u_ref, _, err = Oracle(cd).step_lsrk45(u, np.zeros_like(u), dt, 3)
+    assert err == 0
+    hp.set_state(u)
+    hp.step(dt, 3)
+    np.testing.assert_array_equal(hp.get_state()[0], u_ref)
+    uh = np.array(u, copy=True)
+    hf.set_state(uh)
+    hf.step_host(uh, dt, 3, 2)
+    assert rel(uh, u_ref) <= RUN_TOL
