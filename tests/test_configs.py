@@ -128,3 +128,60 @@ def test_c4_full_size_properties_k1d1024():
     noise_ref = np.abs(ref[elems]).max()
     assert noise_ref < 1e-8
     assert np.abs(du_free).max() <= 8.0 * noise_ref
+
+
+def _entropy_vars(h, hu, hv, b, g):
+    vx, vy = hu / h, hv / h
+    return g * (h + b) - 0.5 * (vx * vx + vy * vy), vx, vy
+
+
+def test_fast_modal_entropy_balance_and_mass_k1d64():
+    """The reference's semi-discrete entropy balance (test_solver.cpp:172-206) for the
+    FAST N=4 pair kernel on a curved K1D=64 mesh: entropy-conservative flux ->
+    sum_k v_h^T M_h du ~ 0 (1e-9 of the RHS scale), Lax-Friedrichs -> <= 0,
+    mass conserved by both (entropy_rate / conservation_rate, solver.hpp:503-563)."""
+    c = capi.Case("smooth", N=4, nx=64, warp=0.1)
+    K, Np, nq = c.K, c.Np, c.nq
+    u = c.u0()
+    Vq = c.array("Vq").reshape(Np, nq).T
+    Pq = c.array("Pq").reshape(nq, Np).T
+    w = c.array("volq_w")
+    J = c.array("J_vol").reshape(K, nq)
+    uq = np.einsum("qm,kcm->kcq", Vq, u)
+    bq = c.b() @ Vq.T
+    v1, v2, v3 = _entropy_vars(uq[:, 0], uq[:, 1], uq[:, 2], bq, c.g)
+    vh = np.stack([v1 @ Pq.T, v2 @ Pq.T, v3 @ Pq.T], axis=1)           # [K][3][Np]
+    rates = {}
+    for pen in (capi.PENALTY_EC, capi.PENALTY_LF):
+        h = c.handle(mode=capi.MODE_FAST, penalty=pen)
+        du = h.rhs(u)
+        duq = np.einsum("qm,kcm->kcq", Vq, du)                          # M_h du = Vq^T wJ Vq du
+        mdu = np.einsum("qm,kcq->kcm", Vq, (w[None, :] * J)[:, None, :] * duq)
+        rates[pen] = (float((vh * mdu).sum()), float(np.abs(du).max()))
+        assert abs(float(((w[None, :] * J) * duq[:, 0]).sum())) < 1e-10 * (1 + rates[pen][1])
+        h.close()
+    r_ec, scale = rates[capi.PENALTY_EC]
+    assert abs(r_ec) < 1e-9 * (1.0 + scale)
+    assert rates[capi.PENALTY_LF][0] <= 1e-12 * (1.0 + scale)
+
+
+def test_fast_sbp_entropy_balance_k1d32():
+    """test_solver.cpp:208-236 for the FAST SBP N=4 kernel: perturbed lake at rest on a
+    curved K1D=32 mesh, sum_k v^T M du ~ 0 with the EC flux, <= 0 with LF, mass kept."""
+    c = capi.Case("lake", scheme=capi.SCHEME_SBP, N=4, nx=32, warp=0.1)
+    K, nq = c.K, c.nq
+    rng = np.random.default_rng(3)
+    u = c.u0() + rng.uniform(-0.05, 0.05, (K, 3, nq))
+    b = c.b()
+    m = c.array("M_diag")[None, :] * c.array("J_vol").reshape(K, nq)
+    v = np.stack(_entropy_vars(u[:, 0], u[:, 1], u[:, 2], b, c.g), axis=1)
+    rates = {}
+    for pen in (capi.PENALTY_EC, capi.PENALTY_LF):
+        h = c.handle(mode=capi.MODE_FAST, penalty=pen)
+        du = h.rhs(u)
+        rates[pen] = (float((m[:, None, :] * v * du).sum()), float(np.abs(du).max()))
+        assert abs(float((m * du[:, 0]).sum())) < 1e-10 * (1 + rates[pen][1])
+        h.close()
+    r_ec, scale = rates[capi.PENALTY_EC]
+    assert abs(r_ec) < 1e-9 * (1.0 + scale)
+    assert rates[capi.PENALTY_LF][0] <= 1e-12 * (1.0 + scale)
