@@ -41,6 +41,7 @@ struct SbpParams {
     double rk_a, rk_b, dt;
     int rk_mode;
     double* du_scratch;  // RK mode: du written here, applied by sbp_update_kernel
+    double* u_next;      // pair kernel, fused RK: u_next = u + b (a res + dt du), res in place (no du store)
     ErrRec* err;
     unsigned stage_id;
     int early_exit;

@@ -1,0 +1,288 @@
+// FAST-mode SBP RHS kernel for N = 4 (rhs_sbp, solver.hpp:369-434), laid out like
+// the modal pair kernel (modal_pair_n4.cuh): TWO elements per warp (one per
+// half-warp), 16 lanes per element; lane l' owns volume rows l' and l'+16 over
+// all 37 columns, and rows 32..36 are split over lanes 0..14 by column phase
+// (l' % 3) and reduced with shuffles.  Each lane's rows of (Q_SBP_x/4, Q_SBP_y/4)
+// live in TENSOR MEMORY (348 of 512 columns), so shared memory carries only the
+// node-j broadcasts (two addresses per warp, one per element), each feeding two
+// rows per lane; the next pair's state and geometric factors stream in with
+// cp.async during the flux loops.  Same arithmetic as sbp_rhs_kernel<4,false>
+// (factored accumulation, reciprocal-form surface flux).  With prm.u_next set the
+// LSRK45 register update is fused (the state ping-pongs between two buffers, since
+// neighbours read the stage's input state).
+//
+// (The thread-per-node kernel is shared-memory bound: Q_SBP operands are not
+// shared between elements and every node-j fetch feeds one pair, ncu 70 %
+// shared wavefronts at 39 % FP64.)
+#pragma once
+
+#include <stdint.h>
+
+#include "modal_pair_n4.cuh"  // Row6 / pair6 / row_finish, TMEM and cp.async helpers
+#include "sbp_kernels.cuh"
+
+namespace swedg {
+
+struct SbpPairN4 {
+    static constexpr int nq = 37, nf = 15, npf = 5, nrow = 52;
+    static constexpr int WARPS = 16, T = WARPS * 32;
+    // TMEM columns (32-bit): (QA,QB)_ij = 4 columns
+    static constexpr int t0 = 0;     // row l'      : 37 columns j
+    static constexpr int t1 = 148;   // row l'+16   : 37 columns j
+    static constexpr int tX = 296;   // row 32+l'/3 : 13 column slots j = l'%3 + 3s
+    static constexpr int tcols = 512;
+    // per-element work block (doubles): double2 (hu,hv) (u,v) (g1,g2) (g3,g4) | h
+    static constexpr int wA = 0, wB = 74, wC = 148, wD = 222, wH = 296;
+    static constexpr int work_stride = 338;  // == 2 (mod 16)
+    // staging per element: u [3][37] | gf columns 0..3, rows 0..36
+    static constexpr int sU = 0, sG = 112;
+    static constexpr int stage_stride = 260;
+    static constexpr int per_warp = 2 * work_stride + 2 * stage_stride;
+    static constexpr size_t bytes() { return sizeof(double) * (size_t)WARPS * per_warp + 16; }
+};
+
+__global__ void __launch_bounds__(SbpPairN4::T, 1)
+sbp_rhs_pair_n4_kernel(SbpParams prm) {
+    using W = SbpPairN4;
+    using O = SbpOps<4>;
+    constexpr int nq = W::nq, nf = W::nf, npf = W::npf, nrow = W::nrow;
+    if (prm.early_exit && error_pending(prm.err)) return;
+
+    extern __shared__ __align__(16) double smem[];
+    __shared__ uint32_t tmem_base_sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int half = lane >> 4, lp = lane & 15;
+    double* wbase = smem + warp * W::per_warp;
+    double* work = wbase + half * W::work_stride;
+    double* stage = wbase + 2 * W::work_stride;
+    const double2* nA = reinterpret_cast<const double2*>(work + W::wA);
+    const double2* nB = reinterpret_cast<const double2*>(work + W::wB);
+    const double2* nC = reinterpret_cast<const double2*>(work + W::wC);
+    const double2* nD = reinterpret_cast<const double2*>(work + W::wD);
+    const double* nH = work + W::wH;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_addr_u32(&tmem_base_sh)),
+                     "n"(W::tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16);
+    const int r0 = lp, r1 = lp + 16, rX = 32 + lp / 3, ph = lp % 3;
+    const bool xrow = lp < 15;  // lanes 0..14 share rows 32..36, three lanes per row
+    if (warp < 4) {  // the operator rows depend only on l': one copy per TMEM lane quarter
+        const double* QA = prm.ops + O::QA;
+        const double* QB = prm.ops + O::QB;
+        for (int j = 0; j < nq; ++j) {
+            tmem_st4(tbase + W::t0 + 4 * j, QA[r0 + j * nq], QB[r0 + j * nq]);
+            tmem_st4(tbase + W::t1 + 4 * j, QA[r1 + j * nq], QB[r1 + j * nq]);
+        }
+        for (int s = 0; s < 13; ++s) {
+            const int j = ph + 3 * s;
+            const bool ok = xrow && j < nq;
+            tmem_st4(tbase + W::tX + 4 * s, ok ? QA[rX + j * nq] : 0.0, ok ? QB[rX + j * nq] : 0.0);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    const double g = prm.g, g2 = 2.0 * g;
+    // surface slot of each owned row (face_index inverse, -1: interior node)
+    const int slot0 = prm.fidx[nf + r0], slot1 = prm.fidx[nf + r1], slotX = xrow ? prm.fidx[nf + rX] : -1;
+    const int npairs = (prm.K + 1) / 2;
+    const int gw = blockIdx.x * W::WARPS + warp, nw = gridDim.x * W::WARPS;
+
+    auto issue = [&](int pr) {
+        const int k0 = 2 * pr;
+        const int ne = k0 + 1 < prm.K ? 2 : 1;
+        const double* gu = prm.u + (size_t)k0 * 3 * nq;
+        for (int x = lane; x < ne * 3 * nq; x += 32) {
+            const int e = x / (3 * nq), r = x - e * 3 * nq;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sU + r)),
+                         "l"(gu + x)
+                         : "memory");
+        }
+        for (int x = lane; x < ne * 4 * nq; x += 32) {
+            const int e = x / (4 * nq), r = x - e * 4 * nq, c = r / nq, i = r - c * nq;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sG + r)),
+                         "l"(prm.gf + (size_t)(k0 + e) * 4 * nrow + c * nrow + i)
+                         : "memory");
+        }
+        cp_async_commit();
+    };
+
+    if (gw < npairs) issue(gw);
+    for (int pr = gw; pr < npairs; pr += nw) {
+        const int k = 2 * pr + half;
+        const bool valid = k < prm.K;
+        cp_async_wait_all();
+        __syncwarp();
+        // ---- park: staging -> packed node arrays (+ velocities, positivity)
+        {
+            const double* st = stage + half * W::stage_stride;
+            for (int j = lp; j < nq; j += 16) {
+                const double h = st[W::sU + j], hu = st[W::sU + nq + j], hv = st[W::sU + 2 * nq + j];
+                if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);  // check_positive (:381)
+                const double ih = 1.0 / h;
+                reinterpret_cast<double2*>(work + W::wA)[j] = make_double2(hu, hv);
+                reinterpret_cast<double2*>(work + W::wB)[j] = make_double2(hu * ih, hv * ih);
+                reinterpret_cast<double2*>(work + W::wC)[j] = make_double2(st[W::sG + j], st[W::sG + nq + j]);
+                reinterpret_cast<double2*>(work + W::wD)[j] = make_double2(st[W::sG + 2 * nq + j], st[W::sG + 3 * nq + j]);
+                work[W::wH + j] = h;
+            }
+        }
+        __syncwarp();
+        if (pr + nw < npairs) issue(pr + nw);
+
+        auto load_row = [&](Row6& r, int row) {
+            const double2 a = nA[row], c = nC[row], d = nD[row];
+            r.U = a.x;
+            r.V = a.y;
+            r.g1 = c.x;
+            r.g2 = c.y;
+            r.g3 = d.x;
+            r.g4 = d.y;
+            r.a0 = r.a1 = r.a2 = r.b1 = r.b2 = 0.0;
+        };
+        Row6 R0, R1, RX;
+        load_row(R0, r0);
+        load_row(R1, r1);
+        load_row(RX, xrow ? rX : 32);
+        // ---- rows l', l'+16 x all 37 columns
+#pragma unroll 1
+        for (int j0 = 0; j0 < 36; j0 += 4) {
+            double2 qa[4], qb[4];
+            tmem_ld16(tbase + W::t0 + 4 * j0, qa);
+            tmem_ld16(tbase + W::t1 + 4 * j0, qb);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int j = j0 + p;
+                const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
+                const double hj = nH[j];
+                pair6(R0, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
+                pair6(R1, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
+            }
+        }
+        {
+            const double2 qa = tmem_ld4(tbase + W::t0 + 4 * 36), qb = tmem_ld4(tbase + W::t1 + 4 * 36);
+            const double2 A = nA[36], B = nB[36], C = nC[36], D = nD[36];
+            pair6(R0, qa, A, B, C.x, C.y, D.x, D.y, nH[36]);
+            pair6(R1, qb, A, B, C.x, C.y, D.x, D.y, nH[36]);
+        }
+        // ---- rows 32..36: columns ph, ph+3, ... (13 slots), three lanes per row
+#pragma unroll
+        for (int s0 = 0; s0 < 16; s0 += 4) {
+            double2 qx[4];
+            tmem_ld16(tbase + W::tX + 4 * s0, qx);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int s = s0 + t, j = ph + 3 * s;
+                if (xrow && s < 13 && j < nq) {
+                    const double2 C = nC[j], D = nD[j];
+                    pair6(RX, qx[t], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o <= 2; ++o) {  // partial sums of lanes 3r+1, 3r+2 into lane 3r
+            const double s0 = __shfl_down_sync(0xffffffffu, RX.a0, o), s1 = __shfl_down_sync(0xffffffffu, RX.a1, o);
+            const double s2 = __shfl_down_sync(0xffffffffu, RX.a2, o), s3 = __shfl_down_sync(0xffffffffu, RX.b1, o);
+            const double s4 = __shfl_down_sync(0xffffffffu, RX.b2, o);
+            if (ph == 0) {
+                RX.a0 += s0;
+                RX.a1 += s1;
+                RX.a2 += s2;
+                RX.b1 += s3;
+                RX.b2 += s4;
+            }
+        }
+        // ---- per row: row constants, surface term, source, inverse mass (solver.hpp:395-428)
+        auto finish = [&](Row6& R, const int row, const int slot) {
+            const double hi = nH[row];
+            const double2 uv = nB[row];
+            const double Ui = R.U, Vi = R.V, ui = uv.x, vi = uv.y;
+            row_finish(R, ui, vi, g2 * hi);
+            double acc0 = 2.0 * R.a0, acc1 = R.a1, acc2 = R.a2;
+            if (slot >= 0) {
+                const int f = slot / npf;
+                const double* sf = prm.surf + (size_t)k * 3 * nf + slot;
+                const double m = sf[0], nxi = sf[nf], nyi = sf[2 * nf];
+                const double Bx = m * nxi, By = m * nyi;
+                double up[3];
+                const int nb = prm.nbr[(size_t)k * 3 + f];
+                if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
+                    const double un = Ui * nxi + Vi * nyi;
+                    up[0] = hi;
+                    up[1] = Ui - 2.0 * un * nxi;
+                    up[2] = Vi - 2.0 * un * nyi;
+                } else {
+                    const int jn = prm.fidx[prm.perm[(size_t)k * nf + slot]];
+                    const double* un = prm.u + (size_t)nb * 3 * nq + jn;
+                    up[0] = un[0];
+                    up[1] = un[nq];
+                    up[2] = un[2 * nq];
+                }
+                const double ip = 1.0 / up[0];
+                const double uxa = up[1] * ip, uya = up[2] * ip;
+                const double p = 0.5 * g * up[0] * hi;  // g {h}^2 - g/4 (h+^2 + h^2) = g/2 h+ h
+                const double ux = 0.5 * (uxa + ui), uy = 0.5 * (uya + vi);
+                const double hu = 0.5 * (up[1] + Ui), hv = 0.5 * (up[2] + Vi);
+                const double pp = 0.5 * g * hi * hi;
+                const double dx1 = __fma_rn(hu, ux, p) - __fma_rn(Ui, ui, pp);
+                const double dy2 = __fma_rn(hv, uy, p) - __fma_rn(Vi, vi, pp);
+                acc0 += __fma_rn(Bx, hu - Ui, By * (hv - Vi));
+                acc1 += __fma_rn(Bx, dx1, By * (hv * ux - Vi * ui));
+                acc2 += __fma_rn(Bx, hu * uy - Ui * vi, By * dy2);
+                if (prm.lf) {
+                    const double wl = fabs(ui * nxi + vi * nyi) + sqrt(g * hi);
+                    const double wr = fabs(uxa * nxi + uya * nyi) + sqrt(g * up[0]);
+                    const double mhl = 0.5 * m * fmax(wl, wr);
+                    acc0 = __fma_rn(-mhl, up[0] - hi, acc0);
+                    acc1 = __fma_rn(-mhl, up[1] - Ui, acc1);
+                    acc2 = __fma_rn(-mhl, up[2] - Vi, acc2);
+                }
+            }
+            const double* sr = prm.src + (size_t)k * 2 * nq;
+            const double gh = g * hi;
+            const double mv = prm.minv[(size_t)k * nq + row];
+            const double d0 = mv * -acc0;
+            const double d1 = mv * (-acc1 - gh * sr[row]);
+            const double d2 = mv * (-acc2 - gh * sr[nq + row]);
+            if (!(isfinite(d0) && isfinite(d1) && isfinite(d2))) record_error(prm.err, prm.stage_id, 1, k);
+            const size_t o = (size_t)k * 3 * nq + row;
+            if (prm.u_next) {  // fused LSRK45 update into the other state buffer (neighbours read u)
+                const double uo[3] = {hi, Ui, Vi}, dd[3] = {d0, d1, d2};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double r = __fma_rn(prm.rk_a, prm.res[o + c * nq], prm.dt * dd[c]);
+                    prm.res[o + c * nq] = r;
+                    prm.u_next[o + c * nq] = __fma_rn(prm.rk_b, r, uo[c]);
+                }
+            } else {
+                double* out = (prm.rk_mode ? prm.du_scratch : prm.du) + o;
+                out[0] = d0;
+                out[nq] = d1;
+                out[2 * nq] = d2;
+            }
+        };
+        if (valid) {
+            finish(R0, r0, slot0);
+            finish(R1, r1, slot1);
+            if (xrow && ph == 0) finish(RX, rX, slotX);
+        }
+        __syncwarp();
+    }
+    cp_async_wait_all();
+
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(W::tcols));
+}
+
+}  // namespace swedg

@@ -24,6 +24,7 @@
 #include "modal_quad_n4.cuh"
 #include "modal_pair_n4.cuh"
 #include "sbp_kernels.cuh"
+#include "sbp_pair_n4.cuh"
 #include "diag_kernels.cuh"
 #include "ratio_kernels.cuh"
 
@@ -65,6 +66,7 @@ struct swedg_handle_s {
     double* bs = nullptr;    // [K][nh] (modal)
     double* src = nullptr;   // [K][2][nh] (SBP: [K][2][nq])
     double* u = nullptr;     // resident state
+    double* u_alt = nullptr; // SBP pair path: second state buffer (fused RK stages ping-pong)
     double* res = nullptr;   // LSRK register
     double* utmp = nullptr;  // host-API scratch state
     double* du = nullptr;    // host-API scratch rhs
@@ -258,6 +260,7 @@ struct StageArgs {
     unsigned stage_id;
     bool early_exit;
     int k0 = 0, k1 = -1;  // volume part: element range [k0, k1) (k1 < 0: all K)
+    double* u_next = nullptr;  // SBP pair kernel: fused RK update into this buffer
 };
 
 template <int N>
@@ -401,6 +404,7 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
     sp.stage_id = sa.stage_id;
     sp.early_exit = sa.early_exit ? 1 : 0;
     sp.du_scratch = h->du;
+    sp.u_next = sa.u_next;
     using C = SbpCfg<N>;
     const size_t smem = SbpSmem<N>::bytes(C::E);
     const int grid = (h->K + C::E - 1) / C::E;
@@ -410,13 +414,20 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
     };
     {
         KTimer kt(h, 0);
-        if (h->mode == SWEDG_MODE_PARITY)
+        if (h->mode == SWEDG_MODE_PARITY) {
             go(sbp_rhs_kernel<N, true>);
-        else
+        } else if (N == 4 && h->vol_variant == 0) {  // pair kernel, operators in TMEM
+            auto kern = sbp_rhs_pair_n4_kernel;
+            const size_t psm = SbpPairN4::bytes();
+            const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, SbpPairN4::T, psm);
+            const int blocks = (h->K + 2 * SbpPairN4::WARPS - 1) / (2 * SbpPairN4::WARPS);
+            kern<<<std::max(1, std::min(blocks, occ * h->nsm)), SbpPairN4::T, psm, h->stream>>>(sp);
+        } else {
             go(sbp_rhs_kernel<N, false>);
+        }
     }
     h->launches++;
-    if (sa.rk) {
+    if (sa.rk && !sa.u_next) {
         // the SBP RHS reads neighbour states: the RK update runs after all du are known
         SbpUpdateParams up;
         up.n = (size_t)h->K * 3 * h->nq;
@@ -533,7 +544,23 @@ int run_fused_tail(swedg_handle h, const unsigned* ids, double dt) {
 }
 
 // One LSRK45 step on the resident state: 6 launches on the fused path, else 10.
+bool sbp_pair_path(swedg_handle h) {
+    return h->scheme == SWEDG_SCHEME_SBP && h->mode == SWEDG_MODE_FAST && h->N == 4 && h->vol_variant == 0;
+}
+
 int run_step(swedg_handle h, const unsigned* ids, double dt) {
+    if (sbp_pair_path(h)) {
+        // stages 0..3 fuse the RK update and ping-pong the state (u -> u_alt -> u -> ...):
+        // neighbours read the stage's input; stage 4 (input in u) uses the separate
+        // update kernel in place, so the step ends with the state in h->u
+        for (int s = 0; s < 5; ++s) {
+            double* in = (s & 1) ? h->u_alt : h->u;
+            StageArgs sa{in, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
+            sa.u_next = s < 4 ? ((s & 1) ? h->u : h->u_alt) : nullptr;
+            if (run_stage(h, sa)) return h->last_code;
+        }
+        return SWEDG_OK;
+    }
     if (fused_path(h)) {
         StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, ids[0], true};
         if (run_stage(h, sa)) return h->last_code;
@@ -919,7 +946,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     }
     const size_t ns = K * 3 * h->nstate();
     if (dalloc(h, &h->u, ns) || dalloc(h, &h->res, ns)) return bail(h->last_code);
-    if (h->scheme == SWEDG_SCHEME_SBP && dalloc(h, &h->du, ns)) return bail(h->last_code);
+    if (h->scheme == SWEDG_SCHEME_SBP && (dalloc(h, &h->du, ns) || dalloc(h, &h->u_alt, ns))) return bail(h->last_code);
     if (dalloc(h, &h->err, 1)) return bail(h->last_code);
     ErrRec none_rec{kNoError, 0ull};
     if (cudaMemcpyAsync(h->err, &none_rec, sizeof(none_rec), cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
@@ -940,7 +967,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
-                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2};
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2, h->u_alt};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& p : h->ev_pending) {
