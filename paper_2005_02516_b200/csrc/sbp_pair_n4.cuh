@@ -138,6 +138,27 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         }
         __syncwarp();
         if (pr + nw < npairs) issue(pr + nw);
+        if (valid) {  // L2 prefetch of this pair's finish-phase inputs (consumed after the flux loops)
+            const char* line = nullptr;
+            const size_t ke = (size_t)k;
+            switch (lp) {  // 16 lanes per element, one 128-byte line each
+                case 0: case 1: case 2: case 3: case 4: case 5: case 6:
+                    line = (const char*)(prm.res + ke * 3 * nq) + 128 * lp; break;   // 888 B
+                case 7: case 8: case 9: case 10: case 11:
+                    line = (const char*)(prm.src + ke * 2 * nq) + 128 * (lp - 7); break;  // 592 B
+                case 12: case 13:
+                    line = (const char*)(prm.minv + ke * nq) + 128 * (lp - 12); break;  // 296 B
+                case 14: line = (const char*)(prm.surf + ke * 3 * nf); break;         // 360 B
+                default: line = (const char*)(prm.surf + ke * 3 * nf) + 128; break;
+            }
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
+            if (lp < 3) {
+                const char* l2 = lp == 0 ? (const char*)(prm.minv + ke * nq) + 256
+                               : lp == 1 ? (const char*)(prm.surf + ke * 3 * nf) + 256
+                                         : (const char*)(prm.perm + ke * nf);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(l2));
+            }
+        }
 
         auto load_row = [&](Row6& r, int row) {
             const double2 a = nA[row], c = nC[row], d = nD[row];
