@@ -228,6 +228,8 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         }
         __syncwarp();
         if (pr + nw < npairs) issue(pr + nw);
+        if (valid && lp < 5)  // L2 prefetch of this element's source rows (read after the flux loops)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(prm.src + (size_t)k * 2 * nh) + 128 * lp));
 
         // ---- interface phase of stage s-1 (modal_surface_kernel<4,false> arithmetic):
         //      lane l' < 15 = surface slot l' and modal coefficient l' of its element
