@@ -511,8 +511,7 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
 #pragma unroll 1
         for (int j0 = 0; j0 < 24; j0 += 4) {
             double2 qa[4], qb[4];
-            tmem_ld16(tbase + W::tA + 4 * j0, qa);
-            tmem_ld16(tbase + W::tB + 4 * j0, qb);
+            tmem_ld16x2(tbase + W::tA + 4 * j0, tbase + W::tB + 4 * j0, qa, qb);
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const int j = j0 + p;
@@ -544,8 +543,7 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
 #pragma unroll 1
         for (int j0 = nq; j0 < nh; j0 += 4) {
             double2 qa[4], qb[4];
-            tmem_ld16(tbase + W::tA + 4 * j0, qa);
-            tmem_ld16(tbase + W::tB + 4 * j0, qb);
+            tmem_ld16x2(tbase + W::tA + 4 * j0, tbase + W::tB + 4 * j0, qa, qb);
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const int j = j0 + p;

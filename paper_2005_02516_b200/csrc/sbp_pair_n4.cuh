@@ -178,8 +178,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
 #pragma unroll 1
         for (int j0 = 0; j0 < 36; j0 += 4) {
             double2 qa[4], qb[4];
-            tmem_ld16(tbase + W::t0 + 4 * j0, qa);
-            tmem_ld16(tbase + W::t1 + 4 * j0, qb);
+            tmem_ld16x2(tbase + W::t0 + 4 * j0, tbase + W::t1 + 4 * j0, qa, qb);
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const int j = j0 + p;
