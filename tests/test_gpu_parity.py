@@ -293,3 +293,23 @@ def test_odd_element_count_imported_mesh(N):
     hf.set_state(uh)
     hf.step_host(uh, dt, 3, 2)
     assert rel(uh, u_ref) <= RUN_TOL
+
+
+@pytest.mark.parametrize("scheme", ["modal", "sbp"])
+def test_positivity_error_in_pair_kernels(scheme):
+    """FAST N=4 pair kernels (modal and SBP) report a nonpositive height with the
+    reference's element id, from rhs() and from graph-replayed steps."""
+    sc = capi.SCHEME_SBP if scheme == "sbp" else capi.SCHEME_HYBRIDIZED
+    c = capi.Case("smooth", scheme=sc, N=4, nx=8, warp=0.1)
+    h = c.handle(mode=capi.MODE_FAST)
+    u = c.u0()
+    u[77, 0, :] = -1.0 if sc == capi.SCHEME_SBP else 0.0
+    if sc != capi.SCHEME_SBP:
+        u[77, 0, 0] = -1.0
+    with pytest.raises(capi.PositivityError) as ei:
+        h.rhs(u)
+    assert ei.value.elem == 77
+    h.set_state(u, None, 0.125)
+    with pytest.raises(capi.PositivityError) as ei:
+        h.step(1e-4, 3)
+    assert ei.value.elem == 77 and abs(ei.value.t - 0.125) < 1e-12
