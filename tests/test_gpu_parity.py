@@ -313,3 +313,19 @@ def test_positivity_error_in_pair_kernels(scheme):
     with pytest.raises(capi.PositivityError) as ei:
         h.step(1e-4, 3)
     assert ei.value.elem == 77 and abs(ei.value.t - 0.125) < 1e-12
+
+
+@pytest.mark.parametrize("variant", ["tworow", "row", "warp", "quad"])
+def test_opt_in_volume_kernel_variants(variant):
+    """The opt-in FAST volume kernels kept for comparison (SWEDG_VOLUME_KERNEL; DESIGN §4.1
+    history) stay correct: N=4 modal and SBP rhs within the FAST acceptance criterion."""
+    import os
+    os.environ["SWEDG_VOLUME_KERNEL"] = variant
+    try:
+        for name in ("modal_n4_warp", "sbp_dam_n4"):
+            c = load_golden(name)
+            h = make(c, capi.MODE_FAST)
+            assert_fast_rhs(h.rhs(c["u"]), c["du_lf"], c, c["u"])
+            h.close()
+    finally:
+        os.environ.pop("SWEDG_VOLUME_KERNEL", None)
