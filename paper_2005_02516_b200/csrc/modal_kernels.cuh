@@ -376,6 +376,7 @@ modal_surface_kernel(ModalSurfParams prm) {
         const double* src = prm.Mpk + (size_t)k0 * NPK;
         for (int x = tid; x < ne * NPK; x += T) sMpk[x] = src[x];
     }
+    static_assert(32 % L == 0, "an element's lanes must lie in one warp");
 
     // ---- issue every independent global load up front (memory-level parallelism:
     //      ncu showed this kernel long-scoreboard bound with phase-serial loads)
@@ -451,7 +452,7 @@ modal_surface_kernel(ModalSurfParams prm) {
         sst[e][nf + s] = A::sub(A::mul(mgh, srx), acc[1]);
         sst[e][2 * nf + s] = A::sub(A::mul(mgh, sry), acc[2]);
     }
-    __syncthreads();
+    __syncthreads();  // the CTA's staged V_f / M_h^{-1}, and this element's stacked rows
     // modal = T1 + Vf^T stacked_surface  (solver.hpp:285-286)
     if (act && s < Np) {
 #pragma unroll
@@ -462,7 +463,7 @@ modal_surface_kernel(ModalSurfParams prm) {
             smod[e][c * Np + s] = A::add(t1r[c], t2);
         }
     }
-    __syncthreads();
+    __syncwarp();  // an element's L lanes lie in one warp (L divides 32)
     // du = Mh_inv modal; finiteness; fused LSRK45 register update
     if (act && s < Np) {
         double du[3] = {0.0, 0.0, 0.0};
