@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--k1d", type=int, default=1024)
     p.add_argument("--warp", type=float, default=0.1)
     p.add_argument("--mode", choices=["fast", "parity"], default="fast")
-    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ref-k1d", type=int, default=128, help="reference CPU sample size")
     return p.parse_args()
@@ -427,8 +427,10 @@ def run_ours(args, rank, world, local):
         "config": workload_config(args, args.k1d, world),
         "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes,
+                "steps": args.e2e_steps,
                 "path": "swedg_step_lsrk45_host: per step H2D of the state from pinned host memory + 5 "
-                        "stages + D2H of the result, chunk-pipelined (N>1: swedg_set_state + stages + "
+                        "stages + D2H of the result; 16 element chunks run through the stages as a "
+                        "wavefront so copies overlap compute (N>1: swedg_set_state + stages + "
                         "swedg_get_state)"},
         "gpu_launches": launches,
         "roofline": roofline,

@@ -144,9 +144,13 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync);
 /* The same steps on a HOST-resident state u_host [K][3][Np] (the reference's
  * calling pattern: state.u lives on the host between steps).  Each step reads
  * its input from u_host and writes its result back; the transfers are
- * pipelined with the compute in `nchunks` element chunks (0 = 16): step n's D2H,
- * step n+1's H2D (full duplex) and the element-local stage-1 volume kernel
- * overlap.  u_host should be pinned.  Syncs and checks errors at the end. */
+ * pipelined with the compute in `nchunks` element chunks (0 = 16).  When every
+ * element's neighbours lie in its own or an adjacent chunk (row-ordered meshes),
+ * the chunks run through the stages and steps as a wavefront, so a chunk's
+ * D2H, its H2D for the next step and other chunks' kernels all overlap;
+ * otherwise only the first stage's volume kernel and the last stage's interface
+ * kernel overlap the copies.  u_host should be pinned.  Syncs and checks errors
+ * at the end; results are bit-for-bit those of swedg_step_lsrk45. */
 int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps, int nchunks);
 /* Replay nsteps >= 2 as a captured one-step CUDA graph (default on; off while
  * per-kernel timers are enabled). */

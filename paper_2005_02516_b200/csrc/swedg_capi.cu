@@ -97,6 +97,9 @@ struct swedg_handle_s {
     cudaStream_t cp_in = nullptr, cp_out = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_out;
     cudaEvent_t ev_step = nullptr;
+    std::vector<cudaEvent_t> ev_s4;  // wavefront host stepping: last interface kernel of a chunk done
+    int wave_C = 0;                  // chunk count the adjacency check below was made for
+    bool wave_ok = false;            // every element's neighbours lie in its own or an adjacent chunk
     size_t dev_bytes = 0;
     bool bathy_set = false;
     unsigned next_stage = 1;
@@ -978,6 +981,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     for (auto e : h->ev_in) cudaEventDestroy(e);
     for (auto e : h->ev_out) cudaEventDestroy(e);
+    for (auto e : h->ev_s4) cudaEventDestroy(e);
     if (h->ev_step) cudaEventDestroy(h->ev_step);
     if (h->cp_in) cudaStreamDestroy(h->cp_in);
     if (h->cp_out) cudaStreamDestroy(h->cp_out);
@@ -1667,6 +1671,111 @@ int swedg_ratio_kernels(int device, int n, int nq, int K, const double* Q, const
     return rc;
 }
 
+namespace {
+// Element chunk c = [K c / C, K (c+1) / C).  The wavefront schedule needs every
+// neighbour of a chunk-c element in chunk c-1, c or c+1 (cyclically): true for the
+// row-ordered structured meshes of the native setup, checked once per chunk count.
+bool wave_adjacent(swedg_handle h, int C) {
+    if (h->wave_C == C) return h->wave_ok;
+    std::vector<int> nbr((size_t)h->K * 3);
+    if (cudaMemcpy(nbr.data(), h->nbr, nbr.size() * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    std::vector<int> chunk(h->K);
+    for (int c = 0; c < C; ++c)
+        for (long e = (long)h->K * c / C; e < (long)h->K * (c + 1) / C; ++e) chunk[e] = c;
+    bool ok = true;
+    for (long e = 0; e < h->K && ok; ++e)
+        for (int f = 0; f < 3; ++f) {
+            const int nb = nbr[e * 3 + f];
+            if (nb < 0) continue;
+            const int d = ((chunk[nb] - chunk[e]) % C + C) % C;
+            if (!(d == 0 || d == 1 || d == C - 1)) ok = false;
+        }
+    h->wave_C = C;
+    h->wave_ok = ok;
+    return ok;
+}
+
+// Wavefront host-state stepping: every (global stage g, chunk) volume and interface
+// kernel is enqueued on the compute stream in an order that lets early chunks run
+// ahead through the stages and across steps while later chunks are still being
+// copied.  Chunks are visited in ring order A = 0, 1, C-1, 2, C-2, ... so that the
+// neighbours of the chunk at position p sit at positions p-2..p+2; volume(g, p) is
+// enqueued at tick 6g + p and interface(g, p) at tick 6g + p + 3, which orders every
+// dependency (traces of positions p±2, the update of position p, the trace buffer
+// reuse of the next stage) before its consumer in the single compute stream.
+// Copies: H2D(n, c) waits for D2H(n-1, c) (host round trip); the stage-0 volume of
+// chunk c waits for H2D(n, c); D2H(n, c) waits for the step's last interface kernel
+// on chunk c.
+int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, int C) {
+    const size_t per = (size_t)3 * h->Np;
+    auto lo = [&](int c) { return (int)((long)h->K * c / C); };
+    std::vector<int> A;
+    A.push_back(0);
+    for (int k = 1; (int)A.size() < C; ++k) {
+        A.push_back(k);
+        if ((int)A.size() < C) A.push_back(C - k);
+    }
+    while ((int)h->ev_s4.size() < C) {
+        cudaEvent_t e;
+        CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_s4.push_back(e);
+    }
+    const int G = 5 * nsteps;
+    std::vector<unsigned> ids(G);
+    std::vector<double> tstep(nsteps + 1);
+    tstep[0] = h->t;
+    for (int n = 0; n < nsteps; ++n) {
+        for (int s = 0; s < 5; ++s) ids[5 * n + s] = new_stage(h, tstep[n] + Lsrk45::c[s] * dt);
+        tstep[n + 1] = tstep[n] + dt;
+    }
+    auto h2d = [&](int c) -> int {
+        const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+        CUDA_TRY(h, cudaMemcpyAsync(h->u + a, u_host + a, (e - a) * 8, cudaMemcpyHostToDevice, h->cp_in));
+        CUDA_TRY(h, cudaEventRecord(h->ev_in[c], h->cp_in));
+        return SWEDG_OK;
+    };
+    CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_step, 0));
+    for (int p = 0; p < C; ++p)
+        if (h2d(A[p])) return h->last_code;
+    const int ticks = 6 * (G - 1) + C + 3;
+    for (int tau = 0; tau < ticks; ++tau) {
+        for (int g = 0; g < G; ++g) {
+            const int s = g % 5;
+            const int pv = tau - 6 * g;  // volume(g, pv)
+            if (pv >= 0 && pv < C) {
+                const int c = A[pv];
+                if (s == 0) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
+                StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
+                             lo(c), lo(c + 1)};
+                if (run_stage(h, sa)) return h->last_code;
+            }
+            const int ps = tau - 6 * g - 3;  // interface(g, ps)
+            if (ps >= 0 && ps < C) {
+                const int c = A[ps];
+                StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
+                             lo(c), lo(c + 1)};
+                if (run_stage(h, ss)) return h->last_code;
+                if (s == 4) {  // chunk c finished step g / 5: copy it out, and back in for the next step
+                    const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+                    CUDA_TRY(h, cudaEventRecord(h->ev_s4[c], h->stream));
+                    CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_s4[c], 0));
+                    CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
+                    CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
+                    if (g / 5 + 1 < nsteps) {
+                        CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_out[c], 0));
+                        if (h2d(c)) return h->last_code;
+                    }
+                }
+            }
+        }
+    }
+    for (int c = 0; c < C; ++c) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_out[c], 0));
+    h->t = tstep[nsteps];
+    return check_errors(h);
+}
+}  // namespace
+
 // The reference's step_lsrk45 on a HOST-resident state (solver.hpp:466-484 called
 // in a loop with state.u on the host): every step's input is read from u_host
 // and its result written back to u_host.  The copies are pipelined with the
@@ -1702,6 +1811,8 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
         h->ev_in.push_back(a);
         h->ev_out.push_back(b);
     }
+    if (nsteps > 0 && !fused_path(h) && !h->timers && C >= 3 && wave_adjacent(h, C))
+        return step_host_wavefront(h, u_host, dt, nsteps, C);
     auto lo = [&](int c) { return (int)((long)h->K * c / C); };
     // the copy streams start after everything already queued on the handle stream
     CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
