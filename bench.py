@@ -327,15 +327,24 @@ def run_ours(args, rank, world, local):
     value = dof * world * 5 * args.steps / (ms * 1e-3) / 1e9
 
     # ---- e2e through the public API with pinned host buffers
-    uh = torch.empty((K, 3, Np), dtype=torch.float64, pin_memory=True).numpy()
+    uh_t = torch.empty((K, 3, Np), dtype=torch.float64, pin_memory=True)
+    uh = uh_t.numpy()
     uh[...] = u0
     h.set_state(uh)
+    stepper = None
+    if plan is not None:
+        from paper_2005_02516_b200.partition import HostStepper
+
+        stepper = HostStepper(h, plan, stream, comm_stream)
+    # untimed warm-up of the host-state path (copy streams, events, pinned pages)
     if plan is None:
-        h.step_host(uh, dt, 1)  # untimed warm-up of the host-state path (copy streams, pinned pages)
-        uh[...] = u0
-        h.set_state(uh)
+        h.step_host(uh, dt, 1)
     else:
-        steps(1, True)
+        stepper.step(uh_t, dt, 1)
+        torch.cuda.synchronize()
+        h.check()
+    uh[...] = u0
+    h.set_state(uh)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -347,10 +356,9 @@ def run_ours(args, rank, world, local):
         # transfers pipelined with the compute in element chunks
         h.step_host(uh, dt, args.e2e_steps)
     else:
-        for _ in range(args.e2e_steps):
-            h.set_state(uh)               # H2D of the step's input state
-            steps(1, False)               # 5 stages on the device (+ halo exchanges)
-            h.get_state(uh, with_res=False)  # D2H of the step's result
+        # per rank: H2D of the strip's state, 5 stages with halo exchanges, D2H of the
+        # result every step; chunked copies overlap the first and last stage
+        stepper.step(uh_t, dt, args.e2e_steps)
     ee1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1)
@@ -430,8 +438,8 @@ def run_ours(args, rank, world, local):
                 "steps": args.e2e_steps,
                 "path": "swedg_step_lsrk45_host: per step H2D of the state from pinned host memory + 5 "
                         "stages + D2H of the result; 16 element chunks run through the stages as a "
-                        "wavefront so copies overlap compute (N>1: swedg_set_state + stages + "
-                        "swedg_get_state)"},
+                        "wavefront so copies overlap compute (N>1: partition.HostStepper, chunked "
+                        "copies overlapping the first and last stage around the halo exchanges)"},
         "gpu_launches": launches,
         "roofline": roofline,
         "roofline_surface": roofline_surface,

@@ -172,6 +172,9 @@ int swedg_stage_surface(swedg_handle h, int stage, double dt);
  * opens the stage; the ranges of one stage must cover [0, K) before
  * swedg_stage_surface. */
 int swedg_stage_volume_range(swedg_handle h, int stage, double dt, int k0, int k1);
+/* swedg_stage_surface on [k0, k1) (e.g. to copy finished chunks out while the rest
+ * runs); the range ending at k1 == K closes the step (advances t) for stage 4. */
+int swedg_stage_surface_range(swedg_handle h, int stage, double dt, int k0, int k1);
 int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo);
 /* Check the device error record (syncs the stream). */
 int swedg_check(swedg_handle h);

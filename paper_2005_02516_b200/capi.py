@@ -122,6 +122,7 @@ def lib() -> C.CDLL:
     L.swedg_stage_volume.argtypes = [vp, C.c_int, C.c_double]
     L.swedg_stage_surface.argtypes = [vp, C.c_int, C.c_double]
     L.swedg_stage_volume_range.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_int]
+    L.swedg_stage_surface_range.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_int]
     L.swedg_trace_device_ptr.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
     L.swedg_set_diagnostics.argtypes = [vp, C.POINTER(_DiagDesc)]
     L.swedg_compute_invariants.argtypes = [vp, _dp, C.c_double, _dp]
@@ -152,7 +153,7 @@ EXPORTED = [
     "swedg_set_diagnostics", "swedg_compute_invariants", "swedg_l2_error", "swedg_diag_raw_bytes",
     "swedg_diag_raw", "swedg_diag_from_raw", "swedg_sample_invariants", "swedg_read_invariants",
     "swedg_read_invariants_raw", "swedg_run", "swedg_exact_sum", "swedg_ratio_kernels",
-    "swedg_step_lsrk45_host", "swedg_stage_volume_range",
+    "swedg_step_lsrk45_host", "swedg_stage_volume_range", "swedg_stage_surface_range",
 ]
 
 
@@ -315,6 +316,9 @@ class Handle:
 
     def stage_volume_range(self, stage: int, dt: float, k0: int, k1: int):
         self._check(self._lib.swedg_stage_volume_range(self._h, int(stage), float(dt), int(k0), int(k1)))
+
+    def stage_surface_range(self, stage: int, dt: float, k0: int, k1: int):
+        self._check(self._lib.swedg_stage_surface_range(self._h, int(stage), float(dt), int(k0), int(k1)))
 
     def stage_surface(self, stage: int, dt: float):
         self._check(self._lib.swedg_stage_surface(self._h, int(stage), float(dt)))

@@ -1336,6 +1336,22 @@ int swedg_stage_surface(swedg_handle h, int stage, double dt) {
     return rc;
 }
 
+int swedg_stage_surface_range(swedg_handle h, int stage, double dt, int k0, int k1) {
+    if (!h || stage < 0 || stage > 4 || k0 < 0 || k1 < k0 || k1 > h->K) return SWEDG_ERR_INVALID;
+    if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
+    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
+        return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
+    cudaSetDevice(h->device);
+    int rc = SWEDG_OK;
+    if (k1 > k0) {
+        StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true,
+                     k0, k1};
+        rc = run_stage(h, sa);
+    }
+    if (rc == SWEDG_OK && stage == 4 && k1 == h->K) h->t = h->t + dt;  // the range ending at K closes the step
+    return rc;
+}
+
 int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo) {
     if (!h) return SWEDG_ERR_INVALID;
     if (trace) *trace = h->trace;

@@ -106,6 +106,102 @@ def stage_overlapped(h, stage: int, dt: float, trace, plan: StripHalo, stream, c
     h.stage_surface(stage, dt)
 
 
+def state_tensor(handle):
+    """Zero-copy torch view [K][3][Np] of a handle's device-resident state."""
+    import torch
+
+    u_ptr, _ = handle.state_device_ptrs()
+    s = handle.sizes
+    return torch.as_tensor(_CudaArray(u_ptr, (s.K, 3, handle.nstate)), device="cuda")
+
+
+class HostStepper:
+    """Host-state LSRK45 steps of one rank (the multi-rank counterpart of
+    swedg_step_lsrk45_host): every step copies the rank's state in from a pinned
+    host buffer and its result back out, and the copies overlap the work:
+    the two boundary rows arrive first, the stage-0 volume kernel runs chunk by chunk
+    as the rest lands (the halo exchange starts after the boundary rows), and the
+    last interface kernel runs chunk by chunk, each chunk's D2H starting at once.
+    Stages 1..3 use stage_overlapped."""
+
+    def __init__(self, h, plan: StripHalo, stream, comm_stream, chunks: int = 16, group=None, exchange_fn=None):
+        import torch
+
+        self.h, self.plan, self.stream, self.comm = h, plan, stream, comm_stream
+        self.group, self.exchange_fn = group, exchange_fn
+        K, row = plan.K, plan.row
+        inner = max(1, min(chunks - 2, (K - 2 * row) // max(1, row)))
+        cuts = [row + (K - 2 * row) * i // inner for i in range(inner + 1)]
+        # processing order: first row, last row, then the interior from the bottom up
+        self.ranges = [(0, row), (K - row, K)] + [(cuts[i], cuts[i + 1]) for i in range(inner) if cuts[i] < cuts[i + 1]]
+        self.copy_in = torch.cuda.Stream(device=stream.device)
+        self.copy_out = torch.cuda.Stream(device=stream.device)
+        n = len(self.ranges)
+        self.ev_in = [torch.cuda.Event() for _ in range(n)]
+        self.ev_out = [torch.cuda.Event() for _ in range(n)]
+        self.ev_done = [torch.cuda.Event() for _ in range(n)]
+        self.trace = trace_tensor(h)
+        self.dev = state_tensor(h)
+
+    def _exchange(self):
+        ex = self.exchange_fn or (lambda t, p: exchange(t, p, self.group))
+        ex(self.trace, self.plan)
+
+    def step(self, host_u, dt: float, nsteps: int = 1) -> None:
+        """host_u: torch CPU tensor (pinned) [K][3][Np], updated in place every step."""
+        import torch
+
+        h, st, comm = self.h, self.stream, self.comm
+        K, row = self.plan.K, self.plan.row
+        ready = torch.cuda.Event()
+        ready.record(st)
+        self.copy_in.wait_event(ready)
+        for n in range(nsteps):
+            for i, (a, b) in enumerate(self.ranges):  # H2D, after the previous step's D2H of the chunk
+                if n > 0:
+                    self.copy_in.wait_event(self.ev_out[i])
+                with torch.cuda.stream(self.copy_in):
+                    self.dev[a:b].copy_(host_u[a:b], non_blocking=True)
+                self.ev_in[i].record(self.copy_in)
+            with torch.cuda.stream(st):
+                for s in range(5):
+                    if s in (1, 2, 3):
+                        stage_overlapped(h, s, dt, self.trace, self.plan, st, comm, self.group, self.exchange_fn)
+                        continue
+                    # boundary rows first (stage 0: as they land), exchange on the comm stream
+                    for i in (0, 1):
+                        if s == 0:
+                            st.wait_event(self.ev_in[i])
+                        h.stage_volume_range(s, dt, *self.ranges[i])
+                    boundary = torch.cuda.Event()
+                    boundary.record(st)
+                    with torch.cuda.stream(comm):
+                        comm.wait_event(boundary)
+                        self._exchange()
+                        halos = torch.cuda.Event()
+                        halos.record(comm)
+                    for i in range(2, len(self.ranges)):
+                        if s == 0:
+                            st.wait_event(self.ev_in[i])
+                        h.stage_volume_range(s, dt, *self.ranges[i])
+                    st.wait_event(halos)
+                    if s == 0:
+                        h.stage_surface(s, dt)
+                        continue
+                    # last stage: interface kernel by chunk (the range ending at K last), D2H right after
+                    order = sorted(range(len(self.ranges)), key=lambda i: self.ranges[i][1] == K)
+                    for i in order:
+                        a, b = self.ranges[i]
+                        h.stage_surface_range(s, dt, a, b)
+                        self.ev_done[i].record(st)
+                        self.copy_out.wait_event(self.ev_done[i])
+                        with torch.cuda.stream(self.copy_out):
+                            host_u[a:b].copy_(self.dev[a:b], non_blocking=True)
+                        self.ev_out[i].record(self.copy_out)
+        for e in self.ev_out:
+            st.wait_event(e)
+
+
 def copy_halos_local(traces, plans) -> None:
     """Single-process stand-in for `exchange` over P logical partitions (device copies)."""
     P = len(plans)

@@ -211,3 +211,31 @@ def test_stage_overlapped_single_rank_equals_step():
     h2.check()
     u2, _, _ = h2.get_state()
     np.testing.assert_array_equal(u1, u2)
+
+
+@pytest.mark.gpu
+def test_host_stepper_single_rank_equals_step():
+    """partition.HostStepper (per-rank host-state steps with chunked copies overlapping the
+    stage-0 volume and last interface kernels) on one rank == swedg_step_lsrk45, bitwise,
+    and the host buffer holds every step's result."""
+    from paper_2005_02516_b200.partition import HostStepper
+
+    c = capi.Case("smooth", N=4, nx=NX, ny=8, warp=0.1, threads=1)
+    dt = 1e-3
+    h1 = c.handle(mode=capi.MODE_FAST)
+    h1.set_state(c.u0())
+    h1.step(dt, 3)
+    u1, _, t1 = h1.get_state()
+    h2 = c.handle(mode=capi.MODE_FAST)
+    stream, comm = torch.cuda.Stream(), torch.cuda.Stream()
+    h2.set_stream(stream.cuda_stream)
+    h2.set_state(c.u0())
+    hu = torch.from_numpy(c.u0().copy()).pin_memory()
+    hs = HostStepper(h2, StripHalo(1, 0, NX, c.K), stream, comm, chunks=5)
+    hs.step(hu, dt, 3)
+    torch.cuda.synchronize()
+    h2.check()
+    np.testing.assert_array_equal(hu.numpy(), u1)
+    u2, _, t2 = h2.get_state()
+    np.testing.assert_array_equal(u2, u1)
+    assert t2 == t1
