@@ -147,7 +147,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
         "steps": r["steps"], "warmup": r["warmup"], "ms_per_step": r["ms_per_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args, args.ref_k1d),
+        "data": "synthetic", "config": workload_config(args, args.ref_k1d, reference=True),
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -156,12 +156,13 @@ def run_reference(args, rank, world):
     return 0
 
 
-def workload_config(args, k1d, world=1):
+def workload_config(args, k1d, world=1, reference=False):
     K = 2 * k1d * k1d
     cfg = {"workload": f"C4: modal ESDG N={args.N}, K1D={k1d} (K={K} curved tris, warp {args.warp}), "
                        "smooth wave + lake bathymetry, periodic [-1,1]^2, LF flux, LSRK45",
            "N": args.N, "K1D": k1d, "K": K, "warp": args.warp, "scheme": "hybridized",
-           "mode": args.mode, "step": "one LSRK45 step = 5 RHS stages",
+           "mode": "reference CPU (IEEE, reference order)" if reference else args.mode,
+           "step": "one LSRK45 step = 5 RHS stages",
            "l2": "inputs larger than L2 (device-resident state+geometry >> 126 MB)"}
     if world > 1:
         cfg["partition"] = (f"weak scaling: {world} y-strips of a K1D x (K1D*{world}) periodic mesh on "
