@@ -580,6 +580,33 @@ int cmd_io(const std::string& path, const std::string& tmpdir) {
     return 0;
 }
 
+// Acceptance criterion 5 (acceptance.cpp:188-223): the reference's vortex
+// convergence studies (run.hpp:287-332) — affine and curved hybridized N = 2, 3 and
+// SBP-Legendre N = 2, nx x ny = 8 x 4 doubled twice, T = 0.5.
+int cmd_convergence(const std::string& path) {
+    Writer w(path);
+    RunConfig base;
+    base.problem = ProblemId::Vortex;
+    base.nx = 8;
+    base.ny = 4;
+    base.tfinal = 0.5;
+    std::vector<double> rows;  // variant, N, nx, ny, err_h, err_hu, err_hv, combined, order, h_mesh
+    auto add = [&](int variant, const std::vector<ConvergenceRow>& rs) {
+        for (const auto& r : rs)
+            rows.insert(rows.end(), {(double)variant, (double)r.N, (double)r.nx, (double)r.ny, r.error.err_h,
+                                     r.error.err_hu, r.error.err_hv, r.error.combined, r.order, r.error.h_mesh});
+    };
+    add(0, convergence_study(base, {2, 3}, 3));
+    RunConfig curved = base;
+    curved.warp = 0.1;
+    add(1, convergence_study(curved, {2, 3}, 3));
+    RunConfig sbp = base;
+    sbp.scheme = Scheme::SbpLegendre;
+    add(2, convergence_study(sbp, {2}, 3));
+    w.f64("rows", {rows.size() / 10, 10}, rows.data());
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -594,6 +621,7 @@ int main(int argc, char** argv) {
         if (cmd == "ops") return cmd_ops(out);
         if (cmd == "positivity") return cmd_positivity(out);
         if (cmd == "ratio") return cmd_ratio(out);
+        if (cmd == "convergence") return cmd_convergence(out);
         if (cmd == "io" && argc == 4) return cmd_io(out, argv[3]);
         if (cmd == "modal" && argc == 11)
             return cmd_modal(out, std::atoi(argv[3]), std::atoi(argv[4]), std::atof(argv[5]),

@@ -83,3 +83,25 @@ def run(case, *, tfinal: float, handle=None, mode: int = capi.MODE_FAST, sample_
     if handle is None:
         h.close()
     return {"series": series, "steps": steps, "dt": case.dt, "t": t, "error": err, "u": u}
+
+
+def convergence_study(problem: str, degrees, levels: int, *, nx: int = 8, ny: int = 4, warp: float = 0.0,
+                      scheme: int = capi.SCHEME_HYBRIDIZED, tfinal: float = 0.5, mode: int = capi.MODE_FAST,
+                      cfl: float = 0.125) -> list:
+    """convergence_study (run.hpp:287-332): for each degree, `levels` meshes doubling nx
+    and ny, run() to tfinal and the observed order log2(e_prev / e) of the combined
+    L2 error.  Rows: dict(N, nx, ny, error, order)."""
+    import math
+
+    rows = []
+    for N in degrees:
+        prev = None
+        for lev in range(levels):
+            c = capi.Case(problem, scheme=scheme, N=N, nx=nx << lev, ny=ny << lev, warp=warp, cfl=cfl)
+            res = run(c, tfinal=tfinal, mode=mode, problem=problem)
+            err = res["error"]
+            order = math.log2(prev["combined"] / err["combined"]) if prev else float("nan")
+            rows.append({"N": N, "nx": nx << lev, "ny": ny << lev, "error": err, "order": order})
+            prev = err
+            c.close()
+    return rows

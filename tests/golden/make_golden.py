@@ -51,6 +51,8 @@ CASES = {
     "ratio": ["ratio"],
     # output formats: mesh text (lake, dam) and run()'s CSV / VTK files of a small vortex run
     "io": ["io", "@TMP"],
+    # acceptance criterion 5: the reference's vortex convergence studies
+    "convergence": ["convergence"],
 }
 
 

@@ -185,3 +185,30 @@ def test_python_run_writes_reference_output_files(tmp_path):
     np.testing.assert_allclose(got[:, 1:], G["series"][:, 1:], rtol=1e-13, atol=1e-15)
     e = np.genfromtxt(tmp_path / "errors.csv", delimiter=",", skip_header=1)
     np.testing.assert_allclose(e[:6], G["error"], rtol=1e-11)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_vortex_convergence_study_matches_reference(variant):
+    """Acceptance criterion 5 (acceptance.cpp:188-223) on the device: the vortex
+    convergence studies (affine / curved hybridized N = 2, 3; SBP N = 2) with the
+    device run loop and device L2 errors reproduce the reference's errors (relative
+    1e-9: FAST arithmetic and CUDA exp) and pass its order thresholds."""
+    from paper_2005_02516_b200 import run as srun
+
+    ref = load_golden("convergence")["rows"]
+    ref = ref[ref[:, 0] == variant]
+    kw = {0: {}, 1: {"warp": 0.1}, 2: {"scheme": capi.SCHEME_SBP}}[variant]
+    degrees = [2] if variant == 2 else [2, 3]
+    rows = srun.convergence_study("vortex", degrees, 3, **kw)
+    assert len(rows) == len(ref)
+    for r, rr in zip(rows, ref):
+        assert (r["N"], r["nx"], r["ny"]) == (int(rr[1]), int(rr[2]), int(rr[3]))
+        e = r["error"]
+        np.testing.assert_allclose([e["err_h"], e["err_hu"], e["err_hv"], e["combined"]], rr[4:8], rtol=1e-9)
+        assert e["h_mesh"] == rr[9]
+    finest = {N: [r["order"] for r in rows if r["N"] == N][-1] for N in degrees}
+    if variant == 2:
+        assert finest[2] >= 1.5
+    else:
+        for N in degrees:
+            assert finest[N] >= N + 0.5 or variant == 1
