@@ -185,3 +185,37 @@ def test_fast_sbp_entropy_balance_k1d32():
     r_ec, scale = rates[capi.PENALTY_EC]
     assert abs(r_ec) < 1e-9 * (1.0 + scale)
     assert rates[capi.PENALTY_LF][0] <= 1e-12 * (1.0 + scale)
+
+
+@pytest.mark.parametrize("mode", [capi.MODE_FAST, capi.MODE_PARITY])
+def test_acceptance_2_lake_at_rest_all_degrees(mode):
+    """Acceptance criterion 2 (acceptance.cpp:96-117) through the device run loop:
+    lake at rest, N = 1..4, 8x8 and 16x16, affine and curved, to t = 0.5: L2
+    deviation from the discrete steady state <= 1e-9 (the reference's worst: 4.2e-13)."""
+    from paper_2005_02516_b200 import run as srun
+
+    worst = 0.0
+    for N in range(1, 5):
+        for n in (8, 16):
+            for warp in (0.0, 0.1):
+                c = capi.Case("lake", N=N, nx=n, warp=warp)
+                res = srun.run(c, tfinal=0.5, mode=mode)
+                worst = max(worst, res["error"]["combined"])
+                c.close()
+    assert worst <= 1e-9, worst
+
+
+def test_acceptance_7_dam_break_robustness():
+    """Acceptance criterion 7 (acceptance.cpp:279-305): hybridized N = 3 dam break on
+    20x20 to t = 1.5 with CFL 0.0625 stays positive (min_h over the invariant series)
+    and conserves mass to 1e-8 (reference: min_h 1.146, drift 2.8e-14)."""
+    from paper_2005_02516_b200 import run as srun
+
+    c = capi.Case("dambreak", N=3, nx=20, cfl=0.0625)
+    res = srun.run(c, tfinal=1.5)
+    s = res["series"]
+    assert abs(res["t"] - 1.5) < 1e-12
+    min_h = s[:, 5].min()
+    drift = abs(s[-1, 1] - s[0, 1]) / s[0, 1]
+    assert min_h > 0.0 and drift <= 1e-8, (min_h, drift)
+    assert abs(min_h - 1.146) < 5e-3, min_h  # the reference's value (3 digits printed)
