@@ -46,6 +46,10 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ref-k1d", type=int, default=128, help="reference CPU sample size")
+    # functional check of the multi-rank orchestration on a single-GPU box (no timing
+    # claims): every rank on device 0, halos exchanged over gloo through host memory
+    p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
+    p.add_argument("--shared-device", action="store_true")
     return p.parse_args()
 
 
@@ -245,12 +249,17 @@ def run_ours(args, rank, world, local):
 
     from paper_2005_02516_b200 import capi
 
+    if args.shared_device:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     # weak scaling: rank r owns y-strip r (K1D x K1D quads) of a global
     # K1D x (K1D*world) periodic mesh; one halo exchange of face traces per stage
     # (paper_2005_02516_b200/partition.py, NCCL point-to-point over NVLink).

@@ -65,6 +65,14 @@ def exchange(trace, plan: StripHalo, group=None) -> None:
 
     if plan.P == 1:
         return
+    if trace.is_cuda and dist.get_backend(group) == "gloo":  # gloo P2P needs host tensors
+        host = trace.cpu()
+        exchange(host, plan, group)
+        c0, c1 = plan.recv_from_prev
+        d0, d1 = plan.recv_from_next
+        trace[c0:c1].copy_(host[c0:c1])
+        trace[d0:d1].copy_(host[d0:d1])
+        return
     a0, a1 = plan.send_to_next
     b0, b1 = plan.send_to_prev
     c0, c1 = plan.recv_from_prev
