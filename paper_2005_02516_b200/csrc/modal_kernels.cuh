@@ -361,22 +361,23 @@ modal_surface_kernel(ModalSurfParams prm) {
     if (prm.early_exit && error_pending(prm.err)) return;
 
     constexpr int NPK = Np * (Np + 1) / 2;
-    __shared__ double sVf[nf * Np];
     __shared__ double sst[E][3 * nf];
     __shared__ double smod[E][3 * Np];
     __shared__ double sMpk[P ? 1 : E * NPK];
+    const double* gVf = prm.ops + O::Vf;  // 1.8 KB, read through L1 by every warp
     const int tid = threadIdx.x;
-    for (int x = tid; x < nf * Np; x += T) sVf[x] = prm.ops[O::Vf + x];
     const int e = tid / L, s = tid % L;
     const int k = prm.k_begin + blockIdx.x * E + e;  // elements [k_begin, K)
     const bool act = k < prm.K;
     const double g = prm.g;
-    if constexpr (!P) {  // packed M_h^{-1} of the block's elements: one contiguous coalesced copy
-        const int k0 = prm.k_begin + blockIdx.x * E, ne = min(E, prm.K - k0);
-        const double* src = prm.Mpk + (size_t)k0 * NPK;
-        for (int x = tid; x < ne * NPK; x += T) sMpk[x] = src[x];
-    }
     static_assert(32 % L == 0, "an element's lanes must lie in one warp");
+    if constexpr (!P) {  // packed M_h^{-1} of the warp's elements: one contiguous coalesced copy per warp
+        constexpr int EW = 32 / L;  // elements per warp
+        const int lane = tid & 31, ew0 = (tid >> 5) * EW;
+        const int k0 = prm.k_begin + blockIdx.x * E + ew0, ne = max(0, min(EW, prm.K - k0));
+        const double* src = prm.Mpk + (size_t)k0 * NPK;
+        for (int x = lane; x < ne * NPK; x += 32) sMpk[ew0 * NPK + x] = src[x];
+    }
 
     // ---- issue every independent global load up front (memory-level parallelism:
     //      ncu showed this kernel long-scoreboard bound with phase-serial loads)
@@ -452,14 +453,14 @@ modal_surface_kernel(ModalSurfParams prm) {
         sst[e][nf + s] = A::sub(A::mul(mgh, srx), acc[1]);
         sst[e][2 * nf + s] = A::sub(A::mul(mgh, sry), acc[2]);
     }
-    __syncthreads();  // the CTA's staged V_f / M_h^{-1}, and this element's stacked rows
+    __syncwarp();  // this warp's M_h^{-1} block and its elements' stacked rows
     // modal = T1 + Vf^T stacked_surface  (solver.hpp:285-286)
     if (act && s < Np) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double t2 = 0.0;
 #pragma unroll
-            for (int i = 0; i < nf; ++i) t2 = A::fma(sVf[i + s * nf], sst[e][c * nf + i], t2);
+            for (int i = 0; i < nf; ++i) t2 = A::fma(__ldg(gVf + i + s * nf), sst[e][c * nf + i], t2);
             smod[e][c * Np + s] = A::add(t1r[c], t2);
         }
     }
