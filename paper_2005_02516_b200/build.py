@@ -28,7 +28,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, d) for d in DEPS]
+    deps = [os.path.join(CSRC, d) for d in sorted(set(DEPS) | set(os.listdir(CSRC)))]
     deps.append(os.path.join(os.path.dirname(PKG), "include", "swedg_b200.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 

@@ -132,6 +132,17 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     // ---- CTA setup
     for (int x = threadIdx.x; x < nq * Np; x += W::T) sVq[x] = prm.ops[O::Vq + x];
     for (int x = threadIdx.x; x < nf * Np; x += W::T) sVf[x] = prm.ops[O::Vf + x];
+    // QA, QB, Pq staged in the (still unused) work area with one coalesced pass of the
+    // CTA, so the TMEM fill below reads shared memory instead of making ~100
+    // dependent L2/DRAM round trips per lane
+    double* sQA = smem + W::ops_len;
+    double* sQB = sQA + nh * nh;
+    double* sPq = sQB + nh * nh;
+    for (int x = threadIdx.x; x < nh * nh; x += W::T) {
+        sQA[x] = __ldg(prm.ops + O::QA + x);
+        sQB[x] = __ldg(prm.ops + O::QB + x);
+    }
+    for (int x = threadIdx.x; x < Np * nq; x += W::T) sPq[x] = __ldg(prm.ops + O::Pq + x);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_addr_u32(&tmem_base_sh)),
@@ -143,28 +154,24 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tbase = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16);
     const int rA = lp, rB = lp + 16, rC = 32 + (lp & 7), par = lp >> 3;
-    if (warp < 4) {
-        const double* QA = prm.ops + O::QA;
-        const double* QB = prm.ops + O::QB;
-        for (int j = 0; j < nh; ++j) {
-            tmem_st4(tbase + W::tA + 4 * j, QA[rA + j * nh], QB[rA + j * nh]);
-            tmem_st4(tbase + W::tB + 4 * j, QA[rB + j * nh], QB[rB + j * nh]);
+    {  // rows depend only on l': one copy per TMEM lane quarter, filled by the
+       // quarter's four warps (column phase cph = warp >> 2)
+        const int cph = warp >> 2;
+        for (int j = cph; j < nh; j += 4) {
+            tmem_st4(tbase + W::tA + 4 * j, sQA[rA + j * nh], sQB[rA + j * nh]);
+            tmem_st4(tbase + W::tB + 4 * j, sQA[rB + j * nh], sQB[rB + j * nh]);
         }
-        for (int s = 0; s < 13; ++s) {
+        for (int s = cph; s < 13; s += 4) {
             const int j = par + 2 * s;
             const bool ok = j < nq;
-            tmem_st4(tbase + W::tC + 4 * s, ok ? QA[rC + j * nh] : 0.0, ok ? QB[rC + j * nh] : 0.0);
+            tmem_st4(tbase + W::tC + 4 * s, ok ? sQA[rC + j * nh] : 0.0, ok ? sQB[rC + j * nh] : 0.0);
         }
-        const double* gVq = prm.ops + O::Vq;
-        const double* gVf = prm.ops + O::Vf;
-        const double* gPq = prm.ops + O::Pq;
         const int rows[3] = {rA, rB, rC};
-        for (int q = 0; q < 3; ++q)
-            for (int m = 0; m < Np; ++m) {
-                const int r = rows[q];
-                tmem_st2(tbase + W::tV + 30 * q + 2 * m, r < nq ? gVq[r + m * nq] : gVf[(r - nq) + m * nf]);
-            }
-        for (int i = 0; i < nq; ++i) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? gPq[lp + i * Np] : 0.0);
+        for (int x = cph; x < 3 * Np; x += 4) {
+            const int q = x / Np, m = x - q * Np, r = rows[q];
+            tmem_st2(tbase + W::tV + 30 * q + 2 * m, r < nq ? sVq[r + m * nq] : sVf[(r - nq) + m * nf]);
+        }
+        for (int i = cph; i < nq; i += 4) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? sPq[lp + i * Np] : 0.0);
         asm volatile("tcgen05.wait::st.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -507,6 +514,18 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
                 af[2 * nf] = RC.a2;
             }
         }
+        // source rows of the volume rows: loaded now (L2 hits after the prefetch above),
+        // consumed after loop C, so the load latency hides behind the flux loops
+        double srcA[2] = {0.0, 0.0}, srcB[2] = {0.0, 0.0};
+        if (valid) {
+            const double* sr = prm.src + (size_t)k * 2 * nh;
+            srcA[0] = __ldg(sr + rA);
+            srcA[1] = __ldg(sr + nh + rA);
+            if (rB < nq) {
+                srcB[0] = __ldg(sr + rB);
+                srcB[1] = __ldg(sr + nh + rB);
+            }
+        }
         // ---- loop A: rows rA, rB x volume columns 0..24
 #pragma unroll 1
         for (int j0 = 0; j0 < 24; j0 += 4) {
@@ -566,16 +585,16 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         // ---- stacked = src - acc on volume rows, then T1 = Vq^T stacked
         {
             double* stk = work + W::wU;  // modal u is dead
-            const double* sr = prm.src + (size_t)k * 2 * nh;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int row = q == 0 ? rA : rB;
                 const Row6& r = q == 0 ? RA : RB;
+                const double* sq = q == 0 ? srcA : srcB;
                 if (row < nq) {
                     const double mgh = -g * nH[row];
                     stk[row] = -2.0 * r.a0;
-                    stk[nq + row] = valid ? mgh * sr[row] - r.a1 : 0.0;
-                    stk[2 * nq + row] = valid ? mgh * sr[nh + row] - r.a2 : 0.0;
+                    stk[nq + row] = valid ? mgh * sq[0] - r.a1 : 0.0;
+                    stk[2 * nq + row] = valid ? mgh * sq[1] - r.a2 : 0.0;
                 }
             }
         }

@@ -67,23 +67,32 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                      "n"(W::tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // (QA, QB) staged in shared memory (the work area is free until the element loop)
+    // with one coalesced pass of the whole CTA, instead of ~50 dependent L2/DRAM
+    // round trips per lane in the TMEM fill below
+    double* sQA = smem;
+    double* sQB = smem + nq * nq;
+    for (int x = threadIdx.x; x < nq * nq; x += W::T) {
+        sQA[x] = __ldg(prm.ops + O::QA + x);
+        sQB[x] = __ldg(prm.ops + O::QB + x);
+    }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tbase = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16);
     const int r0 = lp, r1 = lp + 16, rX = 32 + lp / 3, ph = lp % 3;
     const bool xrow = lp < 15;  // lanes 0..14 share rows 32..36, three lanes per row
-    if (warp < 4) {  // the operator rows depend only on l': one copy per TMEM lane quarter
-        const double* QA = prm.ops + O::QA;
-        const double* QB = prm.ops + O::QB;
-        for (int j = 0; j < nq; ++j) {
-            tmem_st4(tbase + W::t0 + 4 * j, QA[r0 + j * nq], QB[r0 + j * nq]);
-            tmem_st4(tbase + W::t1 + 4 * j, QA[r1 + j * nq], QB[r1 + j * nq]);
+    {  // the operator rows depend only on l': one copy per TMEM lane quarter, filled by
+       // the quarter's four warps (column phase warp >> 2)
+        const int cph = warp >> 2;
+        for (int j = cph; j < nq; j += 4) {
+            tmem_st4(tbase + W::t0 + 4 * j, sQA[r0 + j * nq], sQB[r0 + j * nq]);
+            tmem_st4(tbase + W::t1 + 4 * j, sQA[r1 + j * nq], sQB[r1 + j * nq]);
         }
-        for (int s = 0; s < 13; ++s) {
+        for (int s = cph; s < 13; s += 4) {
             const int j = ph + 3 * s;
             const bool ok = xrow && j < nq;
-            tmem_st4(tbase + W::tX + 4 * s, ok ? QA[rX + j * nq] : 0.0, ok ? QB[rX + j * nq] : 0.0);
+            tmem_st4(tbase + W::tX + 4 * s, ok ? sQA[rX + j * nq] : 0.0, ok ? sQB[rX + j * nq] : 0.0);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;");
     }
