@@ -37,7 +37,11 @@ struct SbpPairN4 {
     // staging per element: u [3][37] | gf columns 0..3, rows 0..36
     static constexpr int sU = 0, sG = 112;
     static constexpr int stage_stride = 260;
-    static constexpr int per_warp = 2 * work_stride + 2 * stage_stride;
+    // finish-phase inputs of a pair, copied as contiguous pair blocks (k0 even: 16 B
+    // aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15] |
+    // nbr int[2][3] | perm int[2][15] (8 B granules)
+    static constexpr int rRes = 0, rSrc = 222, rMinv = 370, rSurf = 444, rNbr = 534, rPerm = 537, rlen = 552;
+    static constexpr int per_warp = 2 * work_stride + 2 * stage_stride + rlen;
     static constexpr size_t bytes() { return sizeof(double) * (size_t)WARPS * per_warp + 16; }
 };
 
@@ -55,6 +59,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
     double* wbase = smem + warp * W::per_warp;
     double* work = wbase + half * W::work_stride;
     double* stage = wbase + 2 * W::work_stride;
+    double* rst = stage + 2 * W::stage_stride;  // finish-phase inputs of the current pair
     const double2* nA = reinterpret_cast<const double2*>(work + W::wA);
     const double2* nB = reinterpret_cast<const double2*>(work + W::wB);
     const double2* nC = reinterpret_cast<const double2*>(work + W::wC);
@@ -124,12 +129,54 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         }
         cp_async_commit();
     };
+    // second cp.async group: the pair's res/src/minv/surf, issued after the previous
+    // pair's finish phase, so its latency hides behind a whole flux loop
+    const bool with_res = prm.u_next != nullptr;
+    auto issue_r = [&](int pr) {
+        const int k0 = 2 * pr;
+        if (k0 + 1 < prm.K) {
+            constexpr int gR = 111, gS = 74, gM = 37, gF = 45;  // 16-byte granules per pair block
+            for (int x = lane; x < gR + gS + gM + gF; x += 32) {
+                const double* src;
+                int off;
+                if (x < gR) {
+                    if (!with_res) continue;
+                    src = prm.res + (size_t)k0 * 3 * nq + 2 * x, off = W::rRes + 2 * x;
+                } else if (x < gR + gS) {
+                    src = prm.src + (size_t)k0 * 2 * nq + 2 * (x - gR), off = W::rSrc + 2 * (x - gR);
+                } else if (x < gR + gS + gM) {
+                    src = prm.minv + (size_t)k0 * nq + 2 * (x - gR - gS), off = W::rMinv + 2 * (x - gR - gS);
+                } else {
+                    src = prm.surf + (size_t)k0 * 3 * nf + 2 * (x - gR - gS - gM), off = W::rSurf + 2 * (x - gR - gS - gM);
+                }
+                cp_async16(rst + off, src);
+            }
+            for (int x = lane; x < 18; x += 32) {  // nbr (3 granules) and perm (15 granules)
+                const int* src = x < 3 ? prm.nbr + (size_t)k0 * 3 + 2 * x : prm.perm + (size_t)k0 * nf + 2 * (x - 3);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(rst + W::rNbr + x)), "l"(src)
+                             : "memory");
+            }
+        } else if (k0 < prm.K) {  // odd K: last element alone
+            for (int x = lane; x < 3 * nq; x += 32)
+                if (with_res) rst[W::rRes + x] = prm.res[(size_t)k0 * 3 * nq + x];
+            for (int x = lane; x < 2 * nq; x += 32) rst[W::rSrc + x] = prm.src[(size_t)k0 * 2 * nq + x];
+            for (int x = lane; x < nq; x += 32) rst[W::rMinv + x] = prm.minv[(size_t)k0 * nq + x];
+            for (int x = lane; x < 3 * nf; x += 32) rst[W::rSurf + x] = prm.surf[(size_t)k0 * 3 * nf + x];
+            int* ri = reinterpret_cast<int*>(rst + W::rNbr);
+            for (int x = lane; x < 3; x += 32) ri[x] = prm.nbr[(size_t)k0 * 3 + x];
+            for (int x = lane; x < nf; x += 32) ri[6 + x] = prm.perm[(size_t)k0 * nf + x];
+        }
+        cp_async_commit();
+    };
 
-    if (gw < npairs) issue(gw);
+    if (gw < npairs) {
+        issue(gw);
+        issue_r(gw);
+    }
     for (int pr = gw; pr < npairs; pr += nw) {
         const int k = 2 * pr + half;
         const bool valid = k < prm.K;
-        cp_async_wait_all();
+        cp_async_wait_but1();  // the pair's u/gf group (its res group may still be in flight)
         __syncwarp();
         // ---- park: staging -> packed node arrays (+ velocities, positivity)
         {
@@ -147,28 +194,6 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         }
         __syncwarp();
         if (pr + nw < npairs) issue(pr + nw);
-        if (valid) {  // L2 prefetch of this pair's finish-phase inputs (consumed after the flux loops)
-            const char* line = nullptr;
-            const size_t ke = (size_t)k;
-            switch (lp) {  // 16 lanes per element, one 128-byte line each
-                case 0: case 1: case 2: case 3: case 4: case 5: case 6:
-                    line = (const char*)(prm.res + ke * 3 * nq) + 128 * lp; break;   // 888 B
-                case 7: case 8: case 9: case 10: case 11:
-                    line = (const char*)(prm.src + ke * 2 * nq) + 128 * (lp - 7); break;  // 592 B
-                case 12: case 13:
-                    line = (const char*)(prm.minv + ke * nq) + 128 * (lp - 12); break;  // 296 B
-                case 14: line = (const char*)(prm.surf + ke * 3 * nf); break;         // 360 B
-                default: line = (const char*)(prm.surf + ke * 3 * nf) + 128; break;
-            }
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
-            if (lp < 3) {
-                const char* l2 = lp == 0 ? (const char*)(prm.minv + ke * nq) + 256
-                               : lp == 1 ? (const char*)(prm.surf + ke * 3 * nf) + 256
-                                         : (const char*)(prm.perm + ke * nf);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(l2));
-            }
-        }
-
         auto load_row = [&](Row6& r, int row) {
             const double2 a = nA[row], c = nC[row], d = nD[row];
             r.U = a.x;
@@ -239,18 +264,19 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             double acc0 = 2.0 * R.a0, acc1 = R.a1, acc2 = R.a2;
             if (slot >= 0) {
                 const int f = slot / npf;
-                const double* sf = prm.surf + (size_t)k * 3 * nf + slot;
+                const double* sf = rst + W::rSurf + half * 3 * nf + slot;
                 const double m = sf[0], nxi = sf[nf], nyi = sf[2 * nf];
                 const double Bx = m * nxi, By = m * nyi;
                 double up[3];
-                const int nb = prm.nbr[(size_t)k * 3 + f];
+                const int* ri = reinterpret_cast<const int*>(rst + W::rNbr);  // nbr [2][3] | perm [2][15]
+                const int nb = ri[half * 3 + f];
                 if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
                     const double un = Ui * nxi + Vi * nyi;
                     up[0] = hi;
                     up[1] = Ui - 2.0 * un * nxi;
                     up[2] = Vi - 2.0 * un * nyi;
                 } else {
-                    const int jn = prm.fidx[prm.perm[(size_t)k * nf + slot]];
+                    const int jn = prm.fidx[ri[6 + half * nf + slot]];
                     const double* un = prm.u + (size_t)nb * 3 * nq + jn;
                     up[0] = un[0];
                     up[1] = un[nq];
@@ -276,9 +302,9 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                     acc2 = __fma_rn(-mhl, up[2] - Vi, acc2);
                 }
             }
-            const double* sr = prm.src + (size_t)k * 2 * nq;
+            const double* sr = rst + W::rSrc + half * 2 * nq;
             const double gh = g * hi;
-            const double mv = prm.minv[(size_t)k * nq + row];
+            const double mv = rst[W::rMinv + half * nq + row];
             const double d0 = mv * -acc0;
             const double d1 = mv * (-acc1 - gh * sr[row]);
             const double d2 = mv * (-acc2 - gh * sr[nq + row]);
@@ -288,7 +314,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 const double uo[3] = {hi, Ui, Vi}, dd[3] = {d0, d1, d2};
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const double r = __fma_rn(prm.rk_a, prm.res[o + c * nq], prm.dt * dd[c]);
+                    const double r = __fma_rn(prm.rk_a, rst[W::rRes + half * 3 * nq + c * nq + row], prm.dt * dd[c]);
                     prm.res[o + c * nq] = r;
                     prm.u_next[o + c * nq] = __fma_rn(prm.rk_b, r, uo[c]);
                 }
@@ -299,12 +325,18 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 out[2 * nq] = d2;
             }
         };
+        if (pr + nw < npairs)
+            cp_async_wait_but1();  // this pair's res/src/minv/surf group (the next u/gf group may pend)
+        else
+            cp_async_wait_all();
+        __syncwarp();
         if (valid) {
             finish(R0, r0, slot0);
             finish(R1, r1, slot1);
             if (xrow && ph == 0) finish(RX, rX, slotX);
         }
         __syncwarp();
+        if (pr + nw < npairs) issue_r(pr + nw);
     }
     cp_async_wait_all();
 
