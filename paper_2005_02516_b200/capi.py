@@ -85,9 +85,11 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if _build.needs_build():
-        _build.build()
+    path = os.environ.get("SWEDG_LIB_VARIANT")  # profiling tools: an alternative in-tree build
+    if not path:
+        path = _build.LIB
+        if _build.needs_build():
+            _build.build()
     if not os.path.exists(path):
         raise RuntimeError(f"CUDA extension missing: {path} (run __graft_entry__.build())")
     L = C.CDLL(path)
