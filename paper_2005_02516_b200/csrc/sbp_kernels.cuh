@@ -279,6 +279,7 @@ struct SbpUpdateParams {
 template <bool P>
 __global__ void sbp_update_kernel(SbpUpdateParams prm) {
     using A = Ar<P>;
+    asm volatile("griddepcontrol.launch_dependents;");  // the next (PDL) RHS launch may stage its operators
     if (prm.early_exit && error_pending(prm.err)) return;
     for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < prm.n; x += (size_t)gridDim.x * blockDim.x) {
         const double r = A::fma(prm.a, prm.res[x], A::mul(prm.dt, prm.du[x]));

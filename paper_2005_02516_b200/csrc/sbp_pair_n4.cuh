@@ -34,43 +34,81 @@ struct SbpPairN4 {
     // per-element work block (doubles): double2 (hu,hv) (u,v) (g1,g2) (g3,g4) | h
     static constexpr int wA = 0, wB = 74, wC = 148, wD = 222, wH = 296;
     static constexpr int work_stride = 338;  // == 2 (mod 16)
-    // staging per element: u [3][37] | gf columns 0..3, rows 0..36
-    static constexpr int sU = 0, sG = 112;
-    static constexpr int stage_stride = 260;
-    // finish-phase inputs of a pair, copied as contiguous pair blocks (k0 even: 16 B
-    // aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15] |
-    // nbr int[2][3] | perm int[2][15] (8 B granules)
+    // pair staging, filled by bulk (TMA) copies: u [2][3][37] | gf [2][4][38] (volume
+    // rows 0..36 of each gf column plus one pad row, so every copy is a 16 B multiple)
+    static constexpr int sU = 0, sG = 222, gseg = 38, slen = 526;
+    // finish-phase inputs of a pair, bulk-copied as contiguous pair blocks (k0 even:
+    // 16 B aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15];
+    // nbr int[2][3] | perm int[2][15] by cp.async (8 B granules)
     static constexpr int rRes = 0, rSrc = 222, rMinv = 370, rSurf = 444, rNbr = 534, rPerm = 537, rlen = 552;
-    static constexpr int per_warp = 2 * work_stride + 2 * stage_stride + rlen;
+    static constexpr int per_warp = 2 * work_stride + slen + rlen;
     static constexpr size_t bytes() { return sizeof(double) * (size_t)WARPS * per_warp + 16; }
+    // bytes per pair of each bulk group
+    static constexpr uint32_t g1_bytes = 8u * (222 + 8 * gseg);
+    static constexpr uint32_t g2_bytes_nores = 8u * (148 + 74 + 90), g2_res = 8u * 222;
 };
+
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr_u32(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_addr_u32(mb)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (TMA engine, no tensor map): bytes and both addresses 16 B multiples
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr_u32(mb))
+                 : "memory");
+}
 
 __global__ void __launch_bounds__(SbpPairN4::T, 1)
 sbp_rhs_pair_n4_kernel(SbpParams prm) {
     using W = SbpPairN4;
     using O = SbpOps<4>;
     constexpr int nq = W::nq, nf = W::nf, npf = W::npf, nrow = W::nrow;
-    if (prm.early_exit && error_pending(prm.err)) return;
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ __align__(8) uint64_t mbar[W::WARPS][2];  // per warp: staging group, finish group
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int half = lane >> 4, lp = lane & 15;
     double* wbase = smem + warp * W::per_warp;
     double* work = wbase + half * W::work_stride;
     double* stage = wbase + 2 * W::work_stride;
-    double* rst = stage + 2 * W::stage_stride;  // finish-phase inputs of the current pair
+    double* rst = stage + W::slen;  // finish-phase inputs of the current pair
     const double2* nA = reinterpret_cast<const double2*>(work + W::wA);
     const double2* nB = reinterpret_cast<const double2*>(work + W::wB);
     const double2* nC = reinterpret_cast<const double2*>(work + W::wC);
     const double2* nD = reinterpret_cast<const double2*>(work + W::wD);
     const double* nH = work + W::wH;
+    uint64_t* mb1 = &mbar[warp][0];
+    uint64_t* mb2 = &mbar[warp][1];
 
+    // ---- setup that reads only launch-invariant data (operators): under programmatic
+    //      dependent launch it overlaps the previous kernel's tail
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_addr_u32(&tmem_base_sh)),
                      "n"(W::tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (lane == 0) {
+        mbar_init(mb1, 1);
+        mbar_init(mb2, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // (QA, QB) staged in shared memory (the work area is free until the element loop)
     // with one coalesced pass of the whole CTA, instead of ~50 dependent L2/DRAM
@@ -111,49 +149,56 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
     const int npairs = (prm.K + 1) / 2;
     const int gw = blockIdx.x * W::WARPS + warp, nw = gridDim.x * W::WARPS;
 
+    // everything below reads the previous kernel's outputs (state, LSRK register); the
+    // next stage's launch may begin its own setup as soon as every CTA got here
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (prm.early_exit && error_pending(prm.err)) {
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(W::tcols));
+        return;
+    }
+
+    // staging group: u and gf volume rows of the pair (one bulk copy per block, lane 0)
     auto issue = [&](int pr) {
         const int k0 = 2 * pr;
-        const int ne = k0 + 1 < prm.K ? 2 : 1;
-        const double* gu = prm.u + (size_t)k0 * 3 * nq;
-        for (int x = lane; x < ne * 3 * nq; x += 32) {
-            const int e = x / (3 * nq), r = x - e * 3 * nq;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sU + r)),
-                         "l"(gu + x)
-                         : "memory");
+        if (k0 + 1 < prm.K) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(mb1, W::g1_bytes);
+                bulk_g2s(stage + W::sU, prm.u + (size_t)k0 * 3 * nq, 8u * 222, mb1);
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    bulk_g2s(stage + W::sG + s * W::gseg, prm.gf + ((size_t)k0 * 4 + s) * nrow, 8u * W::gseg, mb1);
+            }
+        } else {  // odd K: last element alone, plain loads
+            for (int x = lane; x < 3 * nq; x += 32) stage[W::sU + x] = prm.u[(size_t)k0 * 3 * nq + x];
+            for (int x = lane; x < 4 * nq; x += 32) {
+                const int c = x / nq, i = x - c * nq;
+                stage[W::sG + c * W::gseg + i] = prm.gf[((size_t)k0 * 4 + c) * nrow + i];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(mb1);
         }
-        for (int x = lane; x < ne * 4 * nq; x += 32) {
-            const int e = x / (4 * nq), r = x - e * 4 * nq, c = r / nq, i = r - c * nq;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sG + r)),
-                         "l"(prm.gf + (size_t)(k0 + e) * 4 * nrow + c * nrow + i)
-                         : "memory");
-        }
-        cp_async_commit();
     };
-    // second cp.async group: the pair's res/src/minv/surf, issued after the previous
-    // pair's finish phase, so its latency hides behind a whole flux loop
+    // finish group: res/src/minv/surf pair blocks (bulk) and nbr/perm (cp.async)
     const bool with_res = prm.u_next != nullptr;
     auto issue_r = [&](int pr) {
         const int k0 = 2 * pr;
         if (k0 + 1 < prm.K) {
-            constexpr int gR = 111, gS = 74, gM = 37, gF = 45;  // 16-byte granules per pair block
-            for (int x = lane; x < gR + gS + gM + gF; x += 32) {
-                const double* src;
-                int off;
-                if (x < gR) {
-                    if (!with_res) continue;
-                    src = prm.res + (size_t)k0 * 3 * nq + 2 * x, off = W::rRes + 2 * x;
-                } else if (x < gR + gS) {
-                    src = prm.src + (size_t)k0 * 2 * nq + 2 * (x - gR), off = W::rSrc + 2 * (x - gR);
-                } else if (x < gR + gS + gM) {
-                    src = prm.minv + (size_t)k0 * nq + 2 * (x - gR - gS), off = W::rMinv + 2 * (x - gR - gS);
-                } else {
-                    src = prm.surf + (size_t)k0 * 3 * nf + 2 * (x - gR - gS - gM), off = W::rSurf + 2 * (x - gR - gS - gM);
-                }
-                cp_async16(rst + off, src);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(mb2, W::g2_bytes_nores + (with_res ? W::g2_res : 0u));
+                if (with_res) bulk_g2s(rst + W::rRes, prm.res + (size_t)k0 * 3 * nq, W::g2_res, mb2);
+                bulk_g2s(rst + W::rSrc, prm.src + (size_t)k0 * 2 * nq, 8u * 148, mb2);
+                bulk_g2s(rst + W::rMinv, prm.minv + (size_t)k0 * nq, 8u * 74, mb2);
+                bulk_g2s(rst + W::rSurf, prm.surf + (size_t)k0 * 3 * nf, 8u * 90, mb2);
             }
-            for (int x = lane; x < 18; x += 32) {  // nbr (3 granules) and perm (15 granules)
-                const int* src = x < 3 ? prm.nbr + (size_t)k0 * 3 + 2 * x : prm.perm + (size_t)k0 * nf + 2 * (x - 3);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(rst + W::rNbr + x)), "l"(src)
+            if (lane < 18) {  // nbr (3 granules) and perm (15 granules)
+                const int* src = lane < 3 ? prm.nbr + (size_t)k0 * 3 + 2 * lane : prm.perm + (size_t)k0 * nf + 2 * (lane - 3);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(rst + W::rNbr + lane)), "l"(src)
                              : "memory");
             }
         } else if (k0 < prm.K) {  // odd K: last element alone
@@ -165,6 +210,8 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             int* ri = reinterpret_cast<int*>(rst + W::rNbr);
             for (int x = lane; x < 3; x += 32) ri[x] = prm.nbr[(size_t)k0 * 3 + x];
             for (int x = lane; x < nf; x += 32) ri[6 + x] = prm.perm[(size_t)k0 * nf + x];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(mb2);
         }
         cp_async_commit();
     };
@@ -173,22 +220,23 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         issue(gw);
         issue_r(gw);
     }
-    for (int pr = gw; pr < npairs; pr += nw) {
+    uint32_t phase = 0;
+    for (int pr = gw; pr < npairs; pr += nw, phase ^= 1) {
         const int k = 2 * pr + half;
         const bool valid = k < prm.K;
-        cp_async_wait_but1();  // the pair's u/gf group (its res group may still be in flight)
-        __syncwarp();
+        mbar_wait(mb1, phase);  // the pair's u/gf
         // ---- park: staging -> packed node arrays (+ velocities, positivity)
         {
-            const double* st = stage + half * W::stage_stride;
+            const double* su = stage + W::sU + half * 3 * nq;
+            const double* sg = stage + W::sG + half * 4 * W::gseg;
             for (int j = lp; j < nq; j += 16) {
-                const double h = st[W::sU + j], hu = st[W::sU + nq + j], hv = st[W::sU + 2 * nq + j];
+                const double h = su[j], hu = su[nq + j], hv = su[2 * nq + j];
                 if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);  // check_positive (:381)
                 const double ih = 1.0 / h;
                 reinterpret_cast<double2*>(work + W::wA)[j] = make_double2(hu, hv);
                 reinterpret_cast<double2*>(work + W::wB)[j] = make_double2(hu * ih, hv * ih);
-                reinterpret_cast<double2*>(work + W::wC)[j] = make_double2(st[W::sG + j], st[W::sG + nq + j]);
-                reinterpret_cast<double2*>(work + W::wD)[j] = make_double2(st[W::sG + 2 * nq + j], st[W::sG + 3 * nq + j]);
+                reinterpret_cast<double2*>(work + W::wC)[j] = make_double2(sg[j], sg[W::gseg + j]);
+                reinterpret_cast<double2*>(work + W::wD)[j] = make_double2(sg[2 * W::gseg + j], sg[3 * W::gseg + j]);
                 work[W::wH + j] = h;
             }
         }
@@ -228,6 +276,35 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             pair6(R0, qa, A, B, C.x, C.y, D.x, D.y, nH[36]);
             pair6(R1, qb, A, B, C.x, C.y, D.x, D.y, nH[36]);
         }
+        // ---- the pair's finish-phase inputs (issued one flux loop ago) and, for the
+        //      owned surface rows, the neighbour traces: issued now, consumed after the
+        //      row 32..36 loop
+        mbar_wait(mb2, phase);
+        cp_async_wait_all();
+        __syncwarp();
+        const int* ri = reinterpret_cast<const int*>(rst + W::rNbr);  // nbr [2][3] | perm [2][15]
+        double nb3[3][3];
+        {
+            const int slots[3] = {slot0, slot1, (xrow && ph == 0) ? slotX : -1};
+            const double hs[3] = {nH[r0], nH[r1], nH[xrow ? rX : 32]};
+            const double2 As[3] = {nA[r0], nA[r1], nA[xrow ? rX : 32]};
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                nb3[q][0] = hs[q];
+                nb3[q][1] = As[q].x;
+                nb3[q][2] = As[q].y;
+                const int slot = slots[q];
+                if (valid && slot >= 0) {
+                    const int nb = ri[half * 3 + slot / npf];
+                    if (nb >= 0) {
+                        const double* un = prm.u + (size_t)nb * 3 * nq + prm.fidx[ri[6 + half * nf + slot]];
+                        nb3[q][0] = un[0];
+                        nb3[q][1] = un[nq];
+                        nb3[q][2] = un[2 * nq];
+                    }
+                }
+            }
+        }
         // ---- rows 32..36: columns ph, ph+3, ... (13 slots), three lanes per row
 #pragma unroll
         for (int s0 = 0; s0 < 16; s0 += 4) {
@@ -256,7 +333,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             }
         }
         // ---- per row: row constants, surface term, source, inverse mass (solver.hpp:395-428)
-        auto finish = [&](Row6& R, const int row, const int slot) {
+        auto finish = [&](Row6& R, const int row, const int slot, const double (&nbv)[3]) {
             const double hi = nH[row];
             const double2 uv = nB[row];
             const double Ui = R.U, Vi = R.V, ui = uv.x, vi = uv.y;
@@ -268,19 +345,15 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 const double m = sf[0], nxi = sf[nf], nyi = sf[2 * nf];
                 const double Bx = m * nxi, By = m * nyi;
                 double up[3];
-                const int* ri = reinterpret_cast<const int*>(rst + W::rNbr);  // nbr [2][3] | perm [2][15]
-                const int nb = ri[half * 3 + f];
-                if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
+                if (ri[half * 3 + f] < 0) {  // wall_ghost (swe.hpp:102-105)
                     const double un = Ui * nxi + Vi * nyi;
                     up[0] = hi;
                     up[1] = Ui - 2.0 * un * nxi;
                     up[2] = Vi - 2.0 * un * nyi;
                 } else {
-                    const int jn = prm.fidx[ri[6 + half * nf + slot]];
-                    const double* un = prm.u + (size_t)nb * 3 * nq + jn;
-                    up[0] = un[0];
-                    up[1] = un[nq];
-                    up[2] = un[2 * nq];
+                    up[0] = nbv[0];
+                    up[1] = nbv[1];
+                    up[2] = nbv[2];
                 }
                 const double ip = 1.0 / up[0];
                 const double uxa = up[1] * ip, uya = up[2] * ip;
@@ -325,15 +398,10 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 out[2 * nq] = d2;
             }
         };
-        if (pr + nw < npairs)
-            cp_async_wait_but1();  // this pair's res/src/minv/surf group (the next u/gf group may pend)
-        else
-            cp_async_wait_all();
-        __syncwarp();
         if (valid) {
-            finish(R0, r0, slot0);
-            finish(R1, r1, slot1);
-            if (xrow && ph == 0) finish(RX, rX, slotX);
+            finish(R0, r0, slot0, nb3[0]);
+            finish(R1, r1, slot1, nb3[1]);
+            if (xrow && ph == 0) finish(RX, rX, slotX, nb3[2]);
         }
         __syncwarp();
         if (pr + nw < npairs) issue_r(pr + nw);

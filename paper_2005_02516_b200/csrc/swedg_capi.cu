@@ -52,6 +52,7 @@ struct swedg_handle_s {
     // TMEM operators), 1 = "tworow", 2 = "row", 3 = "warp" (N=4, warp/element, TMEM),
     // 4 = "quad" (N=4, 4 elements/warp; measured slower: latency-bound at 6 warps/SM)
     int vol_variant = 0;
+    bool pdl = true;  // programmatic dependent launch of the SBP pair kernel (SWEDG_PDL=0: off)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // device buffers
@@ -253,6 +254,13 @@ void launch_pair(swedg_handle h, const PairStageParams& ps) {
     kern<<<std::max(grid, 1), PairN4::T, psm, h->stream>>>(ps);
 }
 
+// the SBP pair kernel bulk-copies (TMA) per-pair blocks: every source must be 16 B aligned
+// (true for the handle's own buffers; a caller's rhs_device pointer may not be)
+inline bool sbp_pair_aligned(const SbpParams& sp) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    return al(sp.u) && al(sp.gf) && al(sp.src) && al(sp.minv) && al(sp.surf) && (!sp.u_next || al(sp.res));
+}
+
 struct StageArgs {
     const double* u_in;
     int parts = 3;  // bit 0: volume kernel, bit 1: surface/update kernel
@@ -419,12 +427,25 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             go(sbp_rhs_kernel<N, true>);
-        } else if (N == 4 && h->vol_variant == 0) {  // pair kernel, operators in TMEM
+        } else if (N == 4 && h->vol_variant == 0 && sbp_pair_aligned(sp)) {  // pair kernel, operators in TMEM
             auto kern = sbp_rhs_pair_n4_kernel;
             const size_t psm = SbpPairN4::bytes();
             const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, SbpPairN4::T, psm);
             const int blocks = (h->K + 2 * SbpPairN4::WARPS - 1) / (2 * SbpPairN4::WARPS);
-            kern<<<std::max(1, std::min(blocks, occ * h->nsm)), SbpPairN4::T, psm, h->stream>>>(sp);
+            // programmatic dependent launch: the CTAs' operator staging and TMEM fill
+            // overlap the previous kernel's tail (the kernel waits on griddepcontrol
+            // before touching the state)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(std::max(1, std::min(blocks, occ * h->nsm)));
+            cfg.blockDim = dim3(SbpPairN4::T);
+            cfg.dynamicSmemBytes = psm;
+            cfg.stream = h->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, kern, sp);
         } else {
             go(sbp_rhs_kernel<N, false>);
         }
@@ -828,6 +849,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->g = d->g;
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_FUSION")) h->fusion = std::string(v) == "1";
+    if (const char* v = std::getenv("SWEDG_PDL")) h->pdl = std::string(v) != "0";
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
         h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : (sv == "quad" ? 4 : 0)));
