@@ -23,6 +23,33 @@
 
 namespace swedg {
 
+// mbarrier + bulk (TMA engine, no tensor map) copy helpers
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr_u32(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_addr_u32(mb)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (TMA engine, no tensor map): bytes and both addresses 16 B multiples
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr_u32(mb))
+                 : "memory");
+}
+
 // One stacked row's state in the flux loops.  The EC-flux accumulation is
 // factored so a pair costs 17 FP64 instructions instead of 23: with
 // T = qx sU + qy sV (the mass-flux term, sU = hu_i + hu_j, sV = hv_i + hv_j),
@@ -96,8 +123,9 @@ struct PairN4 {
     static constexpr int wV = 448;   // 75 entropy variables
     static constexpr int wVh = 524;  // 45 projected variables
     static constexpr int work_stride = 578;   // == 2 (mod 16)
-    static constexpr int stage_stride = 246;  // staging per element: u[45](+1) | gf[160] | b[40]
-    static constexpr int sU = 0, sG = 46, sB = 206;
+    static constexpr int stage_stride = 246;  // staging: 2 x 246 doubles per warp
+    // the pair's raw blocks as bulk (TMA) copies land them: u [2][45] | gf [2][160] | b [2][40]
+    static constexpr int sU = 0, sG = 90, sB = 410;
     static constexpr int per_warp = 2 * work_stride + 2 * stage_stride;
     static constexpr int ops_len = 376 + 226; // Vq (25 x 15) for the volume lift, Vf (15 x 15) for the surface lift
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
@@ -116,6 +144,7 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ __align__(8) uint64_t mbar[W::WARPS];  // per warp: the pair's staging copies
     double* sVq = smem;         // 25 x 15
     double* sVf = smem + 376;   // 15 x 15
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -148,6 +177,11 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
                          smem_addr_u32(&tmem_base_sh)),
                      "n"(W::tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    uint64_t* mb = &mbar[warp];
+    if (lane == 0) {
+        mbar_init(mb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -185,56 +219,50 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     const bool do_surface = S && ps.do_surface;
     const bool do_volume = !S || ps.do_volume;
     const bool with_u = !do_surface;  // otherwise u comes from the interface phase
+    const bool bulk_ok = ((reinterpret_cast<uintptr_t>(prm.gf) | reinterpret_cast<uintptr_t>(prm.bs) |
+                           (with_u ? reinterpret_cast<uintptr_t>(prm.u) : 0)) & 15u) == 0;
+    // the pair's u/gf/b: three bulk (TMA) copies of contiguous pair blocks by lane 0
+    // (k0 even: every block is 16 B aligned), completion on the warp's mbarrier
     auto issue = [&](int pr) {
         const int k0 = 2 * pr;
-        if (!do_volume) {
-        } else if (k0 + 1 < prm.K) {
-            // u: 2 x 45 doubles (8 B granules: element blocks are 246 apart)
-            const double* gu = prm.u + (size_t)k0 * 3 * Np;
-            for (int x = lane; with_u && x < 90; x += 32) {
-                const int e = x / 45, r = x - e * 45;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(stage + e * W::stage_stride + W::sU + r)),
-                             "l"(gu + x)
-                             : "memory");
+        if (k0 + 1 < prm.K && bulk_ok) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(mb, 8u * ((with_u ? 90 : 0) + 320 + 80));
+                if (with_u) bulk_g2s(stage + W::sU, prm.u + (size_t)k0 * 3 * Np, 8u * 90, mb);
+                bulk_g2s(stage + W::sG, prm.gf + (size_t)k0 * 4 * nh, 8u * 320, mb);
+                bulk_g2s(stage + W::sB, prm.bs + (size_t)k0 * nh, 8u * 80, mb);
             }
-            // gf: 2 x 160 doubles; b: 2 x 40 doubles — element k0 even, so 16 B aligned
-            const double* gg = prm.gf + (size_t)k0 * 4 * nh;
-            for (int x = lane; x < 160; x += 32) {
-                const int e = (2 * x) / 160, r = 2 * x - e * 160;
-                cp_async16(stage + e * W::stage_stride + W::sG + r, gg + 2 * x);
-            }
-            const double* gb = prm.bs + (size_t)k0 * nh;
-            for (int x = lane; x < 40; x += 32) {
-                const int e = (2 * x) / 40, r = 2 * x - e * 40;
-                cp_async16(stage + e * W::stage_stride + W::sB + r, gb + 2 * x);
-            }
-        } else if (k0 < prm.K) {  // odd K: last element alone
-            for (int r = lane; with_u && r < 45; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
-            for (int r = lane; r < 160; r += 32) stage[W::sG + r] = prm.gf[(size_t)k0 * 160 + r];
-            for (int r = lane; r < 40; r += 32) stage[W::sB + r] = prm.bs[(size_t)k0 * 40 + r];
+        } else if (k0 < prm.K) {  // odd K (last element alone) or unaligned base pointers: plain loads
+            const int ne = k0 + 1 < prm.K ? 2 : 1;
+            for (int r = lane; with_u && r < 45 * ne; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
+            for (int r = lane; r < 160 * ne; r += 32) stage[W::sG + r] = prm.gf[(size_t)k0 * 160 + r];
+            for (int r = lane; r < 40 * ne; r += 32) stage[W::sB + r] = prm.bs[(size_t)k0 * 40 + r];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(mb);
         }
-        cp_async_commit();
     };
 
-    if (gw < npairs) issue(gw);
-    for (int pr = gw; pr < npairs; pr += nw) {
+    if (gw < npairs && do_volume) issue(gw);
+    uint32_t phase = 0;
+    for (int pr = gw; pr < npairs; pr += nw, phase ^= 1) {
         const int k = 2 * pr + half;
         const bool valid = k < prm.K;
-        cp_async_wait_all();
-        __syncwarp();
         // ---- park: staging -> work (u, b, g pairs), freeing the staging for the next pair
         if (do_volume) {
-            const double* st = stage + half * W::stage_stride;
-            for (int r = lp; with_u && r < 45; r += 16) work[W::wU + r] = st[W::sU + r];
+            mbar_wait(mb, phase);
+            const double* su = stage + W::sU + 45 * half;
+            const double* sg = stage + W::sG + 160 * half;
+            const double* sb = stage + W::sB + 40 * half;
+            for (int r = lp; with_u && r < 45; r += 16) work[W::wU + r] = su[r];
             for (int r = lp; r < 40; r += 16) {
-                work[W::wBs + r] = st[W::sB + r];
-                reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(st[W::sG + r], st[W::sG + nh + r]);
-                reinterpret_cast<double2*>(work + W::wD)[r] =
-                    make_double2(st[W::sG + 2 * nh + r], st[W::sG + 3 * nh + r]);
+                work[W::wBs + r] = sb[r];
+                reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(sg[r], sg[nh + r]);
+                reinterpret_cast<double2*>(work + W::wD)[r] = make_double2(sg[2 * nh + r], sg[3 * nh + r]);
             }
         }
         __syncwarp();
-        if (pr + nw < npairs) issue(pr + nw);
+        if (pr + nw < npairs && do_volume) issue(pr + nw);
         if (valid && lp < 5)  // L2 prefetch of this element's source rows (read after the flux loops)
             asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(prm.src + (size_t)k * 2 * nh) + 128 * lp));
 
@@ -628,7 +656,6 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         }
         __syncwarp();
     }
-    cp_async_wait_all();
 
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();

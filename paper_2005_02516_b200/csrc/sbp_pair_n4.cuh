@@ -48,32 +48,6 @@ struct SbpPairN4 {
     static constexpr uint32_t g2_bytes_nores = 8u * (148 + 74 + 90), g2_res = 8u * 222;
 };
 
-__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr_u32(mb)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_addr_u32(mb)),
-        "r"(parity)
-        : "memory");
-}
-// global -> shared bulk copy (TMA engine, no tensor map): bytes and both addresses 16 B multiples
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr_u32(mb))
-                 : "memory");
-}
-
 __global__ void __launch_bounds__(SbpPairN4::T, 1)
 sbp_rhs_pair_n4_kernel(SbpParams prm) {
     using W = SbpPairN4;
