@@ -519,8 +519,8 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
                 tmem_ld16(tbase + W::tC + 4 * s0, qc);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const int j = par + 2 * (s0 + t);
-                    if (s0 + t < 13 && j < nq) {
+                    if (s0 + t < 13) {  // branch-free over lanes: slot 12 of parity 1 (j = 25) holds a zero operator
+                        const int j = min(par + 2 * (s0 + t), nq - 1);
                         const double2 C = nC[j], D = nD[j];
                         pair6(RC, qc[t], nA[j], nB[j], C.x, C.y, D.x, D.y, nH[j]);
                     }

@@ -29,7 +29,7 @@ struct SbpParams {
     const double* ops;
     const int* fidx;     // [nf] surface slot -> volume node
     const double* u;     // [K][3][nq]
-    const double* gf;    // [K][4][nq+nf]
+    const double* gf;    // [K][4][sbp_gstride(nq)]
     const double* surf;  // [K][3][nf]: w*sJ, nx, ny
     const double* src;   // [K][2][nq]
     const double* minv;  // [K][nq]
@@ -71,7 +71,7 @@ sbp_rhs_kernel(SbpParams prm) {
     using A = Ar<P>;
     using O = SbpOps<N>;
     using S = SbpSmem<N>;
-    constexpr int nq = SbpDims<N>::nq, npf = N + 1, nf = 3 * npf, nrow = nq + nf;
+    constexpr int nq = SbpDims<N>::nq, npf = N + 1, nf = 3 * npf, nrow = sbp_gstride(nq);
     constexpr int E = SbpCfg<N>::E, T = SbpCfg<N>::T;
     if (prm.early_exit && error_pending(prm.err)) return;
     extern __shared__ double smem[];
@@ -293,7 +293,7 @@ struct SbpBathyParams {
     int K;
     const double* ops;
     const double* b;   // [K][nq]
-    const double* gf;  // [K][4][nq+nf]
+    const double* gf;  // [K][4][sbp_gstride(nq)]
     double* src;       // [K][2][nq]
 };
 
@@ -301,7 +301,7 @@ template <int N>
 __global__ void sbp_bathymetry_kernel(SbpBathyParams prm) {
     using A = Ar<true>;
     using O = SbpOps<N>;
-    constexpr int nq = SbpDims<N>::nq, nrow = nq + 3 * (N + 1);
+    constexpr int nq = SbpDims<N>::nq, nrow = sbp_gstride(nq);
     const int k = blockIdx.x, i = threadIdx.x;
     if (k >= prm.K || i >= nq) return;
     const double* gf = prm.gf + (size_t)k * 4 * nrow;

@@ -34,9 +34,9 @@ struct SbpPairN4 {
     // per-element work block (doubles): double2 (hu,hv) (u,v) (g1,g2) (g3,g4) | h
     static constexpr int wA = 0, wB = 74, wC = 148, wD = 222, wH = 296;
     static constexpr int work_stride = 338;  // == 2 (mod 16)
-    // pair staging, filled by bulk (TMA) copies: u [2][3][37] | gf [2][4][38] (volume
-    // rows 0..36 of each gf column plus one pad row, so every copy is a 16 B multiple)
-    static constexpr int sU = 0, sG = 222, gseg = 38, slen = 526;
+    // pair staging, filled by two bulk (TMA) copies: u [2][3][37] | gf [2][4][38] (the
+    // device gf layout of SBP: volume rows of each column padded to sbp_gstride(37) = 38)
+    static constexpr int sU = 0, sG = 222, gseg = sbp_gstride(37), slen = 526;
     // finish-phase inputs of a pair, bulk-copied as contiguous pair blocks (k0 even:
     // 16 B aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15];
     // nbr int[2][3] | perm int[2][15] by cp.async (8 B granules)
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(SbpPairN4::T, 1)
 sbp_rhs_pair_n4_kernel(SbpParams prm) {
     using W = SbpPairN4;
     using O = SbpOps<4>;
-    constexpr int nq = W::nq, nf = W::nf, npf = W::npf, nrow = W::nrow;
+    constexpr int nq = W::nq, nf = W::nf, npf = W::npf;
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
@@ -143,15 +143,13 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive_tx(mb1, W::g1_bytes);
                 bulk_g2s(stage + W::sU, prm.u + (size_t)k0 * 3 * nq, 8u * 222, mb1);
-#pragma unroll
-                for (int s = 0; s < 8; ++s)
-                    bulk_g2s(stage + W::sG + s * W::gseg, prm.gf + ((size_t)k0 * 4 + s) * nrow, 8u * W::gseg, mb1);
+                bulk_g2s(stage + W::sG, prm.gf + (size_t)k0 * 4 * W::gseg, 8u * 8 * W::gseg, mb1);
             }
         } else {  // odd K: last element alone, plain loads
             for (int x = lane; x < 3 * nq; x += 32) stage[W::sU + x] = prm.u[(size_t)k0 * 3 * nq + x];
             for (int x = lane; x < 4 * nq; x += 32) {
                 const int c = x / nq, i = x - c * nq;
-                stage[W::sG + c * W::gseg + i] = prm.gf[((size_t)k0 * 4 + c) * nrow + i];
+                stage[W::sG + c * W::gseg + i] = prm.gf[((size_t)k0 * 4 + c) * W::gseg + i];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(mb1);

@@ -921,7 +921,16 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
             surf[(k * 3 + 1) * nf + i] = d->nx[k * nf + i];
             surf[(k * 3 + 2) * nf + i] = d->ny[k * nf + i];
         }
-    if (dalloc(h, &h->gf, K * 4 * nrow) || upload(h, h->gf, d->gf, K * 4 * nrow)) return bail(h->last_code);
+    if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
+        if (dalloc(h, &h->gf, K * 4 * nrow) || upload(h, h->gf, d->gf, K * 4 * nrow)) return bail(h->last_code);
+    } else {  // SBP: volume rows only, columns padded to sbp_gstride(nq)
+        const int gs = sbp_gstride(nq);
+        std::vector<double> g(K * 4 * gs, 0.0);
+        for (size_t k = 0; k < K; ++k)
+            for (int c = 0; c < 4; ++c)
+                std::copy(d->gf + (k * 4 + c) * nrow, d->gf + (k * 4 + c) * nrow + nq, g.begin() + (k * 4 + c) * gs);
+        if (dalloc(h, &h->gf, g.size()) || upload(h, h->gf, g.data(), g.size())) return bail(h->last_code);
+    }
     if (dalloc(h, &h->surf, surf.size()) || upload(h, h->surf, surf.data(), surf.size())) return bail(h->last_code);
     if (dalloc(h, &h->nbr, K * 3) || upload(h, h->nbr, d->nbr, K * 3)) return bail(h->last_code);
     {

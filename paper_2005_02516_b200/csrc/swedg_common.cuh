@@ -91,5 +91,9 @@ template <> struct SbpDims<1> { static constexpr int nq = 6; };
 template <> struct SbpDims<2> { static constexpr int nq = 12; };
 template <> struct SbpDims<3> { static constexpr int nq = 21; };
 template <> struct SbpDims<4> { static constexpr int nq = 37; };
+// device layout of the SBP geometric factors: [K][4][sbp_gstride(nq)], the volume nodes of
+// each gf column padded to an even length (the SBP kernels never read the surface rows), so a
+// pair of elements is one 16 B-aligned block for bulk copies
+__host__ __device__ constexpr int sbp_gstride(int nq) { return (nq + 1) & ~1; }
 
 }  // namespace swedg
