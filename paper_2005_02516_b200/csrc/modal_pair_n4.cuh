@@ -105,9 +105,13 @@ struct PairStageParams {
     unsigned stage_prev;       // stage id of s-1 (non-finite RHS reports)
 };
 
+#ifndef SWEDG_PAIR_WARPS
+#define SWEDG_PAIR_WARPS 16  // warps per CTA (one CTA per SM): 512 threads cap registers at 128
+#endif
+
 struct PairN4 {
     static constexpr int Np = 15, nq = 25, nf = 15, nh = 40;
-    static constexpr int WARPS = 16, T = WARPS * 32;
+    static constexpr int WARPS = SWEDG_PAIR_WARPS, T = WARPS * 32;  // a multiple of 4 (TMEM lane quarters)
     // TMEM columns (32-bit); every (QA,QB) pair = 4 columns, a double = 2 columns
     static constexpr int tA = 0;     // Q row l'      : 40 columns j
     static constexpr int tB = 160;   // Q row l'+16   : 40 columns j
@@ -191,21 +195,21 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     {  // rows depend only on l': one copy per TMEM lane quarter, filled by the
        // quarter's four warps (column phase cph = warp >> 2)
         const int cph = warp >> 2;
-        for (int j = cph; j < nh; j += 4) {
+        for (int j = cph; j < nh; j += W::WARPS / 4) {
             tmem_st4(tbase + W::tA + 4 * j, sQA[rA + j * nh], sQB[rA + j * nh]);
             tmem_st4(tbase + W::tB + 4 * j, sQA[rB + j * nh], sQB[rB + j * nh]);
         }
-        for (int s = cph; s < 13; s += 4) {
+        for (int s = cph; s < 13; s += W::WARPS / 4) {
             const int j = par + 2 * s;
             const bool ok = j < nq;
             tmem_st4(tbase + W::tC + 4 * s, ok ? sQA[rC + j * nh] : 0.0, ok ? sQB[rC + j * nh] : 0.0);
         }
         const int rows[3] = {rA, rB, rC};
-        for (int x = cph; x < 3 * Np; x += 4) {
+        for (int x = cph; x < 3 * Np; x += W::WARPS / 4) {
             const int q = x / Np, m = x - q * Np, r = rows[q];
             tmem_st2(tbase + W::tV + 30 * q + 2 * m, r < nq ? sVq[r + m * nq] : sVf[(r - nq) + m * nf]);
         }
-        for (int i = cph; i < nq; i += 4) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? sPq[lp + i * Np] : 0.0);
+        for (int i = cph; i < nq; i += W::WARPS / 4) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? sPq[lp + i * Np] : 0.0);
         asm volatile("tcgen05.wait::st.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");

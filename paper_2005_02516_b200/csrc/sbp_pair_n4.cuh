@@ -25,7 +25,7 @@ namespace swedg {
 
 struct SbpPairN4 {
     static constexpr int nq = 37, nf = 15, npf = 5, nrow = 52;
-    static constexpr int WARPS = 16, T = WARPS * 32;
+    static constexpr int WARPS = SWEDG_PAIR_WARPS, T = WARPS * 32;  // a multiple of 4 (TMEM lane quarters)
     // TMEM columns (32-bit): (QA,QB)_ij = 4 columns
     static constexpr int t0 = 0;     // row l'      : 37 columns j
     static constexpr int t1 = 148;   // row l'+16   : 37 columns j
@@ -102,11 +102,11 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
     {  // the operator rows depend only on l': one copy per TMEM lane quarter, filled by
        // the quarter's four warps (column phase warp >> 2)
         const int cph = warp >> 2;
-        for (int j = cph; j < nq; j += 4) {
+        for (int j = cph; j < nq; j += W::WARPS / 4) {
             tmem_st4(tbase + W::t0 + 4 * j, sQA[r0 + j * nq], sQB[r0 + j * nq]);
             tmem_st4(tbase + W::t1 + 4 * j, sQA[r1 + j * nq], sQB[r1 + j * nq]);
         }
-        for (int s = cph; s < 13; s += 4) {
+        for (int s = cph; s < 13; s += W::WARPS / 4) {
             const int j = ph + 3 * s;
             const bool ok = xrow && j < nq;
             tmem_st4(tbase + W::tX + 4 * s, ok ? sQA[rX + j * nq] : 0.0, ok ? sQB[rX + j * nq] : 0.0);
