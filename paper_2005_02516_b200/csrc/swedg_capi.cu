@@ -67,7 +67,8 @@ struct swedg_handle_s {
     double* bs = nullptr;    // [K][nh] (modal)
     double* src = nullptr;   // [K][2][nh] (SBP: [K][2][nq])
     double* u = nullptr;     // resident state
-    double* u_alt = nullptr; // SBP pair path: second state buffer (fused RK stages ping-pong)
+    double* u_alt = nullptr;  // SBP pair path: state buffers of the fused RK stages (u -> A -> B -> A -> B -> u)
+    double* u_alt2 = nullptr;
     double* res = nullptr;   // LSRK register
     double* utmp = nullptr;  // host-API scratch state
     double* du = nullptr;    // host-API scratch rhs
@@ -574,13 +575,13 @@ bool sbp_pair_path(swedg_handle h) {
 
 int run_step(swedg_handle h, const unsigned* ids, double dt) {
     if (sbp_pair_path(h)) {
-        // stages 0..3 fuse the RK update and ping-pong the state (u -> u_alt -> u -> ...):
-        // neighbours read the stage's input; stage 4 (input in u) uses the separate
-        // update kernel in place, so the step ends with the state in h->u
+        // every stage fuses the RK update, writing the next state into another buffer
+        // (neighbours read the stage's input): u -> A -> B -> A -> B -> u, so the step
+        // ends with the state in h->u and needs no separate update kernel
+        double* const seq[6] = {h->u, h->u_alt, h->u_alt2, h->u_alt, h->u_alt2, h->u};
         for (int s = 0; s < 5; ++s) {
-            double* in = (s & 1) ? h->u_alt : h->u;
-            StageArgs sa{in, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
-            sa.u_next = s < 4 ? ((s & 1) ? h->u : h->u_alt) : nullptr;
+            StageArgs sa{seq[s], 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
+            sa.u_next = seq[s + 1];
             if (run_stage(h, sa)) return h->last_code;
         }
         return SWEDG_OK;
@@ -980,7 +981,8 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     }
     const size_t ns = K * 3 * h->nstate();
     if (dalloc(h, &h->u, ns) || dalloc(h, &h->res, ns)) return bail(h->last_code);
-    if (h->scheme == SWEDG_SCHEME_SBP && (dalloc(h, &h->du, ns) || dalloc(h, &h->u_alt, ns))) return bail(h->last_code);
+    if (h->scheme == SWEDG_SCHEME_SBP && (dalloc(h, &h->du, ns) || dalloc(h, &h->u_alt, ns) || dalloc(h, &h->u_alt2, ns)))
+        return bail(h->last_code);
     if (dalloc(h, &h->err, 1)) return bail(h->last_code);
     ErrRec none_rec{kNoError, 0ull};
     if (cudaMemcpyAsync(h->err, &none_rec, sizeof(none_rec), cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
@@ -1001,7 +1003,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
-                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2, h->u_alt};
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2, h->u_alt, h->u_alt2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& p : h->ev_pending) {
