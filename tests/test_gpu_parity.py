@@ -329,3 +329,81 @@ def test_opt_in_volume_kernel_variants(variant):
             h.close()
     finally:
         os.environ.pop("SWEDG_VOLUME_KERNEL", None)
+
+
+def test_sbp_pair_pdl_and_state_rotation():
+    """SBP N=4 FAST pair path: every stage fuses the LSRK45 update with the state rotating
+    u -> A -> B -> A -> B -> u; the launches use programmatic dependent launch.  Steps
+    with PDL on / off (SWEDG_PDL=0) and graph replay / individual launches are bitwise
+    equal, and stay within the run tolerance of the reference's steps."""
+    import os
+
+    c = load_golden("sbp_dam_n4")
+    dt = float(c["dt"][0])
+    outs = []
+    for pdl, graphs in (("1", True), ("0", True), ("1", False)):
+        os.environ["SWEDG_PDL"] = pdl
+        try:
+            h = make(c, capi.MODE_FAST)
+        finally:
+            os.environ.pop("SWEDG_PDL", None)
+        h.set_graphs(graphs)
+        h.set_state(c["u"])
+        h.step(dt, 3)
+        u, res, t = h.get_state()
+        outs.append((u, res, t))
+    for u, res, t in outs[1:]:
+        np.testing.assert_array_equal(u, outs[0][0])
+        np.testing.assert_array_equal(res, outs[0][1])
+        assert t == outs[0][2]
+    u_ref, _, err = Oracle(c).step_lsrk45(c["u"], np.zeros_like(c["u"]), dt, 3)
+    assert err == 0
+    assert rel(outs[0][0], u_ref) <= RUN_TOL
+
+
+def test_sbp_rhs_device_unaligned_input_falls_back():
+    """The SBP pair kernel bulk-copies 16 B-aligned pair blocks; a caller's device input
+    that is only 8 B aligned takes the thread-per-node kernel instead (same tolerance)."""
+    import torch
+
+    c = load_golden("sbp_dam_n4")
+    h = make(c, capi.MODE_FAST)
+    u = np.ascontiguousarray(c["u"], dtype=np.float64)
+    n = u.size
+    buf = torch.empty(n + 1, dtype=torch.float64, device="cuda")
+    ua = buf[:n]
+    uu = buf[1:]  # 8 B past a 16 B boundary
+    du_a = torch.empty(n, dtype=torch.float64, device="cuda")
+    du_u = torch.empty(n, dtype=torch.float64, device="cuda")
+    ua.copy_(torch.from_numpy(u.ravel()))
+    h.rhs_device(ua.data_ptr(), du_a.data_ptr())
+    uu.copy_(torch.from_numpy(u.ravel()))
+    h.rhs_device(uu.data_ptr(), du_u.data_ptr())
+    torch.cuda.synchronize()
+    a = du_a.cpu().numpy().reshape(u.shape)
+    b = du_u.cpu().numpy().reshape(u.shape)
+    assert_fast_rhs(a, c["du_lf"], c, c["u"])
+    assert_fast_rhs(b, c["du_lf"], c, c["u"])
+
+
+def test_modal_volume_ranges_with_odd_split():
+    """Volume launches over element ranges [0, k) and [k, K) with k odd: the second
+    range's pair blocks are not 16 B aligned, so the pair kernel stages them with plain
+    loads instead of bulk copies — bitwise the full-range stage."""
+    c = load_golden("modal_n4_warp")
+    K = int(c["K"][0])
+    dt = float(c["dt"][0])
+    h1 = make(c, capi.MODE_FAST)
+    h1.set_state(c["u"])
+    h1.step(dt, 1)
+    u1, _, _ = h1.get_state()
+    h2 = make(c, capi.MODE_FAST)
+    h2.set_state(c["u"])
+    k = K // 2 + (1 - (K // 2) % 2)  # odd split point
+    for s in range(5):
+        h2.stage_volume_range(s, dt, 0, k)
+        h2.stage_volume_range(s, dt, k, K)
+        h2.stage_surface(s, dt)
+    h2.check()
+    u2, _, _ = h2.get_state()
+    np.testing.assert_array_equal(u2, u1)
