@@ -258,11 +258,28 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
             const double* su = stage + W::sU + 45 * half;
             const double* sg = stage + W::sG + 160 * half;
             const double* sb = stage + W::sB + 40 * half;
-            for (int r = lp; with_u && r < 45; r += 16) work[W::wU + r] = su[r];
-            for (int r = lp; r < 40; r += 16) {
-                work[W::wBs + r] = sb[r];
-                reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(sg[r], sg[nh + r]);
-                reinterpret_cast<double2*>(work + W::wD)[r] = make_double2(sg[2 * nh + r], sg[3 * nh + r]);
+            // all loads first (clamped indices, no divergence), then the stores: the
+            // load -> store dependency costs one latency instead of one per row
+            double pu[3], pb[3], p1[3], p2[3], p3[3], p4[3];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int r = lp + 16 * t, ru = r < 45 ? r : 44, rg = r < nh ? r : nh - 1;
+                pu[t] = su[ru];
+                pb[t] = sb[rg];
+                p1[t] = sg[rg];
+                p2[t] = sg[nh + rg];
+                p3[t] = sg[2 * nh + rg];
+                p4[t] = sg[3 * nh + rg];
+            }
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int r = lp + 16 * t;
+                if (with_u && r < 45) work[W::wU + r] = pu[t];
+                if (r < nh) {
+                    work[W::wBs + r] = pb[t];
+                    reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(p1[t], p2[t]);
+                    reinterpret_cast<double2*>(work + W::wD)[r] = make_double2(p3[t], p4[t]);
+                }
             }
         }
         __syncwarp();

@@ -201,15 +201,32 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         {
             const double* su = stage + W::sU + half * 3 * nq;
             const double* sg = stage + W::sG + half * 4 * W::gseg;
-            for (int j = lp; j < nq; j += 16) {
-                const double h = su[j], hu = su[nq + j], hv = su[2 * nq + j];
-                if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);  // check_positive (:381)
-                const double ih = 1.0 / h;
-                reinterpret_cast<double2*>(work + W::wA)[j] = make_double2(hu, hv);
-                reinterpret_cast<double2*>(work + W::wB)[j] = make_double2(hu * ih, hv * ih);
-                reinterpret_cast<double2*>(work + W::wC)[j] = make_double2(sg[j], sg[W::gseg + j]);
-                reinterpret_cast<double2*>(work + W::wD)[j] = make_double2(sg[2 * W::gseg + j], sg[3 * W::gseg + j]);
-                work[W::wH + j] = h;
+            // all loads first (clamped indices, no divergence), then the stores
+            double ph[3], pu[3], pv[3], p1[3], p2[3], p3[3], p4[3];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int j = min(lp + 16 * t, nq - 1);
+                ph[t] = su[j];
+                pu[t] = su[nq + j];
+                pv[t] = su[2 * nq + j];
+                p1[t] = sg[j];
+                p2[t] = sg[W::gseg + j];
+                p3[t] = sg[2 * W::gseg + j];
+                p4[t] = sg[3 * W::gseg + j];
+            }
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int j = lp + 16 * t;
+                if (j < nq) {
+                    const double h = ph[t], hu = pu[t], hv = pv[t];
+                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);  // check_positive (:381)
+                    const double ih = 1.0 / h;
+                    reinterpret_cast<double2*>(work + W::wA)[j] = make_double2(hu, hv);
+                    reinterpret_cast<double2*>(work + W::wB)[j] = make_double2(hu * ih, hv * ih);
+                    reinterpret_cast<double2*>(work + W::wC)[j] = make_double2(p1[t], p2[t]);
+                    reinterpret_cast<double2*>(work + W::wD)[j] = make_double2(p3[t], p4[t]);
+                    work[W::wH + j] = h;
+                }
             }
         }
         __syncwarp();
