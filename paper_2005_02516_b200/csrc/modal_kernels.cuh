@@ -358,7 +358,6 @@ modal_surface_kernel(ModalSurfParams prm) {
     using O = ModalOps<N>;
     constexpr int Np = D::Np, nq = D::nq, nf = D::nf, nh = D::nh, npf = D::npf;
     constexpr int L = SurfCfg<N>::L, E = SurfCfg<N>::E, T = SurfCfg<N>::T;
-    if (prm.early_exit && error_pending(prm.err)) return;
 
     constexpr int NPK = Np * (Np + 1) / 2;
     __shared__ double sst[E][3 * nf];
@@ -378,6 +377,11 @@ modal_surface_kernel(ModalSurfParams prm) {
         const double* src = prm.Mpk + (size_t)k0 * NPK;
         for (int x = lane; x < ne * NPK; x += 32) sMpk[ew0 * NPK + x] = src[x];
     }
+    // M_h^{-1} is launch-invariant: under programmatic dependent launch its copy overlaps
+    // the volume kernel's tail; the traces, accumulators and state are read after the wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (prm.early_exit && error_pending(prm.err)) return;
 
     // ---- issue every independent global load up front (memory-level parallelism:
     //      ncu showed this kernel long-scoreboard bound with phase-serial loads)

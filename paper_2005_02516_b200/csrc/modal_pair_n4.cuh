@@ -144,7 +144,6 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     using O = ModalOps<4>;
     constexpr int Np = W::Np, nq = W::nq, nf = W::nf, nh = W::nh, npf = 5;
     const ModalVolParams& prm = ps.v;
-    if (prm.early_exit && error_pending(prm.err)) return;
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
@@ -215,6 +214,18 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
+
+    // everything above reads launch-invariant operators only: under programmatic
+    // dependent launch it overlaps the previous kernel's tail; from here on the
+    // previous kernels' outputs (state, traces, error record) are read
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (prm.early_exit && error_pending(prm.err)) {
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(W::tcols));
+        return;
+    }
 
     const double g = prm.g, ig = 1.0 / g, g2 = 2.0 * g;
     const int npairs = (prm.K + 1) / 2;
@@ -677,6 +688,9 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         }
         __syncwarp();
     }
+    // the interface kernel's CTAs cannot be resident beside this CTA anyway (shared
+    // memory, registers): let them launch as this CTA's work ends
+    asm volatile("griddepcontrol.launch_dependents;");
 
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();

@@ -52,7 +52,10 @@ struct swedg_handle_s {
     // TMEM operators), 1 = "tworow", 2 = "row", 3 = "warp" (N=4, warp/element, TMEM),
     // 4 = "quad" (N=4, 4 elements/warp; measured slower: latency-bound at 6 warps/SM)
     int vol_variant = 0;
-    bool pdl = true;  // programmatic dependent launch of the SBP pair kernel (SWEDG_PDL=0: off)
+    // programmatic dependent launch (SWEDG_PDL bit mask): 1 modal pair volume kernel,
+    // 2 modal interface kernel, 4 SBP pair kernel.  Default 1|4: measured, PDL on the
+    // interface kernel costs ~2 ms per C4 step (device-resident and chunked alike)
+    int pdl_mask = 5;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // device buffers
@@ -228,6 +231,24 @@ struct KTimer {
 
 // Opt a kernel into its dynamic shared memory once per (kernel, device) and
 // return its occupancy (resident CTAs per SM) for persistent grids.
+// Launch with programmatic dependent launch allowed (pdl): the kernel's prologue
+// (launch-invariant operator staging) may overlap the previous kernel's tail.  Only for
+// kernels that execute griddepcontrol.wait before reading any dependent data.
+template <typename P>
+inline void launch_pdl(void (*kern)(P), int grid, int block, size_t smem, cudaStream_t st, bool pdl, const P& prm) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, prm);
+}
+
 int kernel_occupancy(const void* kern, int device, int threads, size_t smem) {
     struct Entry {
         const void* k;
@@ -252,7 +273,7 @@ void launch_pair(swedg_handle h, const PairStageParams& ps) {
     const size_t psm = PairN4::bytes();
     const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
     const int grid = std::min((ps.v.K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
-    kern<<<std::max(grid, 1), PairN4::T, psm, h->stream>>>(ps);
+    launch_pdl(kern, std::max(grid, 1), PairN4::T, psm, h->stream, (h->pdl_mask & 1) != 0, ps);
 }
 
 // the SBP pair kernel bulk-copies (TMA) per-pair blocks: every source must be 16 B aligned
@@ -380,9 +401,9 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     {
         KTimer kt(h, 1);
         if (h->mode == SWEDG_MODE_PARITY)
-            modal_surface_kernel<N, true><<<grid, SC::T, 0, h->stream>>>(sp);
+            launch_pdl(modal_surface_kernel<N, true>, grid, SC::T, 0, h->stream, (h->pdl_mask & 2) != 0, sp);
         else
-            modal_surface_kernel<N, false><<<grid, SC::T, 0, h->stream>>>(sp);
+            launch_pdl(modal_surface_kernel<N, false>, grid, SC::T, 0, h->stream, (h->pdl_mask & 2) != 0, sp);
     }
     h->launches++;
     cudaError_t e = cudaGetLastError();
@@ -436,17 +457,7 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
             // programmatic dependent launch: the CTAs' operator staging and TMEM fill
             // overlap the previous kernel's tail (the kernel waits on griddepcontrol
             // before touching the state)
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(std::max(1, std::min(blocks, occ * h->nsm)));
-            cfg.blockDim = dim3(SbpPairN4::T);
-            cfg.dynamicSmemBytes = psm;
-            cfg.stream = h->stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            cudaLaunchKernelEx(&cfg, kern, sp);
+            launch_pdl(kern, std::max(1, std::min(blocks, occ * h->nsm)), SbpPairN4::T, psm, h->stream, (h->pdl_mask & 4) != 0, sp);
         } else {
             go(sbp_rhs_kernel<N, false>);
         }
@@ -561,7 +572,7 @@ int run_fused_tail(swedg_handle h, const unsigned* ids, double dt) {
     sp.early_exit = 1;
     sp.k_begin = 0;
     using SC = SurfCfg<4>;
-    modal_surface_kernel<4, false><<<(h->K + SC::E - 1) / SC::E, SC::T, 0, h->stream>>>(sp);
+    launch_pdl(modal_surface_kernel<4, false>, (h->K + SC::E - 1) / SC::E, SC::T, 0, h->stream, (h->pdl_mask & 2) != 0, sp);
     h->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
@@ -850,7 +861,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->g = d->g;
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_FUSION")) h->fusion = std::string(v) == "1";
-    if (const char* v = std::getenv("SWEDG_PDL")) h->pdl = std::string(v) != "0";
+    if (const char* v = std::getenv("SWEDG_PDL")) h->pdl_mask = std::atoi(v);
     if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
         std::string sv(v);
         h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : (sv == "quad" ? 4 : 0)));

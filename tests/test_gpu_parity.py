@@ -334,14 +334,14 @@ def test_opt_in_volume_kernel_variants(variant):
 def test_sbp_pair_pdl_and_state_rotation():
     """SBP N=4 FAST pair path: every stage fuses the LSRK45 update with the state rotating
     u -> A -> B -> A -> B -> u; the launches use programmatic dependent launch.  Steps
-    with PDL on / off (SWEDG_PDL=0) and graph replay / individual launches are bitwise
+    with PDL on / off (SWEDG_PDL=4 / 0) and graph replay / individual launches are bitwise
     equal, and stay within the run tolerance of the reference's steps."""
     import os
 
     c = load_golden("sbp_dam_n4")
     dt = float(c["dt"][0])
     outs = []
-    for pdl, graphs in (("1", True), ("0", True), ("1", False)):
+    for pdl, graphs in (("4", True), ("0", True), ("4", False)):  # SWEDG_PDL bit 4: SBP pair kernel
         os.environ["SWEDG_PDL"] = pdl
         try:
             h = make(c, capi.MODE_FAST)
@@ -407,3 +407,30 @@ def test_modal_volume_ranges_with_odd_split():
     h2.check()
     u2, _, _ = h2.get_state()
     np.testing.assert_array_equal(u2, u1)
+
+
+@pytest.mark.parametrize("mask", ["0", "1", "3"])
+def test_modal_pdl_launches_bitwise(mask):
+    """Modal FAST N=4: programmatic dependent launch of the volume (bit 1) and interface
+    (bit 2) kernels changes only when a kernel's prologue runs, never a result: device
+    steps, host-state (chunked wavefront) steps and an RHS are bitwise the PDL-off ones."""
+    import os
+
+    c = load_golden("modal_n4_warp")
+    dt = float(c["dt"][0])
+    res = []
+    for m in ("0", mask):
+        os.environ["SWEDG_PDL"] = m
+        try:
+            h = make(c, capi.MODE_FAST)
+        finally:
+            os.environ.pop("SWEDG_PDL", None)
+        h.set_state(c["u"])
+        h.step(dt, 3)
+        u, _, _ = h.get_state()
+        uh = np.array(c["u"], copy=True)
+        h.set_state(uh)
+        h.step_host(uh, dt, 2, 4)
+        res.append((u, uh, h.rhs(c["u"])))
+    for a, b in zip(res[0], res[1]):
+        np.testing.assert_array_equal(a, b)

@@ -14,7 +14,7 @@ h = case.handle()
 st = torch.cuda.Stream()
 h.set_stream(st.cuda_stream)
 uh = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
-for C in (4, 6, 8, 12, 16, 24):
+for C in [int(x) for x in (sys.argv[1].split(',') if len(sys.argv) > 1 else '4,6,8,12,16,24'.split(','))]:
     uh[...] = u0
     h.set_state(uh)
     h.step_host(uh, case.dt, 1, C)  # warm-up (adjacency check, events)
