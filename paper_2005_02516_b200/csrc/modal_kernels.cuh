@@ -350,8 +350,11 @@ struct SurfCfg {
     static constexpr int E = T / L;
 };
 
+#ifndef SWEDG_SURF_MINB
+#define SWEDG_SURF_MINB 8
+#endif
 template <int N, bool P>
-__global__ void __launch_bounds__(128, 8)
+__global__ void __launch_bounds__(128, SWEDG_SURF_MINB)
 modal_surface_kernel(ModalSurfParams prm) {
     using D = ModalDims<N>;
     using A = Ar<P>;
@@ -370,12 +373,22 @@ modal_surface_kernel(ModalSurfParams prm) {
     const bool act = k < prm.K;
     const double g = prm.g;
     static_assert(32 % L == 0, "an element's lanes must lie in one warp");
-    if constexpr (!P) {  // packed M_h^{-1} of the warp's elements: one contiguous coalesced copy per warp
+    if constexpr (!P) {  // packed M_h^{-1} of the warp's elements: one contiguous copy per warp,
+        // global -> shared by cp.async (16 B granules: an element's block is 960 B), so it
+        // neither holds registers nor serialises load -> store; waited for before the M^-1 product
         constexpr int EW = 32 / L;  // elements per warp
         const int lane = tid & 31, ew0 = (tid >> 5) * EW;
         const int k0 = prm.k_begin + blockIdx.x * E + ew0, ne = max(0, min(EW, prm.K - k0));
         const double* src = prm.Mpk + (size_t)k0 * NPK;
-        for (int x = lane; x < ne * NPK; x += 32) sMpk[ew0 * NPK + x] = src[x];
+        if (NPK % 2 == 0 && (reinterpret_cast<uintptr_t>(prm.Mpk) & 15u) == 0) {  // (N = 1, 4)
+            for (int x = lane; x < ne * NPK / 2; x += 32) {
+                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sMpk + ew0 * NPK + 2 * x));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 2 * x) : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        } else {
+            for (int x = lane; x < ne * NPK; x += 32) sMpk[ew0 * NPK + x] = src[x];
+        }
     }
     // M_h^{-1} is launch-invariant: under programmatic dependent launch its copy overlaps
     // the volume kernel's tail; the traces, accumulators and state are read after the wait
@@ -468,7 +481,8 @@ modal_surface_kernel(ModalSurfParams prm) {
             smod[e][c * Np + s] = A::add(t1r[c], t2);
         }
     }
-    __syncwarp();  // an element's L lanes lie in one warp (L divides 32)
+    if constexpr (!P) asm volatile("cp.async.wait_all;" ::: "memory");  // this lane's M^-1 granules
+    __syncwarp();  // an element's L lanes lie in one warp (L divides 32); every lane's M^-1 granules
     // du = Mh_inv modal; finiteness; fused LSRK45 register update
     if (act && s < Np) {
         double du[3] = {0.0, 0.0, 0.0};
