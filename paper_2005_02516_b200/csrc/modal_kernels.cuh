@@ -366,6 +366,7 @@ modal_surface_kernel(ModalSurfParams prm) {
     __shared__ double sst[E][3 * nf];
     __shared__ double smod[E][3 * Np];
     __shared__ double sMpk[P ? 1 : E * NPK];
+    __shared__ double sTUR[P ? 1 : 3 * E * 3 * Np];  // FAST: T1 | u | res of the CTA's elements (cp.async)
     const double* gVf = prm.ops + O::Vf;  // 1.8 KB, read through L1 by every warp
     const int tid = threadIdx.x;
     const int e = tid / L, s = tid % L;
@@ -401,12 +402,29 @@ modal_surface_kernel(ModalSurfParams prm) {
     double t1r[3] = {0, 0, 0}, ur[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, mrow[P ? Np : 1];
     if (act && s < Np) {
         const size_t o = (size_t)k * 3 * Np + s;
+        if constexpr (!P) {  // straight into shared memory (8 B cp.async): consumed after the flux work
+            double* d = sTUR + e * 3 * Np + s;
+            constexpr int A = E * 3 * Np;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            t1r[c] = prm.T1[o + c * Np];
-            if (prm.rk_mode) {
-                ur[c] = prm.u[o + c * Np];
-                rr[c] = prm.res[o + c * Np];
+            for (int c = 0; c < 3; ++c) {
+                const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(d + c * Np));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a), "l"(prm.T1 + o + c * Np) : "memory");
+                if (prm.rk_mode) {
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a + 8u * A), "l"(prm.u + o + c * Np)
+                                 : "memory");
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a + 16u * A), "l"(prm.res + o + c * Np)
+                                 : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                t1r[c] = prm.T1[o + c * Np];
+                if (prm.rk_mode) {
+                    ur[c] = prm.u[o + c * Np];
+                    rr[c] = prm.res[o + c * Np];
+                }
             }
         }
         if constexpr (P) {
@@ -470,7 +488,22 @@ modal_surface_kernel(ModalSurfParams prm) {
         sst[e][nf + s] = A::sub(A::mul(mgh, srx), acc[1]);
         sst[e][2 * nf + s] = A::sub(A::mul(mgh, sry), acc[2]);
     }
+    if constexpr (!P) asm volatile("cp.async.wait_all;" ::: "memory");  // M^-1 granules, own T1/u/res
     __syncwarp();  // this warp's M_h^{-1} block and its elements' stacked rows
+    if constexpr (!P) {
+        if (act && s < Np) {
+            constexpr int A = E * 3 * Np;
+            const double* d = sTUR + e * 3 * Np + s;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                t1r[c] = d[c * Np];
+                if (prm.rk_mode) {
+                    ur[c] = d[A + c * Np];
+                    rr[c] = d[2 * A + c * Np];
+                }
+            }
+        }
+    }
     // modal = T1 + Vf^T stacked_surface  (solver.hpp:285-286)
     if (act && s < Np) {
 #pragma unroll
@@ -481,8 +514,7 @@ modal_surface_kernel(ModalSurfParams prm) {
             smod[e][c * Np + s] = A::add(t1r[c], t2);
         }
     }
-    if constexpr (!P) asm volatile("cp.async.wait_all;" ::: "memory");  // this lane's M^-1 granules
-    __syncwarp();  // an element's L lanes lie in one warp (L divides 32); every lane's M^-1 granules
+    __syncwarp();  // an element's L lanes lie in one warp (L divides 32)
     // du = Mh_inv modal; finiteness; fused LSRK45 register update
     if (act && s < Np) {
         double du[3] = {0.0, 0.0, 0.0};
