@@ -196,7 +196,8 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         const int cph = warp >> 2;
         for (int j = cph; j < nh; j += W::WARPS / 4) {
             tmem_st4(tbase + W::tA + 4 * j, sQA[rA + j * nh], sQB[rA + j * nh]);
-            tmem_st4(tbase + W::tB + 4 * j, sQA[rB + j * nh], sQB[rB + j * nh]);
+            const bool ss = rB >= nq && j >= nq;  // surface-surface block: exactly zero in the skew operator
+            tmem_st4(tbase + W::tB + 4 * j, ss ? 0.0 : sQA[rB + j * nh], ss ? 0.0 : sQB[rB + j * nh]);
         }
         for (int s = cph; s < 13; s += W::WARPS / 4) {
             const int j = par + 2 * s;
@@ -618,7 +619,10 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
             af[nf] = RB.a1;
             af[2 * nf] = RB.a2;
         }
-        // ---- loop C: volume rows rA (all), rB (l' <= 8) x surface columns 25..39
+        // ---- loop C: volume rows rA (all), rB (l' <= 8) x surface columns 25..39.  Branch-
+        //      free: for l' >= 9 row rB is a finished surface row whose slots hold the skew
+        //      operator's (exactly zero) surface-surface block, so it gains exact zeros;
+        //      predicating those pairs split the two FMA chains into separate blocks (+1 %)
 #pragma unroll 1
         for (int j0 = nq; j0 < nh; j0 += 4) {
             double2 qa[4], qb[4];
@@ -630,7 +634,7 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
                     const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
                     const double hj = nH[j];
                     pair6(RA, qa[p], A, B, C.x, C.y, D.x, D.y, hj);
-                    if (bvol) pair6(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);
+                    pair6(RB, qb[p], A, B, C.x, C.y, D.x, D.y, hj);  // l' >= 9: zero operator, finished row
                 }
             }
         }
