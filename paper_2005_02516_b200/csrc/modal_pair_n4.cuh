@@ -138,7 +138,11 @@ struct PairN4 {
 // S = true: the fused interface+volume instantiation (ps.do_surface / ps.do_volume
 // select the phases); S = false: the volume-only kernel of the split stage.
 template <bool S>
+#ifdef SWEDG_PAIR_MAXNREG  // register cap below the 1-CTA/SM limit (co-residency experiments)
+__global__ void __maxnreg__(SWEDG_PAIR_MAXNREG)
+#else
 __global__ void __launch_bounds__(PairN4::T, 1)
+#endif
 modal_volume_pair_n4_kernel(PairStageParams ps) {
     using W = PairN4;
     using O = ModalOps<4>;
