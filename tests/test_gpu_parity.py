@@ -434,3 +434,30 @@ def test_modal_pdl_launches_bitwise(mask):
         res.append((u, uh, h.rhs(c["u"])))
     for a, b in zip(res[0], res[1]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("ntri", [1, 2, 3])
+@pytest.mark.parametrize("scheme", ["modal", "sbp"])
+def test_tiny_meshes_pair_kernels(ntri, scheme):
+    """K = 1, 2, 3 (fans of 1..3 wall-bounded triangles): the pair kernels' smallest
+    launches — a lone element, one full pair (bulk copies), a pair plus a tail — for
+    the modal N=4 and SBP N=4 FAST paths, RHS within tolerance of the C oracle and
+    LSRK45 steps within the run tolerance."""
+    import math as m
+    verts = [[0.0, 0.0]] + [[0.6 * m.cos(0.5 * m.pi * i / 3), 0.6 * m.sin(0.5 * m.pi * i / 3)] for i in range(ntri + 1)]
+    tris = [[0, 1 + i, 2 + i] for i in range(ntri)]
+    sch = capi.SCHEME_SBP if scheme == "sbp" else capi.SCHEME_HYBRIDIZED
+    c = capi.Case("smooth", scheme=sch, N=4, mesh=dict(verts=verts, tris=tris, domain=(0.0, 0.0, 2.0, 2.0)))
+    assert c.K == ntri
+    cd = case_dict(c)
+    u = c.u0()
+    ref, err, _ = Oracle(cd).rhs(u)
+    assert err == 0
+    h = c.handle(mode=capi.MODE_FAST)
+    assert_fast_rhs(h.rhs(u), ref, cd, u)
+    dt = 0.5 * c.dt
+    u_ref, _, err = Oracle(cd).step_lsrk45(u, np.zeros_like(u), dt, 3)
+    assert err == 0
+    h.set_state(u)
+    h.step(dt, 3)
+    assert rel(h.get_state()[0], u_ref) <= RUN_TOL
