@@ -219,3 +219,27 @@ def test_acceptance_7_dam_break_robustness():
     drift = abs(s[-1, 1] - s[0, 1]) / s[0, 1]
     assert min_h > 0.0 and drift <= 1e-8, (min_h, drift)
     assert abs(min_h - 1.146) < 5e-3, min_h  # the reference's value (3 digits printed)
+
+
+@pytest.mark.gpu
+def test_c3_positivity_loss_matches_reference_arithmetic():
+    """C3 toward its horizon: the reference scheme itself (PARITY = the reference's
+    arithmetic bit for bit) loses positivity in this dam break at t ~ 0.070 (no limiter in
+    the paper's scheme); FAST stops at the same element and stage time with the
+    reference's message, after a trajectory equal to PARITY's to rounding."""
+    c = capi.Case("dambreak", scheme=capi.SCHEME_SBP, N=4, nx=128, cfl=0.0625)
+    stops = []
+    for mode in (capi.MODE_PARITY, capi.MODE_FAST):
+        h = c.handle(mode=mode)
+        h.set_state(c.u0())
+        h.step(c.dt, 150)
+        u150, _, _ = h.get_state()
+        with pytest.raises(capi.PositivityError) as ei:
+            h.step(c.dt, 100)
+        assert "nonpositive water height in element" in str(ei.value)
+        stops.append((ei.value.elem, ei.value.t, u150))
+    assert stops[0][0] == stops[1][0]
+    assert abs(stops[0][1] - stops[1][1]) < 1e-12
+    assert 0.06 < stops[0][1] < 0.08
+    u_p, u_f = stops[0][2], stops[1][2]
+    assert np.abs(u_f - u_p).max() / (1 + np.abs(u_p).max()) < 1e-10
