@@ -243,3 +243,20 @@ def test_c3_positivity_loss_matches_reference_arithmetic():
     assert 0.06 < stops[0][1] < 0.08
     u_p, u_f = stops[0][2], stops[1][2]
     assert np.abs(u_f - u_p).max() / (1 + np.abs(u_p).max()) < 1e-10
+
+
+@pytest.mark.gpu
+def test_c4_bench_horizon_fast_vs_reference_arithmetic():
+    """The bench workload itself (C4, K = 2,097,152, 25 LSRK45 steps = the bench's warm-up
+    plus timed steps): the production FAST path stays within the run tolerance
+    (1e-10 relative) of PARITY, the reference's arithmetic bit for bit."""
+    c = capi.Case("smooth", N=4, nx=1024, warp=0.1, seed=23)
+    outs = []
+    for mode in (capi.MODE_PARITY, capi.MODE_FAST):
+        h = c.handle(mode=mode)
+        h.set_state(c.u0())
+        h.step(c.dt, 25)
+        outs.append(h.get_state()[0])
+        h.close()
+    d = np.abs(outs[1] - outs[0]).max() / (1 + np.abs(outs[0]).max())
+    assert d <= 1e-10, d
