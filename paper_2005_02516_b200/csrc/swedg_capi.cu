@@ -23,6 +23,7 @@
 #include "modal_warp_n4.cuh"
 #include "modal_quad_n4.cuh"
 #include "modal_pair_n4.cuh"
+#include "modal_pair_n3.cuh"
 #include "sbp_kernels.cuh"
 #include "sbp_pair_n4.cuh"
 #include "diag_kernels.cuh"
@@ -338,6 +339,12 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
             ps.do_surface = 0;
             ps.do_volume = 1;
             launch_pair(h, ps);
+        } else if (N == 3 && h->vol_variant == 0) {  // N = 3 pair kernel, operators in TMEM
+            auto kern = modal_volume_pair_n3_kernel;
+            const size_t psm = PairN3::bytes();
+            const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN3::T, psm);
+            const int grid = std::min((vp.K + 2 * PairN3::WARPS - 1) / (2 * PairN3::WARPS), occ * h->nsm);
+            launch_pdl(kern, std::max(grid, 1), PairN3::T, psm, h->stream, (h->pdl_mask & 1) != 0, vp);
         } else if (N == 4 && h->vol_variant == 4) {
             auto kern = modal_volume_quad_n4_kernel;
             const size_t qsm = QuadN4::bytes();

@@ -135,12 +135,13 @@ def _entropy_vars(h, hu, hv, b, g):
     return g * (h + b) - 0.5 * (vx * vx + vy * vy), vx, vy
 
 
-def test_fast_modal_entropy_balance_and_mass_k1d64():
+@pytest.mark.parametrize("N", [3, 4])
+def test_fast_modal_entropy_balance_and_mass_k1d64(N):
     """The reference's semi-discrete entropy balance (test_solver.cpp:172-206) for the
-    FAST N=4 pair kernel on a curved K1D=64 mesh: entropy-conservative flux ->
+    FAST N=3 and N=4 pair kernels on a curved K1D=64 mesh: entropy-conservative flux ->
     sum_k v_h^T M_h du ~ 0 (1e-9 of the RHS scale), Lax-Friedrichs -> <= 0,
     mass conserved by both (entropy_rate / conservation_rate, solver.hpp:503-563)."""
-    c = capi.Case("smooth", N=4, nx=64, warp=0.1)
+    c = capi.Case("smooth", N=N, nx=64, warp=0.1)
     K, Np, nq = c.K, c.Np, c.nq
     u = c.u0()
     Vq = c.array("Vq").reshape(Np, nq).T

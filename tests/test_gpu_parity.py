@@ -461,3 +461,27 @@ def test_tiny_meshes_pair_kernels(ntri, scheme):
     h.set_state(u)
     h.step(dt, 3)
     assert rel(h.get_state()[0], u_ref) <= RUN_TOL
+
+
+def test_n3_pair_kernel_matches_previous_fast_kernel():
+    """FAST N=3: the pair kernel (default) and the earlier two-rows-per-thread FAST kernel
+    (SWEDG_VOLUME_KERNEL=tworow) agree to rounding on a curved C4-generator mesh with an
+    odd element count, and both stay within the tolerance of the C oracle."""
+    import os
+
+    c = capi.Case("smooth", N=3, nx=9, warp=0.1)  # K = 162
+    cd = case_dict(c)
+    u = c.u0()
+    ref, err, _ = Oracle(cd).rhs(u)
+    assert err == 0
+    hp = c.handle(mode=capi.MODE_FAST)
+    du_pair = hp.rhs(u)
+    os.environ["SWEDG_VOLUME_KERNEL"] = "tworow"
+    try:
+        ho = c.handle(mode=capi.MODE_FAST)
+    finally:
+        os.environ.pop("SWEDG_VOLUME_KERNEL", None)
+    du_old = ho.rhs(u)
+    assert_fast_rhs(du_pair, ref, cd, u)
+    assert_fast_rhs(du_old, ref, cd, u)
+    assert rel(du_pair, du_old) <= 1e-12
