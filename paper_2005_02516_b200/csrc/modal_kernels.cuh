@@ -386,10 +386,13 @@ modal_surface_kernel(ModalSurfParams prm) {
                 const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sMpk + ew0 * NPK + 2 * x));
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 2 * x) : "memory");
             }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        } else {
-            for (int x = lane; x < ne * NPK; x += 32) sMpk[ew0 * NPK + x] = src[x];
+        } else {  // odd block length (N = 2, 3): 8 B granules
+            for (int x = lane; x < ne * NPK; x += 32) {
+                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sMpk + ew0 * NPK + x));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + x) : "memory");
+            }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // M_h^{-1} is launch-invariant: under programmatic dependent launch its copy overlaps
     // the volume kernel's tail; the traces, accumulators and state are read after the wait

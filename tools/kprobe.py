@@ -13,7 +13,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2005_02516_b200 import capi  # noqa: E402
 
-MODAL_FLOP = 48340                           # projection + volume + volume lift per element
+MODAL_N = int(os.environ.get("KPROBE_N", "4"))
+# projection + volume + volume lift per element (SURVEY §8(d) accounting)
+MODAL_FLOP = {3: 3996 + 17356 + 6 * 10 * 16, 4: 48340}[MODAL_N]
 SBP_FLOP = 55 * 666 + 33 * 15 + 7 * 37       # SURVEY §8(d) SBP N=4
 
 
@@ -48,6 +50,6 @@ if __name__ == "__main__":
     PEAK = capi.probe_fp64_peak(0, 3)
     print(f"fp64 peak {PEAK:.2f} TFLOP/s", flush=True)
     if mk > 0:
-        run(capi.Case("smooth", N=4, nx=mk, warp=0.1, seed=23), MODAL_FLOP, steps, f"modal N=4 K1D={mk}")
+        run(capi.Case("smooth", N=MODAL_N, nx=mk, warp=0.1, seed=23), MODAL_FLOP, steps, f"modal N={MODAL_N} K1D={mk}")
     if sk > 0:
         run(capi.Case("dambreak", scheme=capi.SCHEME_SBP, N=4, nx=sk, cfl=0.0625), SBP_FLOP, steps, f"sbp N=4 K1D={sk}")
