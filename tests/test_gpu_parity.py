@@ -295,12 +295,12 @@ def test_odd_element_count_imported_mesh(N):
     assert rel(uh, u_ref) <= RUN_TOL
 
 
-@pytest.mark.parametrize("scheme", ["modal", "sbp"])
+@pytest.mark.parametrize("scheme", ["modal", "sbp", "modal_n3"])
 def test_positivity_error_in_pair_kernels(scheme):
-    """FAST N=4 pair kernels (modal and SBP) report a nonpositive height with the
+    """FAST pair kernels (modal N=4 and N=3, SBP N=4) report a nonpositive height with the
     reference's element id, from rhs() and from graph-replayed steps."""
     sc = capi.SCHEME_SBP if scheme == "sbp" else capi.SCHEME_HYBRIDIZED
-    c = capi.Case("smooth", scheme=sc, N=4, nx=8, warp=0.1)
+    c = capi.Case("smooth", scheme=sc, N=3 if scheme == "modal_n3" else 4, nx=8, warp=0.1)
     h = c.handle(mode=capi.MODE_FAST)
     u = c.u0()
     u[77, 0, :] = -1.0 if sc == capi.SCHEME_SBP else 0.0
