@@ -386,11 +386,12 @@ def test_sbp_rhs_device_unaligned_input_falls_back():
     assert_fast_rhs(b, c["du_lf"], c, c["u"])
 
 
-def test_modal_volume_ranges_with_odd_split():
+@pytest.mark.parametrize("name", ["modal_n4_warp", "modal_n3_warp"])
+def test_modal_volume_ranges_with_odd_split(name):
     """Volume launches over element ranges [0, k) and [k, K) with k odd: the second
-    range's pair blocks are not 16 B aligned, so the pair kernel stages them with plain
-    loads instead of bulk copies — bitwise the full-range stage."""
-    c = load_golden("modal_n4_warp")
+    range's pair blocks are not 16 B aligned, so the pair kernels (N=4, N=3) stage them
+    with plain loads instead of bulk copies — bitwise the full-range stage."""
+    c = load_golden(name)
     K = int(c["K"][0])
     dt = float(c["dt"][0])
     h1 = make(c, capi.MODE_FAST)
