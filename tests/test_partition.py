@@ -147,20 +147,21 @@ def test_logical_partitions_on_one_gpu_equal_global(P):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("N", [3, 4])
 @pytest.mark.parametrize("P", [2, 3])
-def test_boundary_first_volume_ranges_equal_global(P):
+def test_boundary_first_volume_ranges_equal_global(P, N):
     """The overlapped schedule (partition.stage_overlapped): boundary rows' volume kernel,
     halo exchange, interior volume kernel, surface kernel — with logical partitions on
-    one GPU — bit-for-bit the unpartitioned steps."""
+    one GPU — bit-for-bit the unpartitioned steps (N=4 and N=3 pair kernels)."""
     from paper_2005_02516_b200.partition import trace_tensor
 
-    g = capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
+    g = capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
     hg = g.handle(mode=capi.MODE_FAST)
     hg.set_state(g.u0())
     dt = 1e-3
     hg.step(dt, 2)
     ug, _, _ = hg.get_state()
-    cases = [capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, strips=P, strip=r, threads=1) for r in range(P)]
+    cases = [capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=r, threads=1) for r in range(P)]
     hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
     for h, c in zip(hs, cases):
         h.set_state(c.u0())
