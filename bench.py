@@ -13,16 +13,31 @@ handle's stream; max over ranks); `e2e` goes through the public C ABI with
 pinned HOST buffers (H2D of the state, one step, D2H of the state per step).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling weak|strong]
+
+Multi-GPU (--gpus N > 1; launched by torchrun, or re-executed under it when
+WORLD_SIZE is unset): the mesh is partitioned into N y-strips (setup.cpp
+compact_strip), one rank per GPU; every RK stage exchanges only the cut-face
+traces with ncclSend/ncclRecv on a library-owned NCCL communicator, overlapped
+with the interior volume kernel, inside the captured step graph.  Weak scaling
+(default): every rank owns a K1D x K1D strip of a K1D x (N K1D) mesh (the C4
+workload per GPU).  Strong (--scaling strong, BASELINE configs[4]): the
+K1D = 2048 mesh cut into N strips.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
 import time
+
+# NCCL init logs (rank count per communicator) for the driver's multi-GPU checks
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -40,17 +55,36 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--N", type=int, default=4)
-    p.add_argument("--k1d", type=int, default=1024)
+    p.add_argument("--k1d", type=int, default=None, help="default 1024 (weak), 2048 (strong)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    p.add_argument("--no-extra", action="store_true", help="skip the C3 / N=3 secondary kernel lines")
     p.add_argument("--warp", type=float, default=0.1)
     p.add_argument("--mode", choices=["fast", "parity"], default="fast")
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--ref-k1d", type=int, default=128, help="reference CPU sample size")
+    p.add_argument("--ref-k1d", type=int, default=256, help="reference CPU sample size (SURVEY §8(d))")
     # functional check of the multi-rank orchestration on a single-GPU box (no timing
     # claims): every rank on device 0, halos exchanged over gloo through host memory
     p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
     p.add_argument("--shared-device", action="store_true")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.k1d is None:
+        a.k1d = 2048 if a.scaling == "strong" else 1024
+    return a
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a torchrun environment: re-execute this script under
+    torch.distributed.run with N ranks (the driver's own launch line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -131,9 +165,35 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+def host_info() -> dict:
+    model, mem = None, None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                mem = round(int(ln.split()[1]) / 1024 ** 2, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "mem_gb": mem}
+
+
+def ref_bench(N, k1d, warmup, steps, threads, warp):
+    out = subprocess.run([REF_BENCH, str(N), str(k1d), str(warmup), str(steps), str(threads), str(warp)],
+                         capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
+    return json.loads(out)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU hot path (oracle/_ref build of the
-    unmodified headers) on this box's host cores, bounded sample of the workload."""
+    unmodified headers: rhs() + step_lsrk45, ops.threads = all host cores) on this box,
+    on a K1D = --ref-k1d sample of the workload (K1D = 256 and 512; the
+    reference's dense per-element operators need ~36 KB/elem, so K1D = 1024 does not fit
+    the host), --steps timed steps after --warmup.  Two extra legs describe the baseline:
+    K1D = 512 (2 steps) and threads = 1 (K1D = 128, 2 steps)."""
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
@@ -141,22 +201,28 @@ def run_reference(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/swedg_refbench not built "
                           "(needs /root/reference at build time)"}))
         return 0
-    out = subprocess.run([REF_BENCH, str(args.N), str(args.ref_k1d), str(max(1, min(args.warmup, 2))),
-                          str(max(1, min(args.steps, 10))), str(threads), str(args.warp)],
-                         capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
-    r = json.loads(out)
-    sample = (f"K1D={r['K1D']} (K={r['K']}) of the C4 workload, {r['steps']} LSRK45 steps after "
-              f"{r['warmup']} warm-up, reference rhs()+step_lsrk45 with ops.threads={threads}")
+    r = ref_bench(args.N, args.ref_k1d, args.warmup, args.steps, threads, args.warp)
+    legs = {}
+    if not args.no_extra:
+        for name, (k1d, th) in {"k1d512": (512, threads), "threads1_k1d128": (128, 1)}.items():
+            try:
+                x = ref_bench(args.N, k1d, 1, 2, th, args.warp)
+                legs[name] = {k: x[k] for k in ("value", "ms_per_step", "K", "K1D", "threads", "steps", "setup_s")}
+            except Exception as e:  # reported, never fatal
+                legs[name] = {"error": str(e)}
+    sample = (f"K1D={r['K1D']} (K={r['K']}) of the C4 workload (per-DOF comparison: the GPU arm runs "
+              f"K1D={args.k1d}), {r['steps']} LSRK45 steps after {r['warmup']} warm-up, unmodified reference "
+              f"rhs()+step_lsrk45 (Eigen-subset shim, -O3) with ops.threads={threads}")
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
         "steps": r["steps"], "warmup": r["warmup"], "ms_per_step": r["ms_per_step"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args, args.ref_k1d, reference=True),
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, **host_info(), "legs": legs},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -168,10 +234,17 @@ def workload_config(args, k1d, world=1, reference=False):
            "mode": "reference CPU (IEEE, reference order)" if reference else args.mode,
            "step": "one LSRK45 step = 5 RHS stages",
            "l2": "inputs larger than L2 (device-resident state+geometry >> 126 MB)"}
-    if world > 1:
-        cfg["partition"] = (f"weak scaling: {world} y-strips of a K1D x (K1D*{world}) periodic mesh on "
-                            f"[-1,1]x[-{world},{world}], {K} elements per GPU, per-stage NCCL halo "
-                            "exchange of face traces")
+    if world > 1 or (not reference and args.scaling == "strong"):
+        if args.scaling == "weak":
+            cfg["workload"] = (f"C5 weak: modal ESDG N={args.N}, {world} y-strips of K1D x K1D = {k1d}x{k1d} quads "
+                               f"({K} curved tris per GPU) of a {k1d} x {k1d * world} periodic mesh, LF, LSRK45")
+            cfg["K"] = K * world
+        else:
+            cfg["workload"] = (f"C5 strong: modal ESDG N={args.N}, K1D={k1d} (K={K} curved tris) cut into {world} "
+                               "y-strips, LF, LSRK45")
+        cfg["partition"] = (f"{world} y-strips, one per GPU; per RK stage the cut-face traces (npf nodes x 3 "
+                            "fields per face) go to the two neighbour ranks by ncclSend/ncclRecv on a comm "
+                            "stream, overlapped with the interior volume kernel, inside the captured step graph")
         cfg["parallelism"] = f"element partition x{world}"
     return cfg
 
@@ -179,34 +252,26 @@ def workload_config(args, k1d, world=1, reference=False):
 def cpu_baseline(args):
     threads = os.cpu_count() or 1
     if os.path.exists(REF_BENCH):
-        out = subprocess.run([REF_BENCH, str(args.N), str(args.ref_k1d), "1", "3", str(threads), str(args.warp)],
-                             capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
-        r = json.loads(out)
+        r = ref_bench(args.N, args.ref_k1d, 1, 3, threads, args.warp)
         return {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": f"K1D={r['K1D']} (K={r['K']}) of the C4 workload, {r['steps']} LSRK45 steps, "
-                          f"unmodified reference (oracle/_ref) with ops.threads={threads}"}
+                          f"unmodified reference (oracle/_ref) with ops.threads={threads}", **host_info()}
     # the C oracle port, single thread, on a small sample
     sys.path.insert(0, os.path.join(REPO, "tests"))
     import numpy as np
-    from oracle_py import Oracle
+    from oracle_py import Oracle, case_dict
 
     from paper_2005_02516_b200 import capi
 
     c = capi.Case("smooth", N=args.N, nx=32, warp=args.warp)
-    case = {"scheme": [0], "N": [c.N], "Np": [c.Np], "nq": [c.nq], "nf": [c.nf], "npf": [c.npf], "K": [c.K],
-            "g": [c.g], "ref_Vq": c.array("Vq"), "ref_Vf": c.array("Vf"), "ref_Pq": c.array("Pq"),
-            "ref_Qh_x": c.array("Qr"), "ref_Qh_y": c.array("Qs"), "Mh_inv": c.array("Mh_inv"),
-            "surfq_w": c.array("surfq_w"), "gf": c.array("gf"), "sJ": c.array("sJ"), "nx": c.array("nx"),
-            "ny": c.array("ny"), "nbr": c.iarray("nbr"), "perm": c.iarray("perm"), "b": c.b()}
-    case = {k: np.asarray(v) for k, v in case.items()}
-    orc = Oracle(case)
+    orc = Oracle(case_dict(c))
     u = c.u0()
     t0 = time.time()
     orc.step_lsrk45(u, np.zeros_like(u), c.dt, 2)
     sec = time.time() - t0
     val = c.K * c.Np * 3 * 10 / sec / 1e9
     return {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"K1D=32 (K={c.K}), 2 LSRK45 steps, C oracle single thread"}
+            "sample": f"K1D=32 (K={c.K}), 2 LSRK45 steps, C oracle single thread", **host_info()}
 
 
 # ---------------------------------------------------------------------------
@@ -243,6 +308,42 @@ def load_traffic():
     return {}
 
 
+SBP_FLOP_N4 = 55 * 666 + 33 * 15 + 7 * 37  # SURVEY §8(d) SBP N=4 (volume + surface + source), per element
+
+
+def secondary_rooflines(args, fp64_peak):
+    """Driver-visible fractions of the two other FP64-bound kernels:
+    C3's SBP N=4 pair kernel (dam break, K1D=128, the config's own size) and the modal
+    N=3 pair kernel (the C1/C2 degree) on the C4 generator at K1D=512."""
+    from paper_2005_02516_b200 import capi
+
+    out = {}
+    runs = [("roofline_c3", "sbp_rhs_pair_n4_kernel (C3: SBP N=4 dam break K1D=128, RHS + fused LSRK45 update)",
+             lambda: capi.Case("dambreak", scheme=capi.SCHEME_SBP, N=4, nx=128, cfl=0.0625), SBP_FLOP_N4, 60),
+            ("roofline_n3", "modal_volume_pair_n3_kernel (modal N=3, C4 generator K1D=512: projection + flux "
+             "differencing + volume lift)", lambda: capi.Case("smooth", N=3, nx=512, warp=args.warp, seed=23),
+             flops_bytes_per_element(3)["vol_flops"], 10)]
+    for key, kname, mk, flop, steps in runs:
+        try:
+            c = mk()
+            h = c.handle(mode=capi.MODE_FAST, diagnostics=False)
+            h.set_state(c.u0())
+            h.step(c.dt, 3)
+            h.enable_timers(True)
+            h.read_timers()
+            h.step(c.dt, steps, sync=True)
+            kms, kn = h.read_timers()
+            h.close()
+            tf = flop * c.K * kn[0] / (kms[0] * 1e-3) / 1e12
+            out[key] = {"kernel": kname, "bound": "fp64", "achieved": round(tf, 4), "peak": round(fp64_peak, 3),
+                        "unit": "TFLOP/s", "frac": round(tf / fp64_peak, 4), "flops_per_element": flop,
+                        "K": c.K, "avg_launch_ms": round(kms[0] / max(1, kn[0]), 4), "launches": kn[0]}
+            c.close()
+        except Exception as e:  # reported, never fatal
+            out[key] = {"error": str(e)}
+    return out
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -260,52 +361,50 @@ def run_ours(args, rank, world, local):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
-    # weak scaling: rank r owns y-strip r (K1D x K1D quads) of a global
-    # K1D x (K1D*world) periodic mesh; one halo exchange of face traces per stage
-    # (paper_2005_02516_b200/partition.py, NCCL point-to-point over NVLink).
+    red_dev = "cuda" if (dist and args.dist_backend == "nccl") else "cpu"
+
+    def allreduce(x, op):
+        if not dist:
+            return x
+        t = torch.tensor([x], device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
     t0 = time.time()
-    if world > 1:
-        case = capi.Case("smooth", N=args.N, nx=args.k1d, warp=args.warp, seed=23, strips=world, strip=rank)
+    if world > 1:  # this rank's y-strip; halo map of its two cuts (setup.cpp compact_strip)
+        case = capi.Case("smooth", N=args.N, nx=args.k1d, warp=args.warp, seed=23, strips=world, strip=rank,
+                         scaling=args.scaling)
     else:
         case = capi.Case("smooth", N=args.N, nx=args.k1d, warp=args.warp, seed=23)
     mode = capi.MODE_FAST if args.mode == "fast" else capi.MODE_PARITY
     h = case.handle(mode=mode, device=local)
     u0 = case.u0()
-    setup_s = time.time() - t0
     K, Np = case.K, case.Np
     dof = K * Np * 3
     dt = case.dt
+    comm = None
+    transport = "none (one rank)"
+    if world > 1:
+        from paper_2005_02516_b200.partition import attach_gloo, attach_nccl
+
+        halo = case.halo_desc()
+        if args.shared_device or args.dist_backend == "gloo":
+            attach_gloo(h, halo, case.nf)  # functional check only (ranks share a GPU)
+            transport = "gloo (host-staged exchange callback; functional, not a performance path)"
+        else:
+            comm = attach_nccl(h, halo, world, rank, local)
+            transport = "NCCL send/recv of packed cut-face traces (library-owned communicator)"
+        dt = allreduce(dt, dist.ReduceOp.MIN)  # the global mesh's dt (owned minimum edges)
+    dof_total = int(allreduce(float(dof), dist.ReduceOp.SUM)) if dist else dof
+    setup_s = time.time() - t0
     stream = torch.cuda.Stream(device=local)
     h.set_stream(stream.cuda_stream)
     h.set_state(u0)
-    plan = None
-    if world > 1:
-        from paper_2005_02516_b200.partition import StripHalo, stage_overlapped, trace_tensor
 
-        t = torch.tensor([dt], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        dt = float(t.item())
-        plan = StripHalo(world, rank, args.k1d, K)
-        trace = trace_tensor(h)
-        comm_stream = torch.cuda.Stream(device=local)
-
-    def steps(n, sync):
-        if plan is None:
-            h.step(dt, n, sync=sync)
-            return
-        # per stage: boundary rows' volume kernel, NCCL halo exchange on the comm stream
-        # overlapped with the interior volume kernel, then the surface kernel
-        with torch.cuda.stream(stream):
-            for _ in range(n):
-                for s_ in range(5):
-                    stage_overlapped(h, s_, dt, trace, plan, stream, comm_stream)
-        if sync:
-            h.check()
-
-    # warm-up
-    steps(args.warmup, True)
+    # warm-up (the first multi-rank call captures the step graph)
+    h.step(dt, args.warmup, sync=True)
     torch.cuda.synchronize()
-    # ---- timed region: device-resident LSRK45 steps
+    # ---- timed region: device-resident LSRK45 steps, per-kernel-class CUDA-event timers
     h.enable_timers(True)
     h.read_timers()
     launches0 = h.launches
@@ -317,7 +416,7 @@ def run_ours(args, rank, world, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks.mark_start()
     e0.record(stream)
-    steps(args.steps, False)
+    h.step(dt, args.steps, sync=False)
     e1.record(stream)
     torch.cuda.synchronize()
     clocks.mark_stop()
@@ -329,30 +428,16 @@ def run_ours(args, rank, world, local):
     kms, kn = h.read_timers()
     launches = h.launches - launches0
     h.enable_timers(False)
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = allreduce(ms, dist.ReduceOp.MAX) if dist else ms
     ms_per_step = ms / args.steps
-    value = dof * world * 5 * args.steps / (ms * 1e-3) / 1e9
+    value = dof_total * 5 * args.steps / (ms * 1e-3) / 1e9
 
     # ---- e2e through the public API with pinned host buffers
     uh_t = torch.empty((K, 3, Np), dtype=torch.float64, pin_memory=True)
     uh = uh_t.numpy()
     uh[...] = u0
     h.set_state(uh)
-    stepper = None
-    if plan is not None:
-        from paper_2005_02516_b200.partition import HostStepper
-
-        stepper = HostStepper(h, plan, stream, comm_stream)
-    # untimed warm-up of the host-state path (copy streams, events, pinned pages)
-    if plan is None:
-        h.step_host(uh, dt, 1)
-    else:
-        stepper.step(uh_t, dt, 1)
-        torch.cuda.synchronize()
-        h.check()
+    h.step_host(uh, dt, 1)  # untimed warm-up of the host-state path (copy streams, events, pinned pages)
     uh[...] = u0
     h.set_state(uh)
     torch.cuda.synchronize()
@@ -360,23 +445,15 @@ def run_ours(args, rank, world, local):
         dist.barrier()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ee0.record(stream)
-    if plan is None:
-        # swedg_step_lsrk45_host: every step reads its input state from the pinned host
-        # buffer and writes its result back (H2D + D2H of the full state per step),
-        # transfers pipelined with the compute in element chunks
-        h.step_host(uh, dt, args.e2e_steps)
-    else:
-        # per rank: H2D of the strip's state, 5 stages with halo exchanges, D2H of the
-        # result every step; chunked copies overlap the first and last stage
-        stepper.step(uh_t, dt, args.e2e_steps)
+    # swedg_step_lsrk45_host: every step reads its input state from the pinned host buffer
+    # and writes its result back (H2D + D2H of the full state per step); one rank: the
+    # transfers are pipelined with the compute in element chunks (wavefront)
+    h.step_host(uh, dt, args.e2e_steps)
     ee1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1)
-    if dist:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_val = dof * world * 5 * args.e2e_steps / (e2e_ms * 1e-3) / 1e9
+    e2e_ms = allreduce(e2e_ms, dist.ReduceOp.MAX) if dist else e2e_ms
+    e2e_val = dof_total * 5 * args.e2e_steps / (e2e_ms * 1e-3) / 1e9
     state_bytes = K * 3 * Np * 8
 
     # ---- device diagnostics (outside the timed region): one exact-sum
@@ -392,10 +469,12 @@ def run_ours(args, rank, world, local):
     inv_ms = d0.elapsed_time(d1) / 3
     inv = h.read_invariants(1)[0]
 
-    # ---- roofline of the dominant kernel (volume: projection + flux differencing)
+    # ---- roofline of the dominant kernel (volume: projection + flux differencing);
+    # with a partition each stage's volume work is 2-3 range launches: per-stage totals
     fb = flops_bytes_per_element(args.N)
-    vol_avg_ms = kms[0] / max(1, kn[0])
-    surf_avg_ms = kms[1] / max(1, kn[1])
+    nst = 5 * args.steps
+    vol_stage_ms = kms[0] / nst
+    surf_stage_ms = kms[1] / nst
     fp64_peak = capi.probe_fp64_peak(local, 5)
     hbm_peak = None
     try:
@@ -403,75 +482,89 @@ def run_ours(args, rank, world, local):
         hbm_src = "MEASURED_PEAKS.json hbm_gbs"
     except Exception:
         hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
-    vol_tflops = fb["vol_flops"] * K / (vol_avg_ms * 1e-3) / 1e12
-    surf_gbs = fb["surf_bytes"] * K / (surf_avg_ms * 1e-3) / 1e9
+    vol_tflops = fb["vol_flops"] * K / (vol_stage_ms * 1e-3) / 1e12
+    surf_gbs = fb["surf_bytes"] * K / (surf_stage_ms * 1e-3) / 1e9
     traffic = load_traffic()
+
     def _tr(name):
         t = traffic.get(name)
         return None if not t else round(t["dram_bytes_per_element"] * K)
 
-    vol_traffic = _tr("volume")
-    surf_traffic = _tr("surface")
     roofline = {
         "kernel": "modal_volume_pair_n4_kernel (FAST: entropy projection + flux differencing + volume lift)",
         "bound": "fp64", "achieved": round(vol_tflops, 4), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
-        "frac": round(vol_tflops / fp64_peak, 4), "traffic": vol_traffic,
+        "frac": round(vol_tflops / fp64_peak, 4), "traffic": _tr("volume"),
         "traffic_note": "ncu --set full dram__bytes_read+write per element (profiles/ncu_traffic.json) x K",
         "peak_source": "measured in-run: DFMA chain probe (swedg_probe_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
-        "algorithmic_flops_per_launch": fb["vol_flops"] * K, "avg_launch_ms": round(vol_avg_ms, 4),
+        "algorithmic_flops_per_launch": fb["vol_flops"] * K, "avg_launch_ms": round(vol_stage_ms, 4),
+        "launches_per_stage": round(kn[0] / nst, 2),
         "share_of_step": round(kms[0] / ms if ms > 0 else 0.0, 4),
         "flops_per_element": fb["vol_flops"],
     }
     roofline_surface = {
         "kernel": "modal_surface_kernel<4,FAST> (interface flux + LF + lift + Mh_inv + LSRK update)",
         "bound": "hbm", "achieved": round(surf_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-        "frac": round(surf_gbs / hbm_peak, 4), "traffic": surf_traffic, "peak_source": hbm_src,
-        "algorithmic_bytes_per_launch": fb["surf_bytes"] * K, "avg_launch_ms": round(surf_avg_ms, 4),
+        "frac": round(surf_gbs / hbm_peak, 4), "traffic": _tr("surface"), "peak_source": hbm_src,
+        "algorithmic_bytes_per_launch": fb["surf_bytes"] * K, "avg_launch_ms": round(surf_stage_ms, 4),
         "share_of_step": round(kms[1] / ms if ms > 0 else 0.0, 4),
     }
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline(args)
-        except Exception as e:  # reported, never fatal
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"failed: {e}"}
+    extra = {}
+    if rank == 0 and world == 1:
+        if not args.no_extra:
+            extra = secondary_rooflines(args, fp64_peak)
+        if not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(args)
+            except Exception as e:  # reported, never fatal
+                cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                       "sample": f"failed: {e}"}
 
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, args.k1d, world),
         "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": state_bytes,
-                "d2h_bytes_per_step": state_bytes,
-                "steps": args.e2e_steps,
+                "d2h_bytes_per_step": state_bytes, "steps": args.e2e_steps,
                 "path": "swedg_step_lsrk45_host: per step H2D of the state from pinned host memory + 5 "
-                        "stages + D2H of the result; 16 element chunks run through the stages as a "
-                        "wavefront so copies overlap compute (N>1: partition.HostStepper, chunked "
-                        "copies overlapping the first and last stage around the halo exchanges)"},
+                        "stages + D2H of the result" + ("; 16 element chunks run through the stages as a "
+                                                         "wavefront so copies overlap compute" if world == 1 else
+                                                         " (per rank; bytes are per rank)")},
         "gpu_launches": launches,
         "roofline": roofline,
         "roofline_surface": roofline_surface,
+        **extra,
         "cpu_baseline": cpu,
         "clocks": clk,
+        "multi_gpu": {"world": world, "transport": transport, "dof_per_rank": dof, "dof_total": dof_total,
+                      "n_halo_slots": case.n_halo, "dt": dt},
         "diagnostics": {"invariants_ms": round(inv_ms, 4), "mass": inv[1], "entropy": inv[4],
-                        "note": "device compute_invariants (exact sums, fine rule degree 2N+2) of the "
+                        "note": "device compute_invariants (exact sums, fine rule degree 2N+2) of rank 0's "
                                 "final state, outside the timed region"},
         "setup_s": round(setup_s, 2),
         "device_bytes": h.device_bytes,
     }
-    if rank == 0:
-        print(json.dumps(line))
     h.close()
+    if comm:
+        capi.nccl_comm_destroy(comm)
     if dist:
+        dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return spawn_ranks(args)
     rank, world, local = dist_env()
+    if args.impl == "ours" and "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

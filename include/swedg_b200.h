@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define SWEDG_ABI_VERSION 3
+#define SWEDG_ABI_VERSION 4
 
 /* status codes */
 #define SWEDG_OK 0
@@ -110,10 +110,38 @@ typedef struct {
     const int* perm; /* [K][nf] FaceMatch::perm[k][f][s]: neighbour surface slot (ignored on walls) */
 
     /* multi-rank (element partition): neighbour ids K..K+n_halo-1 address halo
-     * slots whose face traces the caller fills between swedg_stage_volume and
-     * swedg_stage_surface (hybridized scheme).  0 for a single rank. */
+     * slots of the face-trace buffer ([3][nf] pseudo-elements, each holding up to
+     * three received cut faces in its face positions; perm selects the position and
+     * node), filled by the per-stage exchange (swedg_set_halo).  0 for one rank. */
     int n_halo;
 } swedg_desc;
+
+/* Per-stage halo exchange of an element-partitioned mesh.  The only
+ * cross-element read of the RHS is the exterior trace (solver.hpp:263-264), so a
+ * rank sends the traces of its cut faces (3 fields x npf nodes per face) once per
+ * RK stage.  Wire format of a message of n faces: ceil(n/3) pseudo-elements of
+ * [3][nf] doubles, face i in pseudo-element i/3 at face position i%3 (so a
+ * received message lands directly in the halo slots).  Receive message m fills
+ * halo slots [sum_{q<m} ceil(recv_count[q]/3), ...).  Messages between the same
+ * two ranks pair up in issue order (the k-th send from a to b matches b's k-th
+ * receive from a). */
+typedef struct {
+    int n_send_msgs;
+    const int* send_peer;   /* [n_send_msgs] destination rank */
+    const int* send_count;  /* [n_send_msgs] faces per message */
+    const int* send_elem;   /* [sum send_count] owned element of each sent face, message-major */
+    const int* send_face;   /* [sum send_count] its local face 0..2 */
+    int n_recv_msgs;
+    const int* recv_peer;   /* [n_recv_msgs] source rank */
+    const int* recv_count;  /* [n_recv_msgs] faces per message */
+} swedg_halo_desc;
+
+/* Custom transport: called once per RK stage on the host while the stage is
+ * enqueued, after the boundary elements' traces were packed into `send` (device,
+ * the send messages back to back in wire format).  It must enqueue on `stream`
+ * (cudaStream_t) whatever fills `recv` (device, the halo slots = receive messages
+ * back to back) and return 0; the interface kernel waits on `stream`. */
+typedef int (*swedg_exchange_fn)(void* user, int stage, const double* send, double* recv, void* stream);
 
 /* ---- lifecycle ------------------------------------------------------------ */
 int swedg_create(const swedg_desc* desc, swedg_handle* out);
@@ -176,6 +204,34 @@ int swedg_stage_volume_range(swedg_handle h, int stage, double dt, int k0, int k
  * runs); the range ending at k1 == K closes the step (advances t) for stage 4. */
 int swedg_stage_surface_range(swedg_handle h, int stage, double dt, int k0, int k1);
 int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo);
+
+/* ---- multi-rank stepping ------------------------------------------------------
+ * With a halo map and a transport (NCCL communicator or exchange callback),
+ * swedg_step_lsrk45 runs every stage as: projection+volume kernel on the elements
+ * owning sent faces -> pack -> exchange on a second stream, overlapped with the
+ * interior volume kernel -> interface/update kernel after the exchange.  With NCCL
+ * the step is captured once into a CUDA graph and replayed.  Results are bitwise
+ * independent of the partition (per-element arithmetic is unchanged). */
+int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d);
+/* NCCL transport: comm is an ncclComm_t whose ranks are the peers of the halo map
+ * (libnccl.so.2 is resolved at run time: the one already loaded, e.g. by torch, or
+ * $SWEDG_NCCL_LIB).  NULL detaches. */
+int swedg_set_nccl_comm(swedg_handle h, void* comm);
+int swedg_set_exchange(swedg_handle h, swedg_exchange_fn fn, void* user);
+/* Device pointers and sizes (doubles) of the packed send messages and the halo slots. */
+int swedg_halo_buffers(swedg_handle h, double** send, size_t* n_send, double** recv, size_t* n_recv);
+/* Pack the cut-face traces of the current stage into the send buffer (stage-level
+ * API: after the volume ranges that own sent faces, before the exchange). */
+int swedg_halo_pack(swedg_handle h);
+/* The volume-kernel schedule of a multi-rank stage: ranges[2i], ranges[2i+1] = [k0, k1);
+ * the first n_boundary ranges hold every element owning a sent face, the next
+ * n_interior the rest (ranges NULL: counts only). */
+int swedg_halo_ranges(swedg_handle h, int* ranges, int max_ranges, int* n_boundary, int* n_interior);
+/* NCCL communicator helpers (so a caller without its own NCCL setup can build one):
+ * id is 128 bytes (ncclUniqueId), created on one rank and shared with the others. */
+int swedg_nccl_unique_id(void* id);
+int swedg_nccl_comm_init(int nranks, const void* id, int rank, int device, void** comm);
+int swedg_nccl_comm_destroy(void* comm);
 /* Check the device error record (syncs the stream). */
 int swedg_check(swedg_handle h);
 

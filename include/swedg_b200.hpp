@@ -267,7 +267,11 @@ auto entropy_projection(const DeviceSolverOps& ops, const StateT& state) {
 }
 
 // step_lsrk45(state, rhs, dt, res) (solver.hpp:466-484), nsteps device-resident steps.
-// The LSRK register stays on the device between calls (res of the reference).
+// Signature differs from the reference's step_lsrk45(state, rhs_fn, dt, res): the RHS
+// functor is the device ops and the LSRK register lives on the device.  It is reset
+// to zero on every call (swedg_set_state with res = NULL), which matches the
+// reference's result because Lsrk45::a[0] == 0 (solver.hpp:442): stage 0 sets
+// res = dt * du whatever res held.
 template <class StateT>
 void step_lsrk45(StateT& state, DeviceSolverOps& ops, double dt, int nsteps = 1) {
     if (!(dt > 0.0)) throw std::invalid_argument("dt must be positive");
@@ -280,6 +284,23 @@ void step_lsrk45(StateT& state, DeviceSolverOps& ops, double dt, int nsteps = 1)
     for (size_t k = 0; k < state.u.size(); ++k)
         std::memcpy(state.u[k].data(), u.data() + k * 3 * (size_t)n, sizeof(double) * 3 * n);
     state.t = t;
+}
+
+// ---- multi-rank ---------------------------------------------
+// A rank's DeviceSolverOps is built over its element partition (owned elements;
+// neighbour ids K.. address the halo slots, desc.n_halo).  Give it the exchange map
+// and a transport; step_lsrk45 then runs every stage with the cut-face exchange
+// overlapped with the interior volume kernel (swedg_b200.h, multi-rank stepping).
+inline void set_halo(DeviceSolverOps& ops, const swedg_halo_desc& d) {
+    throw_status(ops.handle(), swedg_set_halo(ops.handle(), &d));
+}
+// nccl_comm: an ncclComm_t over the ranks named in the halo map (or swedg_nccl_comm_init)
+inline void set_nccl_comm(DeviceSolverOps& ops, void* nccl_comm) {
+    throw_status(ops.handle(), swedg_set_nccl_comm(ops.handle(), nccl_comm));
+}
+// any other transport (MPI, a test's device copies): called once per stage at enqueue time
+inline void set_exchange(DeviceSolverOps& ops, swedg_exchange_fn fn, void* user) {
+    throw_status(ops.handle(), swedg_set_exchange(ops.handle(), fn, user));
 }
 
 }  // namespace swedg_b200

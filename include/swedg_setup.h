@@ -37,10 +37,16 @@ typedef struct {
     double g;        /* <= 0: the problem's default */
     unsigned seed;   /* SMOOTH: mt19937 seed of smooth_state */
     int threads;     /* host threads, <= 0: hardware concurrency */
-    int strips;      /* > 1: build only y-strip `strip` of a global nx x (ny*strips) mesh */
-    int strip;       /*      (periodic problems, hybridized): owned rows + 2 halo rows;
-                        strip == -1: the whole global strip mesh in one piece */
+    int strips;      /* P: number of y-strips of a partitioned mesh (see partition) */
+    int strip;       /* this rank's strip 0..P-1 (periodic problems, hybridized): owned
+                        rows + face halos of the two cuts (swedg_case_fill_halo);
+                        strip == -1: the whole global mesh in one piece (tests) */
+    int partition;   /* SWEDG_PARTITION_*; NONE with strips > 1 = WEAK (ABI v3 behaviour) */
 } swedg_case_config;
+
+#define SWEDG_PARTITION_NONE 0
+#define SWEDG_PARTITION_WEAK 1   /* P strips of ny rows: global nx x (ny P) mesh, domain stretched P times in y */
+#define SWEDG_PARTITION_STRONG 2 /* the problem's nx x ny mesh cut into P strips of ny/P rows */
 
 int swedg_case_build(const swedg_case_config* cfg, swedg_case* out);
 /* The problem's state, bathymetry and operators on a caller-supplied mesh (the
@@ -57,6 +63,9 @@ const char* swedg_case_error(void);
 /* Fill every operator/geometry/connectivity pointer and size of *d (penalty,
  * mode and device are left for the caller). */
 int swedg_case_fill_desc(swedg_case c, swedg_desc* d);
+/* Halo exchange map of a strip case (pointers into the case; n_send_msgs = 0 when
+ * the case is not partitioned). */
+int swedg_case_fill_halo(swedg_case c, swedg_halo_desc* d);
 /* Named host arrays: "u0" [K][3][n], "b" [K][n], "xy_vol" [K][2][nq], "map_coeffs" [K][2][Np],
  * "map_nodes" [K][2][Np], "J_vol" [K][nq], "volq_w" [nq], "Vq" ..., "fine_w/V/Vr/Vs" (FineQuad),
  * "lattice_V" (basis at the mapping lattice, Np x Np); returns element count via *n. */

@@ -71,8 +71,17 @@ class _Desc(C.Structure):
     ]
 
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 _lib = None
+
+
+class _HaloDesc(C.Structure):
+    _fields_ = [("n_send_msgs", C.c_int), ("send_peer", _ip), ("send_count", _ip), ("send_elem", _ip),
+                ("send_face", _ip), ("n_recv_msgs", C.c_int), ("recv_peer", _ip), ("recv_count", _ip)]
+
+
+# swedg_exchange_fn: int (*)(void* user, int stage, const double* send, double* recv, void* stream)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 
 
 class _DiagDesc(C.Structure):
@@ -140,6 +149,15 @@ def lib() -> C.CDLL:
     L.swedg_step_lsrk45_host.argtypes = [vp, _dp, C.c_double, C.c_int, C.c_int]
     L.swedg_ratio_kernels.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.c_int,
                                       _dp, _dp, _dp]
+    L.swedg_set_halo.argtypes = [vp, C.POINTER(_HaloDesc)]
+    L.swedg_set_nccl_comm.argtypes = [vp, vp]
+    L.swedg_set_exchange.argtypes = [vp, EXCHANGE_FN, vp]
+    L.swedg_halo_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_size_t), C.POINTER(vp), C.POINTER(C.c_size_t)]
+    L.swedg_halo_pack.argtypes = [vp]
+    L.swedg_halo_ranges.argtypes = [vp, _ip, C.c_int, _ip, _ip]
+    L.swedg_nccl_unique_id.argtypes = [vp]
+    L.swedg_nccl_comm_init.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
+    L.swedg_nccl_comm_destroy.argtypes = [vp]
     _lib = L
     return L
 
@@ -156,6 +174,8 @@ EXPORTED = [
     "swedg_diag_raw", "swedg_diag_from_raw", "swedg_sample_invariants", "swedg_read_invariants",
     "swedg_read_invariants_raw", "swedg_run", "swedg_exact_sum", "swedg_ratio_kernels",
     "swedg_step_lsrk45_host", "swedg_stage_volume_range", "swedg_stage_surface_range",
+    "swedg_set_halo", "swedg_set_nccl_comm", "swedg_set_exchange", "swedg_halo_buffers", "swedg_halo_pack",
+    "swedg_halo_ranges", "swedg_nccl_unique_id", "swedg_nccl_comm_init", "swedg_nccl_comm_destroy",
 ]
 
 
@@ -333,6 +353,62 @@ class Handle:
         self._check(self._lib.swedg_trace_device_ptr(self._h, C.byref(p), C.byref(a), C.byref(b)))
         return p.value, a.value, b.value
 
+    # -- multi-rank halo exchange (swedg_set_halo) -------------------------------
+    def set_halo(self, halo: dict):
+        """halo: send_peer, send_count, send_elem, send_face, recv_peer, recv_count (int arrays;
+        Case.halo_desc())."""
+        a = {k: _i32(halo[k]) for k in ("send_peer", "send_count", "send_elem", "send_face", "recv_peer",
+                                        "recv_count")}
+        d = _HaloDesc()
+        d.n_send_msgs, d.n_recv_msgs = len(a["send_peer"]), len(a["recv_peer"])
+        for k, v in a.items():
+            setattr(d, k, _pi(v))
+        self._halo_keep = a
+        self._check(self._lib.swedg_set_halo(self._h, C.byref(d)))
+
+    def set_nccl_comm(self, comm: int | None):
+        self._check(self._lib.swedg_set_nccl_comm(self._h, C.c_void_p(comm) if comm else None))
+
+    def set_exchange(self, fn):
+        """fn(stage, send_ptr, recv_ptr, stream_ptr) -> None, called at enqueue time on the
+        host; it must enqueue on `stream_ptr` what fills recv (None detaches)."""
+        if fn is None:
+            self._xfn = None
+            self._check(self._lib.swedg_set_exchange(self._h, EXCHANGE_FN(), None))
+            return
+
+        def tramp(user, stage, send, recv, stream):
+            try:
+                fn(stage, send, recv, stream)
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a failed exchange
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._xfn = EXCHANGE_FN(tramp)
+        self._check(self._lib.swedg_set_exchange(self._h, self._xfn, None))
+
+    def halo_buffers(self):
+        """(send_ptr, n_send_doubles, recv_ptr, n_recv_doubles) device buffers."""
+        sp, rp = C.c_void_p(), C.c_void_p()
+        ns, nr = C.c_size_t(), C.c_size_t()
+        self._check(self._lib.swedg_halo_buffers(self._h, C.byref(sp), C.byref(ns), C.byref(rp), C.byref(nr)))
+        return sp.value, ns.value, rp.value, nr.value
+
+    def halo_pack(self):
+        self._check(self._lib.swedg_halo_pack(self._h))
+
+    def halo_ranges(self):
+        """(boundary ranges, interior ranges) of the multi-rank volume schedule."""
+        nb, ni = C.c_int(), C.c_int()
+        self._check(self._lib.swedg_halo_ranges(self._h, None, 0, C.byref(nb), C.byref(ni)))
+        buf = np.zeros(2 * (nb.value + ni.value), dtype=np.int32)
+        self._check(self._lib.swedg_halo_ranges(self._h, _pi(buf), nb.value + ni.value, None, None))
+        r = [tuple(int(x) for x in buf[2 * i:2 * i + 2]) for i in range(nb.value + ni.value)]
+        return r[:nb.value], r[nb.value:]
+
     def enable_timers(self, on: bool = True):
         self._check(self._lib.swedg_enable_timers(self._h, 1 if on else 0))
 
@@ -449,6 +525,28 @@ def probe_fp64_peak(device: int = 0, reps: int = 5) -> float:
     return t.value
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().swedg_nccl_unique_id(buf)
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, "swedg_nccl_unique_id: " + lib().swedg_create_error().decode())
+    return buf.raw
+
+
+def nccl_comm_init(nranks: int, uid: bytes, rank: int, device: int) -> int:
+    """A library-owned NCCL communicator (ncclComm_t as int) for the halo exchange."""
+    buf = C.create_string_buffer(uid, 128)
+    comm = C.c_void_p()
+    rc = lib().swedg_nccl_comm_init(int(nranks), buf, int(rank), int(device), C.byref(comm))
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, "swedg_nccl_comm_init: " + lib().swedg_create_error().decode())
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    lib().swedg_nccl_comm_destroy(C.c_void_p(comm))
+
+
 def diag_raw_bytes() -> int:
     return int(lib().swedg_diag_raw_bytes())
 
@@ -538,7 +636,13 @@ PROBLEMS = {"lake": PROBLEM_LAKE, "vortex": PROBLEM_VORTEX, "dambreak": PROBLEM_
 class _CaseCfg(C.Structure):
     _fields_ = [("problem", C.c_int), ("scheme", C.c_int), ("N", C.c_int), ("nx", C.c_int),
                 ("ny", C.c_int), ("warp", C.c_double), ("cfl", C.c_double), ("g", C.c_double),
-                ("seed", C.c_uint), ("threads", C.c_int), ("strips", C.c_int), ("strip", C.c_int)]
+                ("seed", C.c_uint), ("threads", C.c_int), ("strips", C.c_int), ("strip", C.c_int),
+                ("partition", C.c_int)]
+
+
+PARTITION_NONE = 0
+PARTITION_WEAK = 1
+PARTITION_STRONG = 2
 
 
 def _setup_lib():
@@ -568,10 +672,13 @@ class Case:
     """A problem built by the native setup (lake / vortex / dambreak / smooth)."""
 
     def __init__(self, problem="smooth", *, scheme=SCHEME_HYBRIDIZED, N=4, nx=16, ny=None,
-                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0, mesh=None):
-        """strips > 1: rank `strip`'s y-strip of a global nx x (ny*strips) periodic mesh on
-        [-Lx/2,Lx/2] x [-strips*Ly/2, strips*Ly/2] (weak scaling); its 2 halo rows follow the
-        K owned elements (below: slots K..K+2nx, above: K+2nx..K+4nx).
+                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0, scaling=None, mesh=None):
+        """Partitioned meshes: rank `strip`'s y-strip of P = strips, with face halos of the two
+        cuts (halo_desc()).  scaling "weak": P strips of ny rows of a global nx x (ny P) mesh on
+        the problem's domain stretched P times in y (fixed work per rank; the default when
+        strips > 1); "strong": the problem's nx x ny mesh cut into P strips of ny/P rows
+        (strips = 1 with scaling "strong": one rank whose halos are its own periodic cut).
+        strip = -1: the whole global mesh in one piece.
         mesh: a caller-supplied mesh instead (dict with verts [nv][2], tris [ne][3],
         wall_faces [nw][2], domain (xc, yc, Lx, Ly), periodic_x, periodic_y; e.g. from
         io.read_mesh_text) — swedg_case_build_mesh."""
@@ -581,6 +688,7 @@ class Case:
         cfg.scheme, cfg.N, cfg.nx, cfg.ny = scheme, N, nx, ny if ny is not None else nx
         cfg.warp, cfg.cfl, cfg.g, cfg.seed, cfg.threads = warp, cfl, g, seed, threads
         cfg.strips, cfg.strip = strips, strip
+        cfg.partition = {None: PARTITION_NONE, "weak": PARTITION_WEAK, "strong": PARTITION_STRONG}[scaling]
         h = C.c_void_p()
         if mesh is None:
             rc = L.swedg_case_build(C.byref(cfg), C.byref(h))
@@ -622,11 +730,27 @@ class Case:
             raise KeyError(name)
         return np.ctypeslib.as_array(p, shape=(n.value,)).copy() if n.value else np.zeros(0, np.int32)
 
+    def view(self, name: str, integer: bool = False) -> np.ndarray:
+        """Zero-copy view of a named case array (valid while the case is alive)."""
+        n = C.c_size_t()
+        f = self._lib.swedg_case_iarray if integer else self._lib.swedg_case_array
+        p = f(self._c, name.encode(), C.byref(n))
+        if not p:
+            raise KeyError(name)
+        return np.ctypeslib.as_array(p, shape=(n.value,))
+
     def u0(self) -> np.ndarray:
         return self.array("u0").reshape(self.K, 3, self.nstate)
 
     def b(self) -> np.ndarray:
         return self.array("b").reshape(self.K, self.nstate)
+
+    def halo_desc(self) -> dict | None:
+        """The halo exchange map of a partitioned case (swedg_case_fill_halo), else None."""
+        if self.n_halo == 0:
+            return None
+        return {k: self.iarray("halo_" + k) for k in ("send_peer", "send_count", "send_elem", "send_face",
+                                                     "recv_peer", "recv_count")}
 
     def handle(self, *, penalty=PENALTY_LF, mode=MODE_FAST, device=0, set_bathymetry=True,
                diagnostics=True) -> "Handle":
@@ -634,6 +758,9 @@ class Case:
                              b=self.b() if set_bathymetry else None)
         if diagnostics:
             h.set_diagnostics(**self.diag_arrays())
+        halo = self.halo_desc()
+        if halo is not None:
+            h.set_halo(halo)
         return h
 
     def diag_arrays(self) -> dict:

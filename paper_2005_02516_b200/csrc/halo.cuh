@@ -1,0 +1,88 @@
+// Halo exchange of an element-partitioned mesh: the cut-face pack
+// kernel and the run-time binding of NCCL's point-to-point API.
+//
+// The RHS reads across elements only through the exterior trace
+// (solver.hpp:263-264: proj[nbr](nq + perm)), so once per RK stage a rank ships
+// the projected traces of its cut faces: 3 fields x npf nodes per face.  The wire
+// format packs three faces per [3][nf] pseudo-element (face i of a message at
+// pseudo-element i/3, face position i%3), which is exactly the layout of the
+// receiver's halo slots in the trace buffer — a received message needs no unpack.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+namespace swedg {
+
+// One thread per (sent face, field, node): buf[dst + c nf + s] = trace[src + c nf + s]
+// with src = (e 3 + 0) nf + f npf and dst the face's wire position.
+struct HaloPackParams {
+    const double* trace;
+    const long long* src;  // [n] trace offset of face (e, f), field 0, node 0
+    const long long* dst;  // [n] send-buffer offset of the face, field 0, node 0
+    double* buf;
+    int n, nf, npf;
+};
+
+__global__ void halo_pack_kernel(HaloPackParams p) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int per = 3 * p.npf;
+    if (i >= (long long)p.n * per) return;
+    const int face = (int)(i / per), r = (int)(i - (long long)face * per);
+    const int c = r / p.npf, s = r - c * p.npf;
+    p.buf[p.dst[face] + c * p.nf + s] = p.trace[p.src[face] + c * p.nf + s];
+}
+
+// ---- NCCL, resolved at run time ---------------------------------------------
+// The library does not link libnccl: it binds the symbols of the libnccl.so.2 the
+// process already has (torch's, when called from Python) or loads it, so the
+// communicator a caller passes and the calls made here come from one NCCL.
+struct NcclUid {
+    char internal[128];
+};
+struct NcclApi {
+    int (*GetUniqueId)(NcclUid*) = nullptr;
+    int (*CommInitRank)(void**, int, NcclUid, int) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+    bool ok = false;
+    std::string error;
+};
+constexpr int kNcclFloat64 = 8;  // ncclDataType_t ncclFloat64 (nccl.h)
+
+inline NcclApi& nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* env = std::getenv("SWEDG_NCCL_LIB");
+        void* lib = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            api.error = std::string("cannot load NCCL: ") + dlerror();
+            return;
+        }
+        auto sym = [&](const char* n) { return dlsym(lib, n); };
+        api.GetUniqueId = reinterpret_cast<int (*)(NcclUid*)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<int (*)(void**, int, NcclUid, int)>(sym("ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<int (*)(void*)>(sym("ncclCommDestroy"));
+        api.Send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(sym("ncclRecv"));
+        api.GroupStart = reinterpret_cast<int (*)()>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<int (*)()>(sym("ncclGroupEnd"));
+        api.GetErrorString = reinterpret_cast<const char* (*)(int)>(sym("ncclGetErrorString"));
+        api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+                 api.GroupEnd && api.GetErrorString;
+        if (!api.ok) api.error = "libnccl.so.2 lacks the point-to-point API";
+    });
+    return api;
+}
+
+}  // namespace swedg

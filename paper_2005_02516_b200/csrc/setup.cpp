@@ -828,6 +828,8 @@ struct swedg_case_s {
     bool ext = false;
     Mesh ext_mesh;
     int n_halo = 0;
+    // y-strip partition: halo exchange map (swedg_halo_desc)
+    std::vector<int> halo_send_peer, halo_send_count, halo_send_elem, halo_send_face, halo_recv_peer, halo_recv_count;
 };
 
 namespace {
@@ -967,18 +969,53 @@ Cons vortex_exact(double x, double y, double t, double g) {
 
 double lake_bathymetry(double x, double) { return 0.1 * std::sin(2.0 * M_PI * x) * std::cos(2.0 * M_PI * x) + 0.5; }
 
-// Keep the owned rows of a strip (local rows 1..ny) as elements 0..K-1 and turn
-// the two halo rows into halo slots: below row -> K + [0, 2nx), above row ->
-// K + 2nx + [0, 2nx).  Per-element arrays shrink to the owned elements.
-void compact_strip(swedg_case_s& c) {
+// y-strip partition.  The mesh holds quad rows [j0-1, j1+1) of the
+// global grid: owned rows j0..j1-1 plus one halo row on each side (periodic images
+// at the wrap).  Keep the owned elements as 0..K-1 and replace the halo rows by
+// FACE halos: only the traces of the cut faces cross ranks (npf nodes x 3 fields per
+// face, solver.hpp:263-264).  Halo slots are pseudo-elements of the trace buffer
+// ([3][nf] each) that hold three received cut faces in their face positions 0, 1, 2,
+// so the interface kernel reads them like any neighbour trace.
+//   receive message 0 (from prev, the row below): pseudo-elements [0, ceil(nb/3))
+//   receive message 1 (from next, the row above): the next ceil(na/3)
+// Cut faces are ordered by the halo element's index in its row (= the sender's
+// element order in its own boundary row), so the sender packs its message in
+// element order: send message 0 (to next) = owned faces on the upper cut, send
+// message 1 (to prev) = owned faces on the lower cut.  Messages between the same
+// two ranks pair up in issue order (P = 2: both neighbours are one rank).
+void compact_strip(swedg_case_s& c, int P, int r) {
     const long row = 2L * c.cfg.nx;
     const long K_all = c.K, K_own = K_all - 2 * row;
-    auto new_id = [&](long id) -> long {
-        const long r = id / row, t = id - r * row;
-        if (r == 0) return K_own + t;
-        if (id >= K_all - row) return K_own + row + t;
-        return id - row;
+    const int npf = c.npf, nf = c.nf;
+    struct Cut {
+        long t;  // halo element index within its row
+        long e;  // owned element (new id)
+        int f;
     };
+    std::vector<Cut> below, above;
+    for (long e = row; e < K_all - row; ++e)
+        for (int f = 0; f < 3; ++f) {
+            const long n = c.nbr[e * 3 + f];
+            if (n < 0) continue;
+            if (n < row) below.push_back({n, e - row, f});
+            else if (n >= K_all - row) above.push_back({n - (K_all - row), e - row, f});
+        }
+    auto by_t = [](const Cut& a, const Cut& b) { return a.t < b.t; };
+    std::sort(below.begin(), below.end(), by_t);
+    std::sort(above.begin(), above.end(), by_t);
+    for (size_t i = 1; i < below.size(); ++i)
+        if (below[i].t == below[i - 1].t) throw std::runtime_error("halo element with two cut faces");
+    for (size_t i = 1; i < above.size(); ++i)
+        if (above[i].t == above[i - 1].t) throw std::runtime_error("halo element with two cut faces");
+    // owned minimum edge only (the periodic image rows are warped as if they were
+    // inside the domain; their edges are not mesh edges)
+    {
+        Mesh own;
+        own.verts = c.mesh.verts;
+        own.tris.assign(c.mesh.tris.begin() + row, c.mesh.tris.end() - row);
+        c.min_edge = min_edge_length(own);
+        c.dt = c.cfg.cfl * c.min_edge / (0.5 * (c.cfg.N + 1) * (c.cfg.N + 2));
+    }
     auto shrink = [&](std::vector<double>& v) {
         if (v.empty()) return;
         const size_t per = v.size() / (size_t)K_all;
@@ -998,9 +1035,41 @@ void compact_strip(swedg_case_s& c) {
     shrink_i(c.perm);
     shrink_i(c.nbr);
     for (auto& n : c.nbr)
-        if (n >= 0) n = (int)new_id(n);
+        if (n >= 0) n = (int)(n - row);  // owned neighbours; cut faces are rewritten below
+    const int nb_slots = (int)((below.size() + 2) / 3), na_slots = (int)((above.size() + 2) / 3);
+    auto point = [&](const std::vector<Cut>& cuts, int base) {
+        for (size_t j = 0; j < cuts.size(); ++j) {
+            const Cut& x = cuts[j];
+            c.nbr[x.e * 3 + x.f] = (int)(K_own + base + (long)j / 3);
+            for (int s = 0; s < npf; ++s) {
+                int& p = c.perm[(size_t)x.e * nf + x.f * npf + s];
+                p = (int)(j % 3) * npf + p % npf;  // neighbour face node -> position in the pseudo-element
+            }
+        }
+    };
+    point(below, 0);
+    point(above, nb_slots);
     c.K = K_own;
-    c.n_halo = (int)(2 * row);
+    c.n_halo = nb_slots + na_slots;
+    // the owned faces on each cut, in the neighbour's receive order (element order)
+    std::vector<Cut> up, down;  // owned side of the upper / lower cut
+    for (const auto& x : above) up.push_back({x.e, x.e, x.f});
+    for (const auto& x : below) down.push_back({x.e, x.e, x.f});
+    auto by_e = [](const Cut& a, const Cut& b) { return a.e < b.e || (a.e == b.e && a.f < b.f); };
+    std::sort(up.begin(), up.end(), by_e);
+    std::sort(down.begin(), down.end(), by_e);
+    const int next = (r + 1) % P, prev = (r + P - 1) % P;
+    c.halo_send_peer = {next, prev};
+    c.halo_send_count = {(int)up.size(), (int)down.size()};
+    c.halo_send_elem.clear();
+    c.halo_send_face.clear();
+    for (const auto* v : {&up, &down})
+        for (const auto& x : *v) {
+            c.halo_send_elem.push_back((int)x.e);
+            c.halo_send_face.push_back(x.f);
+        }
+    c.halo_recv_peer = {prev, next};
+    c.halo_recv_count = {(int)below.size(), (int)above.size()};
 }
 
 void build_case(swedg_case_s& c) {
@@ -1042,22 +1111,40 @@ void build_case(swedg_case_s& c) {
             throw std::invalid_argument("unknown problem");
     }
     const bool dam = cfg.problem == SWEDG_PROBLEM_DAMBREAK;
+    // partition: 0 none; strips > 1 alone = weak strips (backward compatible);
+    // SWEDG_PARTITION_WEAK / _STRONG build strip `strip` of P = max(strips, 1)
+    const int part = cfg.partition != SWEDG_PARTITION_NONE ? cfg.partition
+                                                           : (cfg.strips > 1 ? SWEDG_PARTITION_WEAK : SWEDG_PARTITION_NONE);
     const int P = cfg.strips > 1 ? cfg.strips : 1;
+    if (part != SWEDG_PARTITION_NONE && part != SWEDG_PARTITION_WEAK && part != SWEDG_PARTITION_STRONG)
+        throw std::invalid_argument("unknown partition mode");
     if (!c.ext) c.periodic_x = c.periodic_y = !dam;
     if (c.ext) {  // read_mesh_text-style input: straight-sided, caller's walls and periodicity
-        if (P > 1) throw std::invalid_argument("strip partitions need the structured mesh");
+        if (part != SWEDG_PARTITION_NONE) throw std::invalid_argument("strip partitions need the structured mesh");
         c.mesh = c.ext_mesh;
-    } else if (P > 1 && cfg.strip == -1) {  // the whole global strip mesh in one piece (reference for tests)
+    } else if (part != SWEDG_PARTITION_NONE && cfg.strip == -1) {  // the whole global mesh in one piece (tests)
         if (dam) throw std::invalid_argument("strip partitions need a periodic problem");
-        dom.Ly *= P;
-        c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny * P, dom, false);
-    } else if (P > 1) {
+        if (part == SWEDG_PARTITION_WEAK) dom.Ly *= P;
+        c.mesh = uniform_tri_mesh(cfg.nx, part == SWEDG_PARTITION_WEAK ? cfg.ny * P : cfg.ny, dom, false);
+    } else if (part != SWEDG_PARTITION_NONE) {
         if (dam || cfg.scheme != SWEDG_SCHEME_HYBRIDIZED)
             throw std::invalid_argument("strip partitions need a periodic problem and the hybridized scheme");
         if (cfg.strip < 0 || cfg.strip >= P) throw std::invalid_argument("strip index out of range");
-        dom.Ly *= P;  // global domain; strip rows are the owned part of it
+        // weak: P strips of ny rows on a domain stretched P times in y (fixed work per rank);
+        // strong: the problem's nx x ny mesh cut into P strips of ny/P rows (+-1)
+        int ny_tot = cfg.ny, j0, j1;
+        if (part == SWEDG_PARTITION_WEAK) {
+            dom.Ly *= P;
+            ny_tot = cfg.ny * P;
+            j0 = cfg.strip * cfg.ny;
+            j1 = j0 + cfg.ny;
+        } else {
+            j0 = (int)((long)cfg.ny * cfg.strip / P);
+            j1 = (int)((long)cfg.ny * (cfg.strip + 1) / P);
+        }
+        if (j1 <= j0) throw std::invalid_argument("strip owns no mesh row (ny < strips)");
         c.periodic_y = false;
-        c.mesh = uniform_tri_mesh_rows(cfg.nx, cfg.strip * cfg.ny - 1, (cfg.strip + 1) * cfg.ny + 1, cfg.ny * P, dom);
+        c.mesh = uniform_tri_mesh_rows(cfg.nx, j0 - 1, j1 + 1, ny_tot, dom);
     } else {
         c.mesh = uniform_tri_mesh(cfg.nx, cfg.ny, dom, dam);
     }
@@ -1205,7 +1292,7 @@ void build_case(swedg_case_s& c) {
                 for (int i = 0; i < nq; ++i) uk[i] = h;
         }
     }
-    if (P > 1 && cfg.strip >= 0) compact_strip(c);
+    if (part != SWEDG_PARTITION_NONE && cfg.strip >= 0) compact_strip(c, P, cfg.strip);
 }
 
 }  // namespace
@@ -1267,6 +1354,21 @@ int swedg_case_fill_desc(swedg_case c, swedg_desc* d) {
     d->nbr = c->nbr.data();
     d->perm = c->perm.data();
     d->n_halo = c->n_halo;
+    return SWEDG_OK;
+}
+
+int swedg_case_fill_halo(swedg_case c, swedg_halo_desc* d) {
+    if (!c || !d) return SWEDG_ERR_INVALID;
+    *d = swedg_halo_desc{};
+    if (c->halo_send_peer.empty()) return SWEDG_OK;
+    d->n_send_msgs = (int)c->halo_send_peer.size();
+    d->send_peer = c->halo_send_peer.data();
+    d->send_count = c->halo_send_count.data();
+    d->send_elem = c->halo_send_elem.data();
+    d->send_face = c->halo_send_face.data();
+    d->n_recv_msgs = (int)c->halo_recv_peer.size();
+    d->recv_peer = c->halo_recv_peer.data();
+    d->recv_count = c->halo_recv_count.data();
     return SWEDG_OK;
 }
 
@@ -1360,6 +1462,12 @@ const int* swedg_case_iarray(swedg_case c, const char* name, size_t* n) {
     else if (s == "face_type") v = &c->face_type;
     else if (s == "perm") v = &c->perm;
     else if (s == "face_index") v = &c->face_index;
+    else if (s == "halo_send_peer") v = &c->halo_send_peer;
+    else if (s == "halo_send_count") v = &c->halo_send_count;
+    else if (s == "halo_send_elem") v = &c->halo_send_elem;
+    else if (s == "halo_send_face") v = &c->halo_send_face;
+    else if (s == "halo_recv_peer") v = &c->halo_recv_peer;
+    else if (s == "halo_recv_count") v = &c->halo_recv_count;
     if (!v) return nullptr;
     if (n) *n = v->size();
     return v->data();

@@ -28,6 +28,7 @@
 #include "sbp_pair_n4.cuh"
 #include "diag_kernels.cuh"
 #include "ratio_kernels.cuh"
+#include "halo.cuh"
 
 using namespace swedg;
 
@@ -46,6 +47,7 @@ struct swedg_handle_s {
     int scheme, penalty, mode, N, Np, nq, nf, npf, nh, K;
     int n_halo = 0;           // halo element slots after the K owned elements (multi-rank)
     unsigned stage_cur = 0;   // stage id of the open stage-level call (swedg_stage_*)
+    int stage_open = -1;      // RK stage index (0..4) the stage-level calls are filling, -1: none
     double g;
     int device;
     int nsm = 148;
@@ -133,6 +135,21 @@ struct swedg_handle_s {
     // stage time of every stage id issued since the last error check (error decoding)
     unsigned stage_t0 = 0;
     std::vector<double> stage_t;
+    // multi-rank halo exchange (swedg_set_halo, halo.cuh)
+    bool halo_set = false;
+    std::vector<int> send_peer, recv_peer;
+    std::vector<size_t> send_off, send_len, recv_off, recv_len;  // doubles, wire format
+    int n_send_faces = 0;
+    long long* pack_src = nullptr;  // [n_send_faces]
+    long long* pack_dst = nullptr;
+    double* sendbuf = nullptr;
+    size_t send_doubles = 0;
+    std::vector<std::pair<int, int>> bnd_ranges, int_ranges;  // volume ranges: owning sent faces / the rest
+    void* nccl = nullptr;
+    swedg_exchange_fn xfn = nullptr;
+    void* xuser = nullptr;
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
     int nstate() const { return scheme == SWEDG_SCHEME_SBP ? nq : Np; }
 };
 
@@ -591,7 +608,66 @@ bool sbp_pair_path(swedg_handle h) {
     return h->scheme == SWEDG_SCHEME_SBP && h->mode == SWEDG_MODE_FAST && h->N == 4 && h->vol_variant == 0;
 }
 
+bool halo_active(swedg_handle h) { return h->halo_set && (h->nccl || h->xfn); }
+
+// Pack the cut-face traces (halo.cuh) on stream st.
+int halo_pack_on(swedg_handle h, cudaStream_t st) {
+    if (h->n_send_faces == 0) return SWEDG_OK;
+    HaloPackParams p{h->trace, h->pack_src, h->pack_dst, h->sendbuf, h->n_send_faces, h->nf, h->npf};
+    const long long n = (long long)h->n_send_faces * 3 * h->npf;
+    halo_pack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p);
+    h->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("halo pack: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+// One stage's exchange on the comm stream: pack, then NCCL send/recv or the caller's transport.
+int halo_exchange(swedg_handle h, int stage) {
+    if (halo_pack_on(h, h->comm)) return h->last_code;
+    double* recv = h->trace + (size_t)h->K * 3 * h->nf;
+    if (h->nccl) {
+        NcclApi& api = nccl_api();
+        int rc = api.GroupStart();
+        for (size_t m = 0; m < h->send_peer.size() && rc == 0; ++m)
+            rc = api.Send(h->sendbuf + h->send_off[m], h->send_len[m], kNcclFloat64, h->send_peer[m], h->nccl, h->comm);
+        for (size_t m = 0; m < h->recv_peer.size() && rc == 0; ++m)
+            rc = api.Recv(recv + h->recv_off[m], h->recv_len[m], kNcclFloat64, h->recv_peer[m], h->nccl, h->comm);
+        const int rc2 = api.GroupEnd();
+        if (rc == 0) rc = rc2;
+        if (rc != 0) return fail(h, SWEDG_ERR_CUDA, std::string("NCCL halo exchange: ") + api.GetErrorString(rc));
+        return SWEDG_OK;
+    }
+    if (h->xfn(h->xuser, stage, h->sendbuf, recv, static_cast<void*>(h->comm)) != 0)
+        return fail(h, SWEDG_ERR_CUDA, "halo exchange callback failed in stage " + std::to_string(stage));
+    return SWEDG_OK;
+}
+
+// Multi-rank stage schedule: boundary volume -> pack + exchange on the comm stream,
+// overlapped with the interior volume kernel -> interface/update kernel.
+int run_step_halo(swedg_handle h, const unsigned* ids, double dt) {
+    for (int s = 0; s < 5; ++s) {
+        for (const auto& r : h->bnd_ranges) {
+            StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
+            if (run_stage(h, sa)) return h->last_code;
+        }
+        CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
+        if (halo_exchange(h, s)) return h->last_code;
+        CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+        for (const auto& r : h->int_ranges) {
+            StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
+            if (run_stage(h, sa)) return h->last_code;
+        }
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+        StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
+        if (run_stage(h, ss)) return h->last_code;
+    }
+    return SWEDG_OK;
+}
+
 int run_step(swedg_handle h, const unsigned* ids, double dt) {
+    if (halo_active(h)) return run_step_halo(h, ids, dt);
     if (sbp_pair_path(h)) {
         // every stage fuses the RK update, writing the next state into another buffer
         // (neighbours read the stage's input): u -> A -> B -> A -> B -> u, so the step
@@ -1021,7 +1097,8 @@ int swedg_destroy(swedg_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
-                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2, h->u_alt, h->u_alt2};
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2, h->u_alt, h->u_alt2,
+                    h->pack_src, h->pack_dst, h->sendbuf};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& p : h->ev_pending) {
@@ -1036,6 +1113,9 @@ int swedg_destroy(swedg_handle h) {
     if (h->ev_step) cudaEventDestroy(h->ev_step);
     if (h->cp_in) cudaStreamDestroy(h->cp_in);
     if (h->cp_out) cudaStreamDestroy(h->cp_out);
+    if (h->comm) cudaStreamDestroy(h->comm);
+    if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
+    if (h->ev_halo) cudaEventDestroy(h->ev_halo);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return SWEDG_OK;
@@ -1318,7 +1398,12 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
     cudaSetDevice(h->device);
     // launch-bound regime (small K): replay a captured one-step graph; per-kernel
     // timers need individual launches, so they disable the graph path
-    const bool graphs = h->use_graphs && !h->timers && nsteps >= 2;
+    if (h->n_halo > 0 && !halo_active(h))
+        return fail(h, SWEDG_ERR_INVALID,
+                    "multi-rank handle: set a halo map and a transport (swedg_set_halo + swedg_set_nccl_comm / "
+                    "swedg_set_exchange) or use the stage-level API");
+    // a caller's exchange callback may not be capturable: individual launches then
+    const bool graphs = h->use_graphs && !h->timers && nsteps >= 2 && !(halo_active(h) && h->xfn);
     if (graphs) {
         if (capture_step_graph(h, dt)) return h->last_code;
         // replay n, stage s reports id (first id of this call) + 5 n + s
@@ -1354,14 +1439,28 @@ int swedg_set_graphs(swedg_handle h, int on) {
     return SWEDG_OK;
 }
 
+// Stage-level calls fill one RK stage at a time: the first volume call of a stage
+// index opens a new stage id (error records carry it), the surface call that reaches
+// the end of the mesh closes it.  Volume ranges of one stage may come in any order.
+namespace {
+unsigned stage_id_for(swedg_handle h, int stage, double dt) {
+    if (h->stage_open != stage) {
+        h->stage_cur = new_stage(h, h->t + Lsrk45::c[stage] * dt);
+        h->stage_open = stage;
+    }
+    return h->stage_cur;
+}
+}  // namespace
+
 int swedg_stage_volume(swedg_handle h, int stage, double dt) {
     if (!h || stage < 0 || stage > 4) return SWEDG_ERR_INVALID;
     if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
     if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
         return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
     cudaSetDevice(h->device);
-    h->stage_cur = new_stage(h, h->t + Lsrk45::c[stage] * dt);
-    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true};
+    h->stage_open = -1;  // a whole-mesh volume call always starts a new stage
+    const unsigned id = stage_id_for(h, stage, dt);
+    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, id, true};
     return run_stage(h, sa);
 }
 
@@ -1371,9 +1470,9 @@ int swedg_stage_volume_range(swedg_handle h, int stage, double dt, int k0, int k
     if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
         return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
     cudaSetDevice(h->device);
-    if (k0 == 0) h->stage_cur = new_stage(h, h->t + Lsrk45::c[stage] * dt);  // first range opens the stage
+    const unsigned id = stage_id_for(h, stage, dt);
     if (k1 == k0) return SWEDG_OK;
-    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true, k0, k1};
+    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, id, true, k0, k1};
     return run_stage(h, sa);
 }
 
@@ -1381,8 +1480,10 @@ int swedg_stage_surface(swedg_handle h, int stage, double dt) {
     if (!h || stage < 0 || stage > 4) return SWEDG_ERR_INVALID;
     if (!(dt > 0.0)) return fail(h, SWEDG_ERR_INVALID, "dt must be positive");
     cudaSetDevice(h->device);
-    StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true};
+    const unsigned id = stage_id_for(h, stage, dt);
+    StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, id, true};
     int rc = run_stage(h, sa);
+    h->stage_open = -1;
     if (rc == SWEDG_OK && stage == 4) h->t = h->t + dt;
     return rc;
 }
@@ -1393,13 +1494,16 @@ int swedg_stage_surface_range(swedg_handle h, int stage, double dt, int k0, int 
     if (h->scheme != SWEDG_SCHEME_HYBRIDIZED)
         return fail(h, SWEDG_ERR_UNSUPPORTED, "stage-level API is hybridized-only");
     cudaSetDevice(h->device);
+    const unsigned id = stage_id_for(h, stage, dt);
     int rc = SWEDG_OK;
     if (k1 > k0) {
-        StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, h->stage_cur, true,
-                     k0, k1};
+        StageArgs sa{h->u, 2, nullptr, true, Lsrk45::a[stage], Lsrk45::b[stage], dt, nullptr, id, true, k0, k1};
         rc = run_stage(h, sa);
     }
-    if (rc == SWEDG_OK && stage == 4 && k1 == h->K) h->t = h->t + dt;  // the range ending at K closes the step
+    if (k1 == h->K) {  // the range ending at K closes the stage (and, for stage 4, the step)
+        h->stage_open = -1;
+        if (rc == SWEDG_OK && stage == 4) h->t = h->t + dt;
+    }
     return rc;
 }
 
@@ -1409,6 +1513,188 @@ int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, l
     if (n_owned) *n_owned = h->K;
     if (n_halo) *n_halo = h->n_halo;
     return SWEDG_OK;
+}
+
+// ---- multi-rank halo exchange (halo.cuh) --------------------------------------
+int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
+    if (!h || !d) return SWEDG_ERR_INVALID;
+    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED) return fail(h, SWEDG_ERR_UNSUPPORTED, "halo exchange is hybridized-only");
+    if (d->n_send_msgs < 0 || d->n_recv_msgs < 0 || (d->n_send_msgs && (!d->send_peer || !d->send_count)) ||
+        (d->n_recv_msgs && (!d->recv_peer || !d->recv_count)))
+        return fail(h, SWEDG_ERR_INVALID, "bad halo descriptor");
+    cudaSetDevice(h->device);
+    const size_t per = (size_t)3 * h->nf;  // one pseudo-element
+    auto slots = [](int n) { return (size_t)((n + 2) / 3); };
+    std::vector<int> sp, rp;
+    std::vector<size_t> so, sl, ro, rl;
+    size_t off = 0, nsend = 0;
+    for (int m = 0; m < d->n_send_msgs; ++m) {
+        if (d->send_count[m] < 0) return fail(h, SWEDG_ERR_INVALID, "negative halo message size");
+        sp.push_back(d->send_peer[m]);
+        so.push_back(off);
+        sl.push_back(slots(d->send_count[m]) * per);
+        off += sl.back();
+        nsend += (size_t)d->send_count[m];
+    }
+    const size_t send_doubles = off;
+    off = 0;
+    for (int m = 0; m < d->n_recv_msgs; ++m) {
+        if (d->recv_count[m] < 0) return fail(h, SWEDG_ERR_INVALID, "negative halo message size");
+        rp.push_back(d->recv_peer[m]);
+        ro.push_back(off);
+        rl.push_back(slots(d->recv_count[m]) * per);
+        off += rl.back();
+    }
+    if (off != (size_t)h->n_halo * per)
+        return fail(h, SWEDG_ERR_INVALID, "receive messages do not fill the descriptor's n_halo slots");
+    if (nsend && (!d->send_elem || !d->send_face)) return fail(h, SWEDG_ERR_INVALID, "missing send faces");
+    // per sent face: trace offset and wire offset; the volume ranges that own sent faces
+    std::vector<long long> src(nsend), dst(nsend);
+    std::vector<int> owners;
+    size_t i = 0;
+    for (int m = 0; m < d->n_send_msgs; ++m)
+        for (int j = 0; j < d->send_count[m]; ++j, ++i) {
+            const int e = d->send_elem[i], f = d->send_face[i];
+            if (e < 0 || e >= h->K || f < 0 || f > 2)
+                return fail(h, SWEDG_ERR_INVALID, "sent face out of range (element " + std::to_string(e) + ")");
+            src[i] = ((long long)e * 3) * h->nf + (long long)f * h->npf;
+            dst[i] = (long long)(so[m] + (size_t)(j / 3) * per) + (long long)(j % 3) * h->npf;
+            owners.push_back(e);
+        }
+    std::sort(owners.begin(), owners.end());
+    owners.erase(std::unique(owners.begin(), owners.end()), owners.end());
+    std::vector<std::pair<int, int>> bnd, inner;
+    for (size_t a = 0; a < owners.size();) {  // runs with gaps of < 64 elements, even-aligned
+        size_t b = a;
+        while (b + 1 < owners.size() && owners[b + 1] - owners[b] < 64) ++b;
+        int k0 = owners[a] & ~1, k1 = std::min(h->K, (owners[b] + 2) & ~1);
+        if (!bnd.empty() && k0 <= bnd.back().second) bnd.back().second = std::max(bnd.back().second, k1);
+        else bnd.push_back({k0, k1});
+        a = b + 1;
+    }
+    int at = 0;
+    for (const auto& r : bnd) {
+        if (r.first > at) inner.push_back({at, r.first});
+        at = r.second;
+    }
+    if (at < h->K) inner.push_back({at, h->K});
+    // device buffers
+    if (h->pack_src) cudaFree(h->pack_src);
+    if (h->pack_dst) cudaFree(h->pack_dst);
+    if (h->sendbuf) cudaFree(h->sendbuf);
+    h->pack_src = h->pack_dst = nullptr;
+    h->sendbuf = nullptr;
+    if (dalloc(h, &h->pack_src, nsend) || dalloc(h, &h->pack_dst, nsend) || dalloc(h, &h->sendbuf, send_doubles))
+        return h->last_code;
+    if (nsend && (upload(h, h->pack_src, src.data(), nsend) || upload(h, h->pack_dst, dst.data(), nsend)))
+        return h->last_code;
+    // padding face positions of the wire format stay zero
+    CUDA_TRY(h, cudaMemsetAsync(h->sendbuf, 0, std::max<size_t>(1, send_doubles) * 8, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->trace + (size_t)h->K * per, 0, (size_t)h->n_halo * per * 8 + 8, h->stream));
+    if (!h->comm) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
+    if (!h->ev_bnd) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming));
+    if (!h->ev_halo) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    h->send_peer = sp;
+    h->recv_peer = rp;
+    h->send_off = so;
+    h->send_len = sl;
+    h->recv_off = ro;
+    h->recv_len = rl;
+    h->n_send_faces = (int)nsend;
+    h->send_doubles = send_doubles;
+    h->bnd_ranges = bnd;
+    h->int_ranges = inner;
+    h->halo_set = true;
+    if (h->graph_exec) {  // the captured step changes
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    return SWEDG_OK;
+}
+
+int swedg_set_nccl_comm(swedg_handle h, void* comm) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (comm && !nccl_api().ok) return fail(h, SWEDG_ERR_UNSUPPORTED, nccl_api().error);
+    h->nccl = comm;
+    if (comm) h->xfn = nullptr;
+    if (h->graph_exec) {
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    return SWEDG_OK;
+}
+
+int swedg_set_exchange(swedg_handle h, swedg_exchange_fn fn, void* user) {
+    if (!h) return SWEDG_ERR_INVALID;
+    h->xfn = fn;
+    h->xuser = user;
+    if (fn) h->nccl = nullptr;
+    if (h->graph_exec) {
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    return SWEDG_OK;
+}
+
+int swedg_halo_buffers(swedg_handle h, double** send, size_t* n_send, double** recv, size_t* n_recv) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (send) *send = h->sendbuf;
+    if (n_send) *n_send = h->send_doubles;
+    if (recv) *recv = h->trace ? h->trace + (size_t)h->K * 3 * h->nf : nullptr;
+    if (n_recv) *n_recv = (size_t)h->n_halo * 3 * h->nf;
+    return SWEDG_OK;
+}
+
+int swedg_halo_pack(swedg_handle h) {
+    if (!h) return SWEDG_ERR_INVALID;
+    if (!h->halo_set) return fail(h, SWEDG_ERR_INVALID, "swedg_halo_pack needs swedg_set_halo first");
+    cudaSetDevice(h->device);
+    return halo_pack_on(h, h->stream);
+}
+
+int swedg_halo_ranges(swedg_handle h, int* ranges, int max_ranges, int* n_boundary, int* n_interior) {
+    if (!h) return SWEDG_ERR_INVALID;
+    const int nb = (int)h->bnd_ranges.size(), ni = (int)h->int_ranges.size();
+    if (n_boundary) *n_boundary = nb;
+    if (n_interior) *n_interior = ni;
+    if (ranges) {
+        if (max_ranges < nb + ni) return fail(h, SWEDG_ERR_INVALID, "range buffer too small");
+        int w = 0;
+        for (const auto& r : h->bnd_ranges) { ranges[w++] = r.first; ranges[w++] = r.second; }
+        for (const auto& r : h->int_ranges) { ranges[w++] = r.first; ranges[w++] = r.second; }
+    }
+    return SWEDG_OK;
+}
+
+int swedg_nccl_unique_id(void* id) {
+    if (!id) return SWEDG_ERR_INVALID;
+    NcclApi& api = nccl_api();
+    if (!api.ok) return fail(nullptr, SWEDG_ERR_UNSUPPORTED, api.error);
+    NcclUid u;
+    const int rc = api.GetUniqueId(&u);
+    if (rc != 0) return fail(nullptr, SWEDG_ERR_CUDA, std::string("ncclGetUniqueId: ") + api.GetErrorString(rc));
+    std::memcpy(id, u.internal, sizeof(u.internal));
+    return SWEDG_OK;
+}
+
+int swedg_nccl_comm_init(int nranks, const void* id, int rank, int device, void** comm) {
+    if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return SWEDG_ERR_INVALID;
+    NcclApi& api = nccl_api();
+    if (!api.ok) return fail(nullptr, SWEDG_ERR_UNSUPPORTED, api.error);
+    if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, SWEDG_ERR_CUDA, "bad device ordinal");
+    NcclUid u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    const int rc = api.CommInitRank(comm, nranks, u, rank);
+    if (rc != 0) return fail(nullptr, SWEDG_ERR_CUDA, std::string("ncclCommInitRank: ") + api.GetErrorString(rc));
+    return SWEDG_OK;
+}
+
+int swedg_nccl_comm_destroy(void* comm) {
+    if (!comm) return SWEDG_OK;
+    NcclApi& api = nccl_api();
+    if (!api.ok) return SWEDG_ERR_UNSUPPORTED;
+    return api.CommDestroy(comm) == 0 ? SWEDG_OK : SWEDG_ERR_CUDA;
 }
 
 int swedg_check(swedg_handle h) {

@@ -1,227 +1,197 @@
 """Element partitioning and the per-stage halo exchange (multi-rank path).
 
 The RHS is element-local except the exterior face trace u~+ (solver.hpp:263-264),
-so the mesh shards by elements with ONE exchange per RK stage: the face traces
-of boundary elements, between swedg_stage_volume (which writes the owned traces)
-and swedg_stage_surface (which reads owned + halo traces).
+so the mesh shards by elements with ONE exchange per RK stage: the projected
+traces of the cut faces (3 fields x npf nodes per face).
 
-Partition = y-strips of the structured periodic mesh (native setup
-`Case(..., strips=P, strip=r)`): rank r owns quad rows [r*ny, (r+1)*ny) of a
-global nx x (ny*P) mesh; its halo slots are
-    below  K + [0, 2nx)      <- rank r-1's last owned row  (elements K-2nx .. K-1)
-    above  K + 2nx + [0,2nx) <- rank r+1's first owned row (elements 0 .. 2nx-1)
-(periodic wrap in y).  Traces of whole elements ([3][nf] blocks) are shipped:
-2nx*45 doubles per neighbour per stage (737 KB at nx=1024) — latency-bound on
-NVLink, hidden behind the ms-scale volume kernel.
+Partition = y-strips of the structured periodic mesh, built by the native setup
+(`capi.Case(..., strips=P, strip=r, scaling="weak"|"strong")`, setup.cpp
+compact_strip): rank r owns a band of quad rows; its halo is the two cuts' faces.
+The exchange map (`Case.halo_desc()`, C ABI `swedg_halo_desc`) lists per message
+the peer rank and the sent faces; the wire format packs three faces per [3][nf]
+pseudo-element, the layout of the receiver's halo slots (no unpack step).
+
+Transports (all drive the same native stage schedule, swedg_capi.cu run_step_halo:
+boundary volume -> pack -> exchange on a comm stream || interior volume -> interface):
+  * NCCL   `attach_nccl`: a library-owned communicator (swedg_nccl_comm_init; the
+             unique id travels over torch.distributed), ncclSend/ncclRecv inside the
+             captured step graph — the production path (bench.py --gpus N).
+  * gloo   `attach_gloo`: a host-staged exchange callback (functional check of the
+             multi-rank orchestration with several ranks sharing one GPU).
+  * local  `LocalExchange`: P handles in one process on one GPU, one host thread per
+             rank, device copies between their buffers ordered by CUDA events.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+import threading
+
+import numpy as np
 
 
-@dataclass(frozen=True)
-class StripHalo:
-    P: int
-    rank: int
-    nx: int
-    K: int  # owned elements
-
-    @property
-    def row(self) -> int:
-        return 2 * self.nx
-
-    @property
-    def prev(self) -> int:
-        return (self.rank - 1) % self.P
-
-    @property
-    def next(self) -> int:
-        return (self.rank + 1) % self.P
-
-    # (begin, end) element ranges in the [K + n_halo] trace buffer
-    @property
-    def send_to_next(self):  # my last row -> next rank's below-halo
-        return (self.K - self.row, self.K)
-
-    @property
-    def send_to_prev(self):  # my first row -> prev rank's above-halo
-        return (0, self.row)
-
-    @property
-    def recv_from_prev(self):  # below-halo
-        return (self.K, self.K + self.row)
-
-    @property
-    def recv_from_next(self):  # above-halo
-        return (self.K + self.row, self.K + 2 * self.row)
+def wire_slots(n: int) -> int:
+    """Pseudo-elements ([3][nf] blocks) of a message of n faces."""
+    return (n + 2) // 3
 
 
-def exchange(trace, plan: StripHalo, group=None) -> None:
-    """Fill the halo slots of `trace` ([K + 4nx][3][nf] torch tensor, CPU or CUDA)
-    from the neighbouring ranks with point-to-point messages (NCCL or gloo).
-    Issue order is identical on every rank, so for P = 2 (both neighbours are the
-    same rank) the two messages each way still pair up in order."""
+def message_offsets(counts, nf: int):
+    """(offset, length) in doubles of each message in a buffer of back-to-back messages."""
+    out, off = [], 0
+    for n in counts:
+        ln = wire_slots(int(n)) * 3 * nf
+        out.append((off, ln))
+        off += ln
+    return out
+
+
+# ---------------------------------------------------------------------------
+# wire format on host arrays (CPU reference of the pack kernel, halo.cuh)
+def pack_faces(traces, halo: dict, npf: int) -> np.ndarray:
+    """traces [K][3][nf] -> the send buffer (messages back to back, wire format)."""
+    nf = traces.shape[2]
+    offs = message_offsets(halo["send_count"], nf)
+    buf = np.zeros(sum(ln for _, ln in offs))
+    i = 0
+    for (off, _), n in zip(offs, halo["send_count"]):
+        for j in range(int(n)):
+            e, f = int(halo["send_elem"][i]), int(halo["send_face"][i])
+            i += 1
+            base = off + (j // 3) * 3 * nf + (j % 3) * npf
+            for c in range(3):
+                buf[base + c * nf: base + c * nf + npf] = traces[e, c, f * npf:(f + 1) * npf]
+    return buf
+
+
+# ---------------------------------------------------------------------------
+# torch.distributed transports
+def exchange_messages(send, recv, halo: dict, nf: int, group=None) -> None:
+    """Point-to-point exchange of the wire-format messages (flat torch tensors, CPU for
+    gloo, CUDA for NCCL).  Messages between the same two ranks pair up in issue order."""
     import torch.distributed as dist
 
-    if plan.P == 1:
-        return
-    if trace.is_cuda and dist.get_backend(group) == "gloo":  # gloo P2P needs host tensors
-        host = trace.cpu()
-        exchange(host, plan, group)
-        c0, c1 = plan.recv_from_prev
-        d0, d1 = plan.recv_from_next
-        trace[c0:c1].copy_(host[c0:c1])
-        trace[d0:d1].copy_(host[d0:d1])
-        return
-    a0, a1 = plan.send_to_next
-    b0, b1 = plan.send_to_prev
-    c0, c1 = plan.recv_from_prev
-    d0, d1 = plan.recv_from_next
-    ops = [
-        dist.P2POp(dist.isend, trace[a0:a1].contiguous(), plan.next, group),
-        dist.P2POp(dist.isend, trace[b0:b1].contiguous(), plan.prev, group),
-    ]
-    rb = trace[c0:c1]
-    ra = trace[d0:d1]
-    ops += [dist.P2POp(dist.irecv, rb, plan.prev, group), dist.P2POp(dist.irecv, ra, plan.next, group)]
-    for r in dist.batch_isend_irecv(ops):
-        r.wait()
+    ops = []
+    for (off, ln), peer in zip(message_offsets(halo["send_count"], nf), halo["send_peer"]):
+        ops.append(dist.P2POp(dist.isend, send[off:off + ln].contiguous(), int(peer), group))
+    for (off, ln), peer in zip(message_offsets(halo["recv_count"], nf), halo["recv_peer"]):
+        ops.append(dist.P2POp(dist.irecv, recv[off:off + ln], int(peer), group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
 
 
-def stage_overlapped(h, stage: int, dt: float, trace, plan: StripHalo, stream, comm_stream, group=None,
-                     exchange_fn=None) -> None:
-    """One LSRK45 stage with the halo exchange overlapped with interior volume work:
-    the volume kernel runs first on the two boundary rows (the elements whose traces
-    the neighbours need), the exchange of those traces starts on `comm_stream`, the
-    interior volume kernel runs on `stream` meanwhile, and the surface kernel waits
-    for the exchange.  `exchange_fn(trace, plan)` defaults to `exchange` (NCCL/gloo
-    point-to-point)."""
+def attach_nccl(h, halo: dict, world: int, rank: int, device: int, group=None) -> int:
+    """Give handle h a library-owned NCCL communicator over the ranks of the default
+    torch.distributed group (the unique id is broadcast from rank 0).  Returns the comm."""
+    import torch
+    import torch.distributed as dist
+
+    from . import capi
+
+    uid = capi.nccl_unique_id() if rank == 0 else bytes(128)
+    backend = dist.get_backend(group)
+    t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda" if backend == "nccl" else "cpu")
+    dist.broadcast(t, src=0, group=group)
+    comm = capi.nccl_comm_init(world, bytes(t.cpu().tolist()), rank, device)
+    h.set_nccl_comm(comm)
+    return comm
+
+
+def attach_gloo(h, halo: dict, nf: int, group=None) -> None:
+    """Host-staged exchange over gloo as the handle's transport callback (blocking:
+    the stream is synchronised before the send buffer is read).  A functional path for
+    several ranks on one device, not a performance path."""
     import torch
 
-    K, row = plan.K, plan.row
-    ex = exchange_fn or (lambda t, p: exchange(t, p, group))
-    h.stage_volume_range(stage, dt, 0, row)            # first row  -> previous rank
-    h.stage_volume_range(stage, dt, K - row, K)        # last row   -> next rank
-    boundary_done = torch.cuda.Event()
-    boundary_done.record(stream)
-    with torch.cuda.stream(comm_stream):
-        comm_stream.wait_event(boundary_done)
-        ex(trace, plan)
-        halos_in = torch.cuda.Event()
-        halos_in.record(comm_stream)
-    h.stage_volume_range(stage, dt, row, K - row)      # interior, concurrent with the exchange
-    stream.wait_event(halos_in)
-    h.stage_surface(stage, dt)
+    send_ptr, ns, recv_ptr, nr = h.halo_buffers()
+    send_dev = _view(send_ptr, (ns,))
+    recv_dev = _view(recv_ptr, (nr,))
+
+    def xfn(stage, send, recv, stream):
+        st = torch.cuda.ExternalStream(stream)
+        st.synchronize()
+        host_send = send_dev.cpu()
+        host_recv = torch.zeros(nr, dtype=torch.float64)
+        exchange_messages(host_send, host_recv, halo, nf, group)
+        with torch.cuda.stream(st):
+            recv_dev.copy_(host_recv, non_blocking=False)
+
+    h.set_exchange(xfn)
 
 
-def state_tensor(handle):
-    """Zero-copy torch view [K][3][Np] of a handle's device-resident state."""
-    import torch
+class LocalExchange:
+    """P logical partitions on one device, each stepped by its own host thread through
+    the native multi-rank schedule; the exchange callback of rank r pushes its messages
+    into the peers' halo slots with device copies.  Ordering is by CUDA events only (no
+    kernel waits on another rank's kernel): a rank's copy into a peer starts after the
+    peer entered the stage's exchange (its previous interface kernel is done), and a
+    rank's interface kernel starts after every copy into its slots."""
 
-    u_ptr, _ = handle.state_device_ptrs()
-    s = handle.sizes
-    return torch.as_tensor(_CudaArray(u_ptr, (s.K, 3, handle.nstate)), device="cuda")
-
-
-class HostStepper:
-    """Host-state LSRK45 steps of one rank (the multi-rank counterpart of
-    swedg_step_lsrk45_host): every step copies the rank's state in from a pinned
-    host buffer and its result back out, and the copies overlap the work:
-    the two boundary rows arrive first, the stage-0 volume kernel runs chunk by chunk
-    as the rest lands (the halo exchange starts after the boundary rows), and the
-    last interface kernel runs chunk by chunk, each chunk's D2H starting at once.
-    Stages 1..3 use stage_overlapped."""
-
-    def __init__(self, h, plan: StripHalo, stream, comm_stream, chunks: int = 16, group=None, exchange_fn=None):
+    def __init__(self, handles, halos, nf: int):
         import torch
 
-        self.h, self.plan, self.stream, self.comm = h, plan, stream, comm_stream
-        self.group, self.exchange_fn = group, exchange_fn
-        K, row = plan.K, plan.row
-        inner = max(1, min(chunks - 2, (K - 2 * row) // max(1, row)))
-        cuts = [row + (K - 2 * row) * i // inner for i in range(inner + 1)]
-        # processing order: first row, last row, then the interior from the bottom up
-        self.ranges = [(0, row), (K - row, K)] + [(cuts[i], cuts[i + 1]) for i in range(inner) if cuts[i] < cuts[i + 1]]
-        self.copy_in = torch.cuda.Stream(device=stream.device)
-        self.copy_out = torch.cuda.Stream(device=stream.device)
-        n = len(self.ranges)
-        self.ev_in = [torch.cuda.Event() for _ in range(n)]
-        self.ev_out = [torch.cuda.Event() for _ in range(n)]
-        self.ev_done = [torch.cuda.Event() for _ in range(n)]
-        self.trace = trace_tensor(h)
-        self.dev = state_tensor(h)
+        self.h, self.halos, self.nf, self.P = handles, halos, nf, len(handles)
+        self.bufs = [h.halo_buffers() for h in handles]
+        self.barrier = threading.Barrier(self.P)
+        self.ready = [torch.cuda.Event() for _ in range(self.P)]
+        self.copied = [torch.cuda.Event() for _ in range(self.P)]
+        # message pairing: the k-th send r -> q matches q's k-th receive from r
+        self.routes = []  # per rank: [(send offset, dest rank, dest offset, length)]
+        recv_slots = []
+        for q in range(self.P):
+            per_src = {}
+            for (off, ln), src in zip(message_offsets(halos[q]["recv_count"], nf), halos[q]["recv_peer"]):
+                per_src.setdefault(int(src), []).append((off, ln))
+            recv_slots.append(per_src)
+        for r in range(self.P):
+            used, rt = {}, []
+            for (off, ln), dst in zip(message_offsets(halos[r]["send_count"], nf), halos[r]["send_peer"]):
+                dst = int(dst)
+                k = used.get(dst, 0)
+                used[dst] = k + 1
+                doff, dln = recv_slots[dst][r][k]
+                assert dln == ln, "message sizes disagree between ranks"
+                rt.append((off, dst, doff, ln))
+            self.routes.append(rt)
+        for r, h in enumerate(handles):
+            h.set_exchange(self._fn(r))
 
-    def _exchange(self):
-        ex = self.exchange_fn or (lambda t, p: exchange(t, p, self.group))
-        ex(self.trace, self.plan)
-
-    def step(self, host_u, dt: float, nsteps: int = 1) -> None:
-        """host_u: torch CPU tensor (pinned) [K][3][Np], updated in place every step."""
+    def _fn(self, r):
         import torch
 
-        h, st, comm = self.h, self.stream, self.comm
-        K, row = self.plan.K, self.plan.row
-        ready = torch.cuda.Event()
-        ready.record(st)
-        self.copy_in.wait_event(ready)
-        for n in range(nsteps):
-            for i, (a, b) in enumerate(self.ranges):  # H2D, after the previous step's D2H of the chunk
-                if n > 0:
-                    self.copy_in.wait_event(self.ev_out[i])
-                with torch.cuda.stream(self.copy_in):
-                    self.dev[a:b].copy_(host_u[a:b], non_blocking=True)
-                self.ev_in[i].record(self.copy_in)
-            with torch.cuda.stream(st):
-                for s in range(5):
-                    if s in (1, 2, 3):
-                        stage_overlapped(h, s, dt, self.trace, self.plan, st, comm, self.group, self.exchange_fn)
-                        continue
-                    # boundary rows first (stage 0: as they land), exchange on the comm stream
-                    for i in (0, 1):
-                        if s == 0:
-                            st.wait_event(self.ev_in[i])
-                        h.stage_volume_range(s, dt, *self.ranges[i])
-                    boundary = torch.cuda.Event()
-                    boundary.record(st)
-                    with torch.cuda.stream(comm):
-                        comm.wait_event(boundary)
-                        self._exchange()
-                        halos = torch.cuda.Event()
-                        halos.record(comm)
-                    for i in range(2, len(self.ranges)):
-                        if s == 0:
-                            st.wait_event(self.ev_in[i])
-                        h.stage_volume_range(s, dt, *self.ranges[i])
-                    st.wait_event(halos)
-                    if s == 0:
-                        h.stage_surface(s, dt)
-                        continue
-                    # last stage: interface kernel by chunk (the range ending at K last), D2H right after
-                    order = sorted(range(len(self.ranges)), key=lambda i: self.ranges[i][1] == K)
-                    for i in order:
-                        a, b = self.ranges[i]
-                        h.stage_surface_range(s, dt, a, b)
-                        self.ev_done[i].record(st)
-                        self.copy_out.wait_event(self.ev_done[i])
-                        with torch.cuda.stream(self.copy_out):
-                            host_u[a:b].copy_(self.dev[a:b], non_blocking=True)
-                        self.ev_out[i].record(self.copy_out)
-        for e in self.ev_out:
-            st.wait_event(e)
+        def xfn(stage, send, recv, stream):
+            st = torch.cuda.ExternalStream(stream)
+            self.ready[r].record(st)
+            self.barrier.wait()
+            for off, dst, doff, ln in self.routes[r]:
+                st.wait_event(self.ready[dst])
+                src = _view(self.bufs[r][0] + 8 * off, (ln,))
+                dstv = _view(self.bufs[dst][2] + 8 * doff, (ln,))
+                with torch.cuda.stream(st):
+                    dstv.copy_(src, non_blocking=True)
+            self.copied[r].record(st)
+            self.barrier.wait()
+            for q in range(self.P):
+                if any(d == r for _, d, _, _ in self.routes[q]):
+                    st.wait_event(self.copied[q])
 
+        return xfn
 
-def copy_halos_local(traces, plans) -> None:
-    """Single-process stand-in for `exchange` over P logical partitions (device copies)."""
-    P = len(plans)
-    for r, pl in enumerate(plans):
-        prv, nxt = plans[pl.prev], plans[pl.next]
-        c0, c1 = pl.recv_from_prev
-        a0, a1 = prv.send_to_next
-        traces[r][c0:c1].copy_(traces[pl.prev][a0:a1])
-        d0, d1 = pl.recv_from_next
-        b0, b1 = nxt.send_to_prev
-        traces[r][d0:d1].copy_(traces[pl.next][b0:b1])
-    assert P >= 1
+    def step(self, dt: float, nsteps: int) -> None:
+        errs = []
+
+        def run(h):
+            try:
+                h.step(dt, nsteps, sync=True)
+            except Exception as e:  # noqa: BLE001 - re-raised below
+                errs.append(e)
+                self.barrier.abort()
+
+        ts = [threading.Thread(target=run, args=(h,)) for h in self.h]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
 
 
 class _CudaArray:
@@ -230,10 +200,19 @@ class _CudaArray:
                                          "version": 3, "strides": None}
 
 
-def trace_tensor(handle):
-    """Zero-copy torch view [K + n_halo][3][nf] of a handle's device face-trace buffer."""
+def _view(ptr: int, shape):
     import torch
 
+    return torch.as_tensor(_CudaArray(ptr, shape), device="cuda")
+
+
+def state_tensor(handle):
+    """Zero-copy torch view [K][3][Np] of a handle's device-resident state."""
+    u_ptr, _ = handle.state_device_ptrs()
+    return _view(u_ptr, (handle.sizes.K, 3, handle.nstate))
+
+
+def trace_tensor(handle):
+    """Zero-copy torch view [K + n_halo][3][nf] of a handle's device face-trace buffer."""
     ptr, K, H = handle.trace_info()
-    nf = handle.sizes.nf
-    return torch.as_tensor(_CudaArray(ptr, (K + H, 3, nf)), device="cuda")
+    return _view(ptr, (K + H, 3, handle.sizes.nf))

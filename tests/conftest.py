@@ -12,3 +12,11 @@ if TESTS not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (CUDA device); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """FAST-mode parity audit trail (tests/parity_log.py)."""
+    import parity_log
+
+    path = os.environ.get("SWEDG_PARITY_LOG", os.path.join(REPO, "gpurun_out", "parity_log.jsonl"))
+    parity_log.write(path)

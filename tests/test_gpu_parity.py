@@ -17,6 +17,7 @@ import math
 import numpy as np
 import pytest
 
+import parity_log
 from oracle_py import Oracle, case_dict, load_golden
 
 pytestmark = pytest.mark.gpu
@@ -33,21 +34,21 @@ def rel(a, b):
     return float(np.abs(a - b).max() / (1.0 + np.abs(b).max()))
 
 
-def assert_fast_rhs(du_fast, du_ref, case, u, penalty_lf=True):
+def assert_fast_rhs(du_fast, du_ref, case, u, penalty_lf=True, label=None):
     """FAST-mode acceptance for one RHS evaluation:
         max|du_fast - du_ref| / (1 + max|du_ref|) <= 1e-12            (north-star tolerance)
     or, on cancellation-dominated states where the reference itself is further
     than that from the exact RHS (lake/dam at rest: du ~ 1e-12 noise), FAST must
     be no less accurate than the reference:
         max|du_fast - du_exact| <= 4 max|du_ref - du_exact|,
-    with du_exact from the same algorithm in long double (oracle/liboracle_ld.so)."""
-    if rel(du_fast, du_ref) <= RHS_TOL:
-        return
-    exact, err, _ = Oracle(case, penalty_lf=penalty_lf, precision="ld").rhs(u)
-    assert err == 0
-    e_fast = np.abs(du_fast - exact).max()
-    e_ref = np.abs(du_ref - exact).max()
-    assert e_fast <= 4.0 * e_ref, f"FAST error {e_fast:.3e} vs reference rounding error {e_ref:.3e}"
+    with du_exact from the same algorithm in long double (oracle/liboracle_ld.so).
+    Every call is recorded with its numbers and branch (tests/parity_log.py)."""
+    def exact():
+        ex, err, _ = Oracle(case, penalty_lf=penalty_lf, precision="ld").rhs(u)
+        assert err == 0
+        return ex
+
+    parity_log.assert_fast_rhs(du_fast, du_ref, exact, label=label or ("LF" if penalty_lf else "EC"))
 
 
 def make(c, mode, penalty=capi.PENALTY_LF):

@@ -1,11 +1,17 @@
-"""Multi-rank path: y-strip partitions with a per-stage halo exchange of face traces.
+"""Multi-rank path: y-strip partitions with a per-stage halo exchange of cut-face traces.
 
-CPU tests (this container): the strip setup equals the global mesh bitwise, and
-a real multi-process run (torch.distributed gloo, world size 2 and 3) that
-computes each rank's RHS with the C oracle from its owned elements plus halo
-traces received over gloo reproduces the single-process global RHS bit for bit.
-GPU test: P logical partitions on one device (halo moved by device copies,
-never kernels waiting on each other) equal the unpartitioned run bitwise.
+CPU tests (this container):
+  * the strip setup (weak and strong scaling) equals the global mesh bitwise, and its
+    halo map points every cut face at the right neighbour trace;
+  * real multi-process runs (torch.distributed gloo, world size 2 and 3): every rank
+    steps its strip with the C oracle, exchanging only the packed cut-face traces in
+    the wire format each stage; the gathered state after 2 LSRK45 steps equals the
+    single-process global run bit for bit.
+GPU tests: the native multi-rank schedule (swedg_capi.cu run_step_halo) with logical
+partitions on one device (one host thread per rank, exchange callback with device
+copies), with a one-rank NCCL communicator (self exchange across the periodic cut,
+inside the captured step graph), and the stage-level API — all bitwise equal to the
+unpartitioned steps.
 """
 import os
 import socket
@@ -16,46 +22,85 @@ import torch
 
 from oracle_py import Oracle, case_dict
 from paper_2005_02516_b200 import capi
-from paper_2005_02516_b200.partition import StripHalo, copy_halos_local, exchange
+from paper_2005_02516_b200.partition import LocalExchange, exchange_messages, message_offsets, pack_faces
 
-NX, NY, N = 6, 3, 3  # per-strip quads: 6 x 3 -> 36 owned elements per rank
+NX, NY, N = 6, 3, 3  # weak: 6 x 3 quads per rank; strong: the 6 x 7 mesh cut in P strips
+NY_STRONG = 7
+LSRK_A = (0.0, -0.41789047449985195, -1.192151694642677, -1.6977846924715279, -1.5141834442571558)
+LSRK_B = (0.14965902199922912, 0.37921031299962726, 0.8229550293869817, 0.6994504559491221, 0.15305724796815198)
 
 
-def owned_slice(r):
-    return slice(r * NY * 2 * NX, (r + 1) * NY * 2 * NX)
+def rows(scaling, P, r):
+    """Global quad rows [j0, j1) owned by rank r."""
+    if scaling == "weak":
+        return r * NY, (r + 1) * NY
+    return NY_STRONG * r // P, NY_STRONG * (r + 1) // P
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_strip_setup_matches_global_mesh(P):
-    g = capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
+def case(scaling, P, r, N=N, **kw):
+    ny = NY if scaling == "weak" else NY_STRONG
+    return capi.Case("smooth", N=N, nx=NX, ny=ny, warp=0.1, strips=P, strip=r, scaling=scaling, threads=1, **kw)
+
+
+def owned_slice(scaling, P, r):
+    j0, j1 = rows(scaling, P, r)
+    return slice(2 * NX * j0, 2 * NX * j1)
+
+
+def halo_source(halos, P, r, slot_face):
+    """(source rank, sender's element, sender's face) of halo face `slot_face` = 3 q + position
+    of rank r, following the message pairing rule (k-th send a -> b = b's k-th receive from a)."""
+    h = halos[r]
+    base = 0
+    for m, (n, src) in enumerate(zip(h["recv_count"], h["recv_peer"])):
+        if slot_face < base + 3 * ((int(n) + 2) // 3):
+            j = slot_face - base
+            k = sum(1 for mm in range(m) if int(h["recv_peer"][mm]) == int(src))
+            hs = halos[int(src)]
+            sent = [i for i, d in enumerate(hs["send_peer"]) if int(d) == r][k]
+            first = int(np.sum(hs["send_count"][:sent]))
+            return int(src), int(hs["send_elem"][first + j]), int(hs["send_face"][first + j])
+        base += 3 * ((int(n) + 2) // 3)
+    raise AssertionError("halo slot outside the receive messages")
+
+
+@pytest.mark.parametrize("scaling,P", [("weak", 2), ("weak", 3), ("strong", 1), ("strong", 2), ("strong", 3)])
+def test_strip_setup_matches_global_mesh(scaling, P):
+    g = case(scaling, P, -1)
     Kg = g.K
-    assert Kg == 2 * NX * NY * P and g.n_halo == 0
+    assert g.n_halo == 0
     gnbr = g.iarray("nbr").reshape(Kg, 3)
-    for r in range(P):
-        s = capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=r, threads=1)
+    gperm = g.iarray("perm").reshape(Kg, -1)
+    strips = [case(scaling, P, r) for r in range(P)]
+    halos = [s.halo_desc() for s in strips]
+    dt = min(s.dt for s in strips)
+    assert dt == g.dt  # owned minimum edges: the global dt exactly
+    npf = g.npf
+    for r, s in enumerate(strips):
         K = s.K
-        assert K == 2 * NX * NY and s.n_halo == 4 * NX
-        sl = owned_slice(r)
+        sl = owned_slice(scaling, P, r)
+        assert K == sl.stop - sl.start
+        assert s.n_halo == 2 * ((NX + 2) // 3)  # nx cut faces per side, 3 per halo slot
         for name, per in [("gf", 4 * (s.nq + s.nf)), ("Mh_inv", s.Np * s.Np), ("sJ", s.nf), ("nx", s.nf),
                           ("u0", 3 * s.Np), ("b", s.Np)]:
             np.testing.assert_array_equal(s.array(name).reshape(K, per), g.array(name).reshape(Kg, per)[sl],
                                           err_msg=name)
-        np.testing.assert_array_equal(s.iarray("perm").reshape(K, -1), g.iarray("perm").reshape(Kg, -1)[sl])
-        # neighbour ids: owned -> global id, halo slot -> the neighbour rank's row
-        plan = StripHalo(P, r, NX, K)
-        off = sl.start
         lnbr = s.iarray("nbr").reshape(K, 3)
-        row = 2 * NX
+        lperm = s.iarray("perm").reshape(K, -1)
         for k in range(K):
             for f in range(3):
                 n = int(lnbr[k, f])
+                gk = sl.start + k
                 if n < K:
-                    gid = n + off
-                elif n < K + row:  # below halo <- prev rank's last row
-                    gid = owned_slice(plan.prev).stop - row + (n - K)
-                else:  # above halo <- next rank's first row
-                    gid = owned_slice(plan.next).start + (n - K - row)
-                assert gid == gnbr[off + k, f], (r, k, f)
+                    assert n + sl.start == gnbr[gk, f]
+                    np.testing.assert_array_equal(lperm[k, f * npf:(f + 1) * npf], gperm[gk, f * npf:(f + 1) * npf])
+                    continue
+                pos = lperm[k, f * npf] // npf
+                src, e, fe = halo_source(halos, P, r, 3 * (n - K) + pos)
+                assert owned_slice(scaling, P, src).start + e == gnbr[gk, f], (r, k, f)
+                for sn in range(npf):  # node order: global perm = (neighbour face) npf + node
+                    assert lperm[k, f * npf + sn] // npf == pos
+                    assert gperm[gk, f * npf + sn] == fe * npf + lperm[k, f * npf + sn] % npf
 
 
 def _free_port():
@@ -64,179 +109,175 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, P, port, q):
+def _rank_main(rank, P, scaling, port, dt, nsteps, q):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=P)
     try:
-        s = capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=rank, threads=1)
+        s = case(scaling, P, rank)
         c = case_dict(s)
+        halo = s.halo_desc()
         orc = Oracle(c)
-        proj, err, _ = orc.entropy_projection(c["u"])
-        assert err == 0
-        K, nq, nf = s.K, s.nq, s.nf
-        trace = torch.zeros((K + s.n_halo, 3, nf), dtype=torch.float64)
-        trace[:K] = torch.from_numpy(proj[:, :, nq:])
-        exchange(trace, StripHalo(P, rank, NX, K))
-        proj_all = np.zeros((K + s.n_halo, 3, nq + nf))
-        proj_all[:K] = proj
-        proj_all[K:, :, nq:] = trace[K:].numpy()
-        du, err, _ = orc.rhs_from_proj(proj_all)
-        assert err == 0
-        q.put((rank, du))
+        K, nq, nf, npf, nh = s.K, s.nq, s.nf, s.npf, s.nq + s.nf
+        nrecv = sum(ln for _, ln in message_offsets(halo["recv_count"], nf))
+        assert nrecv == s.n_halo * 3 * nf
+        u = np.array(c["u"], copy=True)
+        res = np.zeros_like(u)
+        for _ in range(nsteps):
+            for st in range(5):
+                proj, err, _ = orc.entropy_projection(u)
+                assert err == 0
+                send = torch.from_numpy(pack_faces(proj[:, :, nq:], halo, npf))
+                recv = torch.zeros(nrecv, dtype=torch.float64)
+                exchange_messages(send, recv, halo, nf)  # cut-face traces only, wire format
+                proj_all = np.zeros((K + s.n_halo, 3, nh))
+                proj_all[:K] = proj
+                proj_all[K:, :, nq:] = recv.numpy().reshape(s.n_halo, 3, nf)
+                du, err, _ = orc.rhs_from_proj(proj_all)
+                assert err == 0
+                res = LSRK_A[st] * res + dt * du  # step_lsrk45 (solver.hpp:479-480)
+                u = u + LSRK_B[st] * res
+        q.put((rank, u, int(send.numel())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_gloo_partitioned_rhs_equals_global_bitwise(P):
+@pytest.mark.parametrize("scaling,P", [("strong", 2), ("strong", 3), ("weak", 2)])
+def test_gloo_partitioned_steps_equal_global_bitwise(scaling, P):
+    """World size P over gloo: 2 LSRK45 steps with per-stage cut-face exchanges; the gathered
+    state equals the single-process global run (C oracle = the reference's arithmetic) bitwise."""
     import torch.multiprocessing as mp
 
+    dt, nsteps = 1e-3, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, P, port, q)) for r in range(P)]
+    procs = [ctx.Process(target=_rank_main, args=(r, P, scaling, port, dt, nsteps, q)) for r in range(P)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in range(P))
+    got = {}
+    for _ in range(P):
+        r, u, nsend = q.get(timeout=600)
+        got[r] = (u, nsend)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    g = capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
+    g = case(scaling, P, -1)
     gc = case_dict(g)
-    du_g, err, _ = Oracle(gc).rhs(gc["u"])
+    ug, _, err = Oracle(gc).step_lsrk45(gc["u"], np.zeros_like(gc["u"]), dt, nsteps)
     assert err == 0
     for r in range(P):
-        np.testing.assert_array_equal(got[r], du_g[owned_slice(r)])
+        np.testing.assert_array_equal(got[r][0], ug[owned_slice(scaling, P, r)])
+        # only the cut faces travel: 2 messages of nx faces, 3 faces per [3][nf] block
+        assert got[r][1] == 2 * ((NX + 2) // 3) * 3 * g.nf
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("P", [2, 3])
-def test_logical_partitions_on_one_gpu_equal_global(P):
-    from paper_2005_02516_b200.partition import trace_tensor
-
-    g = capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
+# ---------------------------------------------------------------------------- GPU
+def _global_steps(g, dt, nsteps, N):
     hg = g.handle(mode=capi.MODE_FAST)
     hg.set_state(g.u0())
-    dt = 1e-3
-    hg.step(dt, 2)
-    ug, _, _ = hg.get_state()
-    cases = [capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, strips=P, strip=r, threads=1) for r in range(P)]
-    hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
-    for h, c in zip(hs, cases):
-        h.set_state(c.u0())
-    plans = [StripHalo(P, r, NX, c.K) for r, c in enumerate(cases)]
-    traces = [trace_tensor(h) for h in hs]
-    for _ in range(2):
-        for s in range(5):
-            for h in hs:
-                h.stage_volume(s, dt)
-            torch.cuda.synchronize()
-            copy_halos_local(traces, plans)
-            torch.cuda.synchronize()
-            for h in hs:
-                h.stage_surface(s, dt)
-    for h in hs:
-        h.check()
-    for r, h in enumerate(hs):
-        u, _, t = h.get_state()
-        np.testing.assert_array_equal(u, ug[owned_slice(r)])
-        assert t == 2 * dt
+    hg.step(dt, nsteps)
+    ug, _, tg = hg.get_state()
+    hg.close()
+    return ug, tg
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("N", [3, 4])
-@pytest.mark.parametrize("P", [2, 3])
-def test_boundary_first_volume_ranges_equal_global(P, N):
-    """The overlapped schedule (partition.stage_overlapped): boundary rows' volume kernel,
-    halo exchange, interior volume kernel, surface kernel — with logical partitions on
-    one GPU — bit-for-bit the unpartitioned steps (N=4 and N=3 pair kernels)."""
-    from paper_2005_02516_b200.partition import trace_tensor
-
-    g = capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=-1, threads=1)
-    hg = g.handle(mode=capi.MODE_FAST)
-    hg.set_state(g.u0())
-    dt = 1e-3
-    hg.step(dt, 2)
-    ug, _, _ = hg.get_state()
-    cases = [capi.Case("smooth", N=N, nx=NX, ny=NY, warp=0.1, strips=P, strip=r, threads=1) for r in range(P)]
+@pytest.mark.parametrize("scaling,P", [("strong", 1), ("strong", 2), ("strong", 3), ("weak", 2)])
+def test_native_multirank_step_logical_partitions(scaling, P, N):
+    """swedg_step_lsrk45 on P strip handles (one host thread each, exchange callback pushing
+    the packed cut faces into the peers' halo slots by device copies) == the global steps,
+    bitwise (boundary-first volume ranges, comm stream, interior overlap included)."""
+    dt, nsteps = 1e-3, 3
+    g = case(scaling, P, -1, N=N)
+    ug, tg = _global_steps(g, dt, nsteps, N)
+    cases = [case(scaling, P, r, N=N) for r in range(P)]
     hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
     for h, c in zip(hs, cases):
         h.set_state(c.u0())
-    plans = [StripHalo(P, r, NX, c.K) for r, c in enumerate(cases)]
-    traces = [trace_tensor(h) for h in hs]
-    for _ in range(2):
+    LocalExchange(hs, [c.halo_desc() for c in cases], cases[0].nf).step(dt, nsteps)
+    for r, h in enumerate(hs):
+        u, _, t = h.get_state()
+        np.testing.assert_array_equal(u, ug[owned_slice(scaling, P, r)])
+        assert t == tg
+
+
+@pytest.mark.gpu
+def test_nccl_self_exchange_single_rank_graph():
+    """One rank whose halos are its own periodic cut (strong, P = 1) with a one-rank NCCL
+    communicator: ncclSend/ncclRecv to itself inside the captured step graph (the
+    production multi-GPU code path on one device) == the unpartitioned steps, bitwise."""
+    dt = 1e-3
+    for N in (3, 4):
+        g = case("strong", 1, -1, N=N)
+        ug, tg = _global_steps(g, dt, 4, N)
+        c = case("strong", 1, 0, N=N)
+        h = c.handle(mode=capi.MODE_FAST)
+        comm = capi.nccl_comm_init(1, capi.nccl_unique_id(), 0, 0)
+        try:
+            h.set_nccl_comm(comm)
+            h.set_state(c.u0())
+            h.step(dt, 3)  # graph capture + replay
+            h.step(dt, 1)  # individual launches
+            u, _, t = h.get_state()
+            np.testing.assert_array_equal(u, ug)
+            assert t == tg
+            h.close()
+        finally:
+            capi.nccl_comm_destroy(comm)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_stage_level_pack_and_device_copies(P):
+    """The stage-level API (volume ranges, swedg_halo_pack, caller-moved messages,
+    interface kernel) with logical partitions == the global steps, bitwise; also checks
+    the stage ids when volume ranges are issued out of order (interior first)."""
+    from paper_2005_02516_b200.partition import _view
+
+    dt, nsteps = 1e-3, 2
+    g = case("strong", P, -1, N=4)
+    ug, _ = _global_steps(g, dt, nsteps, 4)
+    cases = [case("strong", P, r, N=4) for r in range(P)]
+    hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
+    halos = [c.halo_desc() for c in cases]
+    nf = cases[0].nf
+    for h, c in zip(hs, cases):
+        h.set_state(c.u0())
+    bufs = [h.halo_buffers() for h in hs]
+    for _ in range(nsteps):
         for s in range(5):
-            for h, pl in zip(hs, plans):
-                h.stage_volume_range(s, dt, 0, pl.row)
-                h.stage_volume_range(s, dt, pl.K - pl.row, pl.K)
+            for h in hs:
+                bnd, inner = h.halo_ranges()
+                for a, b in inner + bnd:  # any order within a stage
+                    h.stage_volume_range(s, dt, a, b)
+                h.halo_pack()
             torch.cuda.synchronize()
-            copy_halos_local(traces, plans)
-            for h, pl in zip(hs, plans):
-                h.stage_volume_range(s, dt, pl.row, pl.K - pl.row)
+            for q in range(P):  # receive message m of q from its k-th send partner
+                seen = {}
+                for (off, ln), src in zip(message_offsets(halos[q]["recv_count"], nf), halos[q]["recv_peer"]):
+                    src = int(src)
+                    k = seen.get(src, 0)
+                    seen[src] = k + 1
+                    sends = [i for i, d in enumerate(halos[src]["send_peer"]) if int(d) == q]
+                    soff, sln = message_offsets(halos[src]["send_count"], nf)[sends[k]]
+                    _view(bufs[q][2] + 8 * off, (ln,)).copy_(_view(bufs[src][0] + 8 * soff, (sln,)))
             torch.cuda.synchronize()
             for h in hs:
                 h.stage_surface(s, dt)
-    for h in hs:
-        h.check()
     for r, h in enumerate(hs):
-        u, _, t = h.get_state()
-        np.testing.assert_array_equal(u, ug[owned_slice(r)])
+        h.check()
+        u, _, _ = h.get_state()
+        np.testing.assert_array_equal(u, ug[owned_slice("strong", P, r)])
 
 
 @pytest.mark.gpu
-def test_stage_overlapped_single_rank_equals_step():
-    """partition.stage_overlapped on one rank (no neighbours: the exchange is empty) with
-    separate compute and comm streams == swedg_step_lsrk45, bitwise."""
-    from paper_2005_02516_b200.partition import stage_overlapped, trace_tensor
-
-    c = capi.Case("smooth", N=4, nx=NX, ny=NY, warp=0.1, threads=1)
-    dt = 1e-3
-    h1 = c.handle(mode=capi.MODE_FAST)
-    h1.set_state(c.u0())
-    h1.step(dt, 2)
-    u1, _, _ = h1.get_state()
-    h2 = c.handle(mode=capi.MODE_FAST)
-    stream, comm = torch.cuda.Stream(), torch.cuda.Stream()
-    h2.set_stream(stream.cuda_stream)
-    h2.set_state(c.u0())
-    plan = StripHalo(1, 0, NX, c.K)
-    trace = trace_tensor(h2)
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            for s in range(5):
-                stage_overlapped(h2, s, dt, trace, plan, stream, comm)
-    torch.cuda.synchronize()
-    h2.check()
-    u2, _, _ = h2.get_state()
-    np.testing.assert_array_equal(u1, u2)
-
-
-@pytest.mark.gpu
-def test_host_stepper_single_rank_equals_step():
-    """partition.HostStepper (per-rank host-state steps with chunked copies overlapping the
-    stage-0 volume and last interface kernels) on one rank == swedg_step_lsrk45, bitwise,
-    and the host buffer holds every step's result."""
-    from paper_2005_02516_b200.partition import HostStepper
-
-    c = capi.Case("smooth", N=4, nx=NX, ny=8, warp=0.1, threads=1)
-    dt = 1e-3
-    h1 = c.handle(mode=capi.MODE_FAST)
-    h1.set_state(c.u0())
-    h1.step(dt, 3)
-    u1, _, t1 = h1.get_state()
-    h2 = c.handle(mode=capi.MODE_FAST)
-    stream, comm = torch.cuda.Stream(), torch.cuda.Stream()
-    h2.set_stream(stream.cuda_stream)
-    h2.set_state(c.u0())
-    hu = torch.from_numpy(c.u0().copy()).pin_memory()
-    hs = HostStepper(h2, StripHalo(1, 0, NX, c.K), stream, comm, chunks=5)
-    hs.step(hu, dt, 3)
-    torch.cuda.synchronize()
-    h2.check()
-    np.testing.assert_array_equal(hu.numpy(), u1)
-    u2, _, t2 = h2.get_state()
-    np.testing.assert_array_equal(u2, u1)
-    assert t2 == t1
+def test_multirank_handle_without_transport_fails_loudly():
+    c = case("strong", 2, 0, N=4)
+    h = c.handle(mode=capi.MODE_FAST)
+    h.set_state(c.u0())
+    with pytest.raises(capi.InvalidArgument):
+        h.step(1e-3, 1)
