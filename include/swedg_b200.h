@@ -215,7 +215,9 @@ int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, l
 int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d);
 /* NCCL transport: comm is an ncclComm_t whose ranks are the peers of the halo map
  * (libnccl.so.2 is resolved at run time: the one already loaded, e.g. by torch, or
- * $SWEDG_NCCL_LIB).  NULL detaches. */
+ * $SWEDG_NCCL_LIB).  NULL detaches (and drops the captured step graph, which holds
+ * NCCL work): detach or destroy every handle using a communicator before the
+ * communicator is destroyed. */
 int swedg_set_nccl_comm(swedg_handle h, void* comm);
 int swedg_set_exchange(swedg_handle h, swedg_exchange_fn fn, void* user);
 /* Device pointers and sizes (doubles) of the packed send messages and the halo slots. */

@@ -1590,7 +1590,7 @@ int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
         return h->last_code;
     // padding face positions of the wire format stay zero
     CUDA_TRY(h, cudaMemsetAsync(h->sendbuf, 0, std::max<size_t>(1, send_doubles) * 8, h->stream));
-    CUDA_TRY(h, cudaMemsetAsync(h->trace + (size_t)h->K * per, 0, (size_t)h->n_halo * per * 8 + 8, h->stream));
+    if (h->n_halo > 0) CUDA_TRY(h, cudaMemsetAsync(h->trace + (size_t)h->K * per, 0, (size_t)h->n_halo * per * 8, h->stream));
     if (!h->comm) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
     if (!h->ev_bnd) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming));
     if (!h->ev_halo) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
@@ -1690,6 +1690,8 @@ int swedg_nccl_comm_init(int nranks, const void* id, int rank, int device, void*
     return SWEDG_OK;
 }
 
+// The caller detaches (swedg_set_nccl_comm(h, NULL)) or destroys every handle using
+// the communicator first: their captured graphs hold NCCL work of this comm.
 int swedg_nccl_comm_destroy(void* comm) {
     if (!comm) return SWEDG_OK;
     NcclApi& api = nccl_api();

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <barrier>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -30,6 +31,7 @@
 static int failures = 0;
 static void check(bool ok, const std::string& what) {
     std::printf("%s %s\n", ok ? "PASS" : "FAIL", what.c_str());
+    std::fflush(stdout);
     if (!ok) ++failures;
 }
 
@@ -235,16 +237,23 @@ static void nccl_self(int N) {
     }
     check(u.size() == ug.size() && std::memcmp(u.data(), ug.data(), u.size() * 8) == 0,
           "N=" + std::to_string(N) + " one-rank NCCL self exchange across the periodic cut == global, bitwise");
+    swedg_b200::set_nccl_comm(sops, nullptr);  // drops the captured graph (NCCL work) before the comm goes
     swedg_nccl_comm_destroy(comm);
 }
 
 int main(int argc, char** argv) {
-    const bool skip_nccl = argc > 1 && std::string(argv[1]) == "--no-nccl";
+    std::setvbuf(stdout, nullptr, _IOLBF, 0);
+    // multirank_test [--no-nccl | --nccl-only N...]
+    const std::string mode = argc > 1 ? argv[1] : "";
     try {
-        for (int N : {3, 4})
-            for (int P : {1, 2, 3}) logical_partitions(N, P);
-        if (!skip_nccl)
-            for (int N : {3, 4}) nccl_self(N);
+        if (mode == "--nccl-only") {
+            for (int a = 2; a < argc; ++a) nccl_self(std::atoi(argv[a]));
+        } else {
+            for (int N : {3, 4})
+                for (int P : {1, 2, 3}) logical_partitions(N, P);
+            if (mode != "--no-nccl")
+                for (int N : {3, 4}) nccl_self(N);
+        }
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         ++failures;

@@ -223,11 +223,11 @@ def test_nccl_self_exchange_single_rank_graph():
             h.step(dt, 3)  # graph capture + replay
             h.step(dt, 1)  # individual launches
             u, _, t = h.get_state()
-            np.testing.assert_array_equal(u, ug)
-            assert t == tg
-            h.close()
         finally:
+            h.close()  # the handle's captured graph holds NCCL work: it goes before the comm
             capi.nccl_comm_destroy(comm)
+        np.testing.assert_array_equal(u, ug)
+        assert t == tg
 
 
 @pytest.mark.gpu
