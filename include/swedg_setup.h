@@ -42,7 +42,17 @@ typedef struct {
                         rows + face halos of the two cuts (swedg_case_fill_halo);
                         strip == -1: the whole global mesh in one piece (tests) */
     int partition;   /* SWEDG_PARTITION_*; NONE with strips > 1 = WEAK (ABI v3 behaviour) */
+    /* SBP volume rule (sbp_rule, quadrature.hpp:320-343): Gauss-Legendre edges come from
+     * the built-in tables; Gauss-Lobatto edges only from sbp_lobatto_N<N>.txt in
+     * sbp_data_dir (NULL: the working directory); sbp_rule_file (non-NULL) loads that
+     * file for either family (load_sbp_rule_file, quadrature.hpp:290-318). */
+    int sbp_family;              /* SWEDG_SBP_LEGENDRE / SWEDG_SBP_LOBATTO */
+    const char* sbp_data_dir;
+    const char* sbp_rule_file;
 } swedg_case_config;
+
+#define SWEDG_SBP_LEGENDRE 0
+#define SWEDG_SBP_LOBATTO 1
 
 #define SWEDG_PARTITION_NONE 0
 #define SWEDG_PARTITION_WEAK 1   /* P strips of ny rows: global nx x (ny P) mesh, domain stretched P times in y */
@@ -59,6 +69,13 @@ int swedg_case_build_mesh(const swedg_case_config* cfg, const double* verts, int
                           const int* wall_faces, int nw, const double* domain, int periodic_x, int periodic_y,
                           swedg_case* out);
 int swedg_case_destroy(swedg_case c);
+/* load_sbp_rule_file / sbp_rule on their own (the rule a case would use): nq volume
+ * nodes x[nq], y[nq], w[nq] (arrays of max_nodes), npf, face_index[3 npf] (surface slot ->
+ * volume node).  Errors (missing file, header mismatch, non-embedding, nonpositive
+ * weight, exactness) return SWEDG_ERR_INVALID with the reference's message in
+ * swedg_case_error(). */
+int swedg_sbp_rule(int N, int family, const char* data_dir, const char* rule_file, int max_nodes, int* nq,
+                   int* npf, double* x, double* y, double* w, int* face_index);
 const char* swedg_case_error(void);
 /* Fill every operator/geometry/connectivity pointer and size of *d (penalty,
  * mode and device are left for the caller). */

@@ -637,7 +637,11 @@ class _CaseCfg(C.Structure):
     _fields_ = [("problem", C.c_int), ("scheme", C.c_int), ("N", C.c_int), ("nx", C.c_int),
                 ("ny", C.c_int), ("warp", C.c_double), ("cfl", C.c_double), ("g", C.c_double),
                 ("seed", C.c_uint), ("threads", C.c_int), ("strips", C.c_int), ("strip", C.c_int),
-                ("partition", C.c_int)]
+                ("partition", C.c_int), ("sbp_family", C.c_int), ("sbp_data_dir", C.c_char_p),
+                ("sbp_rule_file", C.c_char_p)]
+
+SBP_LEGENDRE = 0
+SBP_LOBATTO = 1
 
 
 PARTITION_NONE = 0
@@ -662,6 +666,7 @@ def _setup_lib():
         L.swedg_case_min_edge.argtypes = [vp]
         L.swedg_case_min_edge.restype = C.c_double
         L.swedg_case_K.argtypes = [vp]
+        L.swedg_sbp_rule.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_int, _ip, _ip, _dp, _dp, _dp, _ip]
         L.swedg_case_build_mesh.argtypes = [C.POINTER(_CaseCfg), _dp, C.c_int, _ip, C.c_int, _ip, C.c_int, _dp,
                                             C.c_int, C.c_int, C.POINTER(vp)]
         L._setup_bound = True
@@ -672,7 +677,8 @@ class Case:
     """A problem built by the native setup (lake / vortex / dambreak / smooth)."""
 
     def __init__(self, problem="smooth", *, scheme=SCHEME_HYBRIDIZED, N=4, nx=16, ny=None,
-                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0, scaling=None, mesh=None):
+                 warp=0.0, cfl=0.125, g=0.0, seed=23, threads=0, strips=1, strip=0, scaling=None, mesh=None,
+                 sbp_family=SBP_LEGENDRE, sbp_data_dir=None, sbp_rule_file=None):
         """Partitioned meshes: rank `strip`'s y-strip of P = strips, with face halos of the two
         cuts (halo_desc()).  scaling "weak": P strips of ny rows of a global nx x (ny P) mesh on
         the problem's domain stretched P times in y (fixed work per rank; the default when
@@ -689,6 +695,9 @@ class Case:
         cfg.warp, cfg.cfl, cfg.g, cfg.seed, cfg.threads = warp, cfl, g, seed, threads
         cfg.strips, cfg.strip = strips, strip
         cfg.partition = {None: PARTITION_NONE, "weak": PARTITION_WEAK, "strong": PARTITION_STRONG}[scaling]
+        cfg.sbp_family = sbp_family
+        cfg.sbp_data_dir = sbp_data_dir.encode() if sbp_data_dir else None
+        cfg.sbp_rule_file = sbp_rule_file.encode() if sbp_rule_file else None
         h = C.c_void_p()
         if mesh is None:
             rc = L.swedg_case_build(C.byref(cfg), C.byref(h))
@@ -781,6 +790,24 @@ class Case:
             self.close()
         except Exception:
             pass
+
+
+def sbp_rule(N: int, family: int = SBP_LEGENDRE, data_dir: str | None = None, rule_file: str | None = None):
+    """sbp_rule / load_sbp_rule_file (quadrature.hpp:290-343) through the native setup:
+    dict(x, y, w, npf, face_index).  Raises InvalidArgument with the reference's message."""
+    L = _setup_lib()
+    mx = 512
+    x, y, w = np.zeros(mx), np.zeros(mx), np.zeros(mx)
+    fi = np.zeros(mx, dtype=np.int32)
+    nq, npf = C.c_int(), C.c_int()
+    rc = L.swedg_sbp_rule(int(N), int(family), data_dir.encode() if data_dir else None,
+                          rule_file.encode() if rule_file else None, mx, C.byref(nq), C.byref(npf), _p(x), _p(y),
+                          _p(w), _pi(fi))
+    if rc != SWEDG_OK:
+        raise _err_class(rc)(rc, L.swedg_case_error().decode())
+    n = nq.value
+    return {"x": x[:n].copy(), "y": y[:n].copy(), "w": w[:n].copy(), "npf": npf.value,
+            "face_index": fi[:3 * npf.value].copy()}
 
 
 def _handle_from_desc(cls, desc, owner, *, penalty=PENALTY_LF, mode=MODE_FAST, device=0, b=None):

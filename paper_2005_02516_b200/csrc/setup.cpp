@@ -12,10 +12,12 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <functional>
 #include <map>
 #include <mutex>
 #include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -451,26 +453,99 @@ struct SbpOps {
     std::vector<int> face_index;
 };
 
-// sbp_rule + build_traditional_sbp (quadrature.hpp:248-288, refelem.hpp:224-274)
-void build_sbp(int N, RefOps& ref, SbpOps& s) {
-    const quad_data::RuleView* view = nullptr;
-    for (const auto& v : quad_data::sbp_rules)
-        if (v.key == N) view = &v;
-    if (!view) throw std::runtime_error("SBP rule unavailable for (N=" + std::to_string(N) + ", legendre)");
-    Rule2D vol;
-    for (int i = 0; i < view->n; ++i) {
-        vol.x.push_back(view->data[i][0]);
-        vol.y.push_back(view->data[i][1]);
-        vol.w.push_back(view->data[i][2]);
+// Gauss-Lobatto nodes/weights on [-1,1] (quadrature.hpp:145-177): Newton on P'_{n-1}
+void gauss_lobatto(int n, std::vector<double>& x, std::vector<double>& w) {
+    if (n < 2) throw std::invalid_argument("Lobatto rule needs >= 2 points");
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    auto legendre = [n](double t, double& p, double& dp) {
+        double p0 = 1.0, p1 = t;
+        for (int k = 2; k <= n - 1; ++k) {
+            double p2 = ((2 * k - 1) * t * p1 - (k - 1) * p0) / k;
+            p0 = p1;
+            p1 = p2;
+        }
+        p = p1;
+        dp = (n - 1) * (t * p1 - p0) / (t * t - 1.0);
+    };
+    for (int i = 0; i < n; ++i) {
+        double t = -std::cos(M_PI * i / (n - 1));
+        if (i > 0 && i < n - 1)
+            for (int it = 0; it < 100; ++it) {
+                double p, dp;
+                legendre(t, p, dp);
+                const double d2p = (2.0 * t * dp - n * (n - 1) * p) / (1.0 - t * t);
+                const double dt = dp / d2p;
+                t -= dt;
+                if (std::abs(dt) < 1e-15) break;
+            }
+        double p, dp;
+        legendre(t, p, dp);
+        x[i] = t;
+        w[i] = 2.0 / (n * (n - 1) * p * p);
     }
-    SurfRule surf = surface_rule(view->npf);
-    std::vector<int> fidx(surf.size());
+}
+
+// surface_rule_1d (quadrature.hpp:180-207): a caller-chosen 1D family on every face
+SurfRule surface_rule_1d(int npf, int family, int* degree) {
+    if (family == SWEDG_SBP_LEGENDRE) {
+        SurfRule s = surface_rule(npf);
+        *degree = 2 * npf - 1;
+        return s;
+    }
+    std::vector<double> r1, w1;
+    gauss_lobatto(npf, r1, w1);
+    *degree = 2 * npf - 3;
+    SurfRule s;
+    s.npf = npf;
+    for (int f = 0; f < 3; ++f)
+        for (int k = 0; k < npf; ++k) {
+            double x, y;
+            face_point(f, r1[k], x, y);
+            s.x.push_back(x);
+            s.y.push_back(y);
+            s.w.push_back(w1[k] * kFaceJac[f]);
+            s.face.push_back(f);
+        }
+    return s;
+}
+
+// verify_exactness (quadrature.hpp:91-108) against the exact monomial integrals (:72-77)
+double exactness_error(const Rule2D& q, int degree) {
+    if (q.size() == 0) throw std::invalid_argument("empty quadrature rule");
+    auto I = [](int m) { return m % 2 == 0 ? 2.0 / (m + 1) : 0.0; };
+    double err = 0.0;
+    for (int d = 0; d <= degree; ++d)
+        for (int i = 0; i <= d; ++i) {
+            const int j = d - i;
+            double approx = 0.0;
+            for (int k = 0; k < q.size(); ++k) approx += q.w[k] * std::pow(q.x[k], i) * std::pow(q.y[k], j);
+            const double exact = ((i % 2 == 0) ? -1.0 : 1.0) / (i + 1) * (I(i + j + 1) - I(j));
+            err = std::max(err, std::abs(approx - exact));
+        }
+    return err;
+}
+
+// An SBP volume rule with its embedded surface rule (make_sbp, quadrature.hpp:248-288)
+struct SbpRule {
+    Rule2D vol;
+    SurfRule surf;
+    std::vector<int> fidx;
+};
+
+SbpRule make_sbp(int N, int family, const Rule2D& vol, int npf) {
+    SbpRule r;
+    r.vol = vol;
+    int sdeg = 0;
+    r.surf = surface_rule_1d(npf, family, &sdeg);
+    if (sdeg < 2 * N) throw std::runtime_error("SBP surface rule exactness below 2N");
+    r.fidx.assign(r.surf.size(), -1);
     std::vector<char> used(vol.size(), 0);
-    for (int i = 0; i < surf.size(); ++i) {
+    for (int i = 0; i < r.surf.size(); ++i) {
         int best = -1;
         double bestd = 1e100;
         for (int j = 0; j < vol.size(); ++j) {
-            double d = std::hypot(surf.x[i] - vol.x[j], surf.y[i] - vol.y[j]);
+            const double d = std::hypot(r.surf.x[i] - vol.x[j], r.surf.y[i] - vol.y[j]);
             if (d < bestd) {
                 bestd = d;
                 best = j;
@@ -478,8 +553,69 @@ void build_sbp(int N, RefOps& ref, SbpOps& s) {
         }
         if (bestd > 1e-12 || used[best]) throw std::runtime_error("SBP surface node does not embed in volume rule");
         used[best] = 1;
-        fidx[i] = best;
+        r.fidx[i] = best;
     }
+    for (int i = 0; i < vol.size(); ++i)
+        if (vol.w[i] <= 0.0) throw std::runtime_error("SBP rule has nonpositive weight");
+    if (exactness_error(vol, 2 * N - 1) > 1e-12) throw std::runtime_error("SBP volume rule failed exactness check");
+    return r;
+}
+
+// load_sbp_rule_file (quadrature.hpp:290-318): header "degree=<d> nodes_per_face=<m>",
+// then one node per line "x y w", the first 3m nodes being the face nodes face-major
+SbpRule load_sbp_rule_file(const std::string& path, int N, int family) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("SBP rule unavailable: cannot open " + path);
+    std::string header;
+    std::getline(in, header);
+    int deg = -1, npf = -1;
+    {
+        std::istringstream hs(header);
+        std::string tok;
+        while (hs >> tok) {
+            if (tok.rfind("degree=", 0) == 0) deg = std::stoi(tok.substr(7));
+            if (tok.rfind("nodes_per_face=", 0) == 0) npf = std::stoi(tok.substr(15));
+        }
+    }
+    if (deg < 2 * N - 1 || npf < N + 1) throw std::runtime_error("SBP rule file header mismatch for " + path);
+    Rule2D vol;
+    double a, b, c;
+    while (in >> a >> b >> c) {
+        vol.x.push_back(a);
+        vol.y.push_back(b);
+        vol.w.push_back(c);
+    }
+    return make_sbp(N, family, vol, npf);
+}
+
+// sbp_rule (quadrature.hpp:320-343): Gauss-Legendre edges from the tables, Gauss-Lobatto
+// edges only from a data file sbp_lobatto_N<N>.txt (in data_dir, or the working directory);
+// rule_file overrides both (the caller's own rule in the file format above)
+SbpRule sbp_rule(int N, int family, const std::string& data_dir, const std::string& rule_file) {
+    if (!rule_file.empty()) return load_sbp_rule_file(rule_file, N, family);
+    if (family == SWEDG_SBP_LEGENDRE) {
+        for (const auto& v : quad_data::sbp_rules)
+            if (v.key == N) {
+                Rule2D vol;
+                for (int i = 0; i < v.n; ++i) {
+                    vol.x.push_back(v.data[i][0]);
+                    vol.y.push_back(v.data[i][1]);
+                    vol.w.push_back(v.data[i][2]);
+                }
+                return make_sbp(N, family, vol, v.npf);
+            }
+        throw std::runtime_error("SBP rule unavailable for (N=" + std::to_string(N) + ", legendre)");
+    }
+    const std::string name = "sbp_lobatto_N" + std::to_string(N) + ".txt";
+    return load_sbp_rule_file(data_dir.empty() ? name : data_dir + "/" + name, N, family);
+}
+
+// build_traditional_sbp (refelem.hpp:224-274): the congruence of the hybridized
+// operators onto the volume nodes
+void build_sbp(int N, RefOps& ref, SbpOps& s, const SbpRule& rule) {
+    const Rule2D& vol = rule.vol;
+    const SurfRule& surf = rule.surf;
+    const std::vector<int>& fidx = rule.fidx;
     ref = build_ref_ops(N, vol, surf);
     int nq = vol.size(), nf = surf.size();
     auto congruence = [&](const Mat& Qh) {
@@ -1083,7 +1219,9 @@ void build_case(swedg_case_s& c) {
     if (cfg.scheme == SWEDG_SCHEME_HYBRIDIZED) {
         c.ref = build_ref_ops(cfg.N, volume_rule_by_degree(2 * cfg.N), surface_rule(cfg.N + 1));
     } else {
-        build_sbp(cfg.N, c.ref, c.sbp);
+        build_sbp(cfg.N, c.ref, c.sbp,
+                  sbp_rule(cfg.N, cfg.sbp_family, cfg.sbp_data_dir ? cfg.sbp_data_dir : "",
+                           cfg.sbp_rule_file ? cfg.sbp_rule_file : ""));
     }
     const RefOps& R = c.ref;
     c.Np = R.Np;
@@ -1318,6 +1456,28 @@ int swedg_case_build(const swedg_case_config* cfg, swedg_case* out) {
         return SWEDG_ERR_INVALID;
     }
     *out = c;
+    return SWEDG_OK;
+}
+
+int swedg_sbp_rule(int N, int family, const char* data_dir, const char* rule_file, int max_nodes, int* nq,
+                   int* npf, double* x, double* y, double* w, int* face_index) {
+    try {
+        if (family != SWEDG_SBP_LEGENDRE && family != SWEDG_SBP_LOBATTO) throw std::invalid_argument("unknown SBP family");
+        SbpRule r = sbp_rule(N, family, data_dir ? data_dir : "", rule_file ? rule_file : "");
+        if (nq) *nq = r.vol.size();
+        if (npf) *npf = r.surf.npf;
+        if (r.vol.size() > max_nodes) throw std::invalid_argument("rule larger than max_nodes");
+        for (int i = 0; i < r.vol.size(); ++i) {
+            if (x) x[i] = r.vol.x[i];
+            if (y) y[i] = r.vol.y[i];
+            if (w) w[i] = r.vol.w[i];
+        }
+        if (face_index)
+            for (size_t i = 0; i < r.fidx.size(); ++i) face_index[i] = r.fidx[i];
+    } catch (const std::exception& e) {
+        g_case_error = e.what();
+        return SWEDG_ERR_INVALID;
+    }
     return SWEDG_OK;
 }
 
