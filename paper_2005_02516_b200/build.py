@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libswedg_b200.so")
 SOURCES = ["swedg_capi.cu", "setup.cpp"]
-DEPS = ["swedg_capi.cu", "swedg_common.cuh", "modal_kernels.cuh", "modal_fast.cuh", "modal_warp_n4.cuh", "modal_quad_n4.cuh", "modal_pair_n4.cuh", "modal_pair_n3.cuh", "sbp_kernels.cuh", "setup.cpp", "quad_data.inc"]
+DEPS = ["swedg_capi.cu", "swedg_common.cuh", "modal_kernels.cuh", "modal_fast.cuh", "modal_pair_n4.cuh", "modal_pair_n3.cuh", "sbp_kernels.cuh", "sbp_pair_n4.cuh", "halo.cuh", "setup.cpp", "quad_data.inc"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

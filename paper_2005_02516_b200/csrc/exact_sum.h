@@ -93,8 +93,8 @@ SWEDG_HD void compact(int64_t* L) {
     L[kLimbs - 1] += carry;
 }
 
-// Correctly rounded (nearest, ties to even) double of the accumulator.
-// Magnitudes below 2^-1022 (subnormal totals) are rounded through ldexp.
+// Correctly rounded (nearest, ties to even) double of the accumulator, subnormal
+// totals included (rounded once, at 2^-1074).
 inline double to_double(const int64_t* acc) {
     int64_t L[kLimbs];
     for (int j = 0; j < kLimbs; ++j) L[j] = acc[j];
@@ -117,22 +117,23 @@ inline double to_double(const int64_t* acc) {
     int base = 32 * (t - 2) - 1074;  // x * 2^base
     int nb = 0;
     for (unsigned __int128 y = x; y; y >>= 1) ++nb;
+    // round at the lsb of a 53-bit mantissa, or at 2^-1074 when the total is subnormal
+    // (one rounding: ldexp below is then exact)
+    int sh = nb > 53 ? nb - 53 : 0;
+    if (base + sh < -1074) sh = -1074 - base;
     uint64_t mant;
-    int ex;
-    if (nb > 53) {
-        const int sh = nb - 53;
+    int ex = base + sh;
+    if (sh > 0) {
         mant = static_cast<uint64_t>(x >> sh);
         const unsigned __int128 rem = x & ((static_cast<unsigned __int128>(1) << sh) - 1);
         const unsigned __int128 half = static_cast<unsigned __int128>(1) << (sh - 1);
         if (rem > half || (rem == half && (sticky || (mant & 1)))) ++mant;
-        ex = base + sh;
         if (mant == (1ull << 53)) {
             mant >>= 1;
             ++ex;
         }
     } else {
         mant = static_cast<uint64_t>(x);  // exact (t < 2: every digit is in x)
-        ex = base;
     }
     double r = __builtin_ldexp(static_cast<double>(mant), ex);
     return neg ? -r : r;

@@ -19,36 +19,9 @@
 
 #include <stdint.h>
 
-#include "modal_quad_n4.cuh"
+#include "modal_kernels.cuh"
 
 namespace swedg {
-
-// mbarrier + bulk (TMA engine, no tensor map) copy helpers
-__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_u32(mb)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr_u32(mb)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_addr_u32(mb)),
-        "r"(parity)
-        : "memory");
-}
-// global -> shared bulk copy (TMA engine, no tensor map): bytes and both addresses 16 B multiples
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr_u32(mb))
-                 : "memory");
-}
 
 // One stacked row's state in the flux loops.  The EC-flux accumulation is
 // factored so a pair costs 17 FP64 instructions instead of 23: with
@@ -82,29 +55,6 @@ __device__ __forceinline__ void row_finish(Row6& r, const double ui, const doubl
     r.a2 = __fma_rn(gh4, r.b2, __fma_rn(vi, r.a0, r.a2));
 }
 
-// Fused stage launch (opt-in, SWEDG_FUSION=1): the interface/lift/M^-1/RK-update
-// phase of stage s-1 (the arithmetic of modal_surface_kernel<4,false>) followed,
-// for the same element pair in the same warp, by the projection + volume phase of
-// stage s; the updated u feeds the projection from shared memory and a step needs
-// 6 launches instead of 10.  Traces are double-buffered by stage parity.  The
-// hoped-for overlap of the memory-bound interface phase with other warps' FP64
-// work does not happen (measured 2 % slower at C4): the volume phase needs every
-// warp slot to keep the FP64 pipe at 65 %, and the warps stay phase-locked.
-struct PairStageParams {
-    ModalVolParams v;          // volume phase, stage s (v.u read only when !do_surface)
-    int do_surface, do_volume;
-    int lf;
-    const double* trace_in;    // [K][3][nf] traces of stage s-1
-    const double* surf;        // [K][3][nf]: w*sJ, nx, ny
-    const int* nbr;            // [K][3]
-    const int* perm;           // [K][nf]
-    const double* Mpk;         // [K][120] packed symmetric M_h^{-1}
-    double* u;                 // state, updated by the interface phase
-    double* res;               // LSRK register
-    double rk_a, rk_b, dt;     // stage s-1 coefficients
-    unsigned stage_prev;       // stage id of s-1 (non-finite RHS reports)
-};
-
 #ifndef SWEDG_PAIR_WARPS
 #define SWEDG_PAIR_WARPS 16  // warps per CTA (one CTA per SM): 512 threads cap registers at 128
 #endif
@@ -135,19 +85,11 @@ struct PairN4 {
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
 };
 
-// S = true: the fused interface+volume instantiation (ps.do_surface / ps.do_volume
-// select the phases); S = false: the volume-only kernel of the split stage.
-template <bool S>
-#ifdef SWEDG_PAIR_MAXNREG  // register cap below the 1-CTA/SM limit (co-residency experiments)
-__global__ void __maxnreg__(SWEDG_PAIR_MAXNREG)
-#else
 __global__ void __launch_bounds__(PairN4::T, 1)
-#endif
-modal_volume_pair_n4_kernel(PairStageParams ps) {
+modal_volume_pair_n4_kernel(ModalVolParams prm) {
     using W = PairN4;
     using O = ModalOps<4>;
-    constexpr int Np = W::Np, nq = W::nq, nf = W::nf, nh = W::nh, npf = 5;
-    const ModalVolParams& prm = ps.v;
+    constexpr int Np = W::Np, nq = W::nq, nf = W::nf, nh = W::nh;
 
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
@@ -236,11 +178,8 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
     const int npairs = (prm.K + 1) / 2;
     const int gw = blockIdx.x * W::WARPS + warp, nw = gridDim.x * W::WARPS;
 
-    const bool do_surface = S && ps.do_surface;
-    const bool do_volume = !S || ps.do_volume;
-    const bool with_u = !do_surface;  // otherwise u comes from the interface phase
     const bool bulk_ok = ((reinterpret_cast<uintptr_t>(prm.gf) | reinterpret_cast<uintptr_t>(prm.bs) |
-                           (with_u ? reinterpret_cast<uintptr_t>(prm.u) : 0)) & 15u) == 0;
+                           reinterpret_cast<uintptr_t>(prm.u)) & 15u) == 0;
     // the pair's u/gf/b: three bulk (TMA) copies of contiguous pair blocks by lane 0
     // (k0 even: every block is 16 B aligned), completion on the warp's mbarrier
     auto issue = [&](int pr) {
@@ -248,14 +187,14 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         if (k0 + 1 < prm.K && bulk_ok) {
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive_tx(mb, 8u * ((with_u ? 90 : 0) + 320 + 80));
-                if (with_u) bulk_g2s(stage + W::sU, prm.u + (size_t)k0 * 3 * Np, 8u * 90, mb);
+                mbar_arrive_tx(mb, 8u * (90 + 320 + 80));
+                bulk_g2s(stage + W::sU, prm.u + (size_t)k0 * 3 * Np, 8u * 90, mb);
                 bulk_g2s(stage + W::sG, prm.gf + (size_t)k0 * 4 * nh, 8u * 320, mb);
                 bulk_g2s(stage + W::sB, prm.bs + (size_t)k0 * nh, 8u * 80, mb);
             }
         } else if (k0 < prm.K) {  // odd K (last element alone) or unaligned base pointers: plain loads
             const int ne = k0 + 1 < prm.K ? 2 : 1;
-            for (int r = lane; with_u && r < 45 * ne; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
+            for (int r = lane; r < 45 * ne; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
             for (int r = lane; r < 160 * ne; r += 32) stage[W::sG + r] = prm.gf[(size_t)k0 * 160 + r];
             for (int r = lane; r < 40 * ne; r += 32) stage[W::sB + r] = prm.bs[(size_t)k0 * 40 + r];
             __syncwarp();
@@ -263,13 +202,13 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
         }
     };
 
-    if (gw < npairs && do_volume) issue(gw);
+    if (gw < npairs) issue(gw);
     uint32_t phase = 0;
     for (int pr = gw; pr < npairs; pr += nw, phase ^= 1) {
         const int k = 2 * pr + half;
         const bool valid = k < prm.K;
         // ---- park: staging -> work (u, b, g pairs), freeing the staging for the next pair
-        if (do_volume) {
+        {
             mbar_wait(mb, phase);
             const double* su = stage + W::sU + 45 * half;
             const double* sg = stage + W::sG + 160 * half;
@@ -290,7 +229,7 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
                 const int r = lp + 16 * t;
-                if (with_u && r < 45) work[W::wU + r] = pu[t];
+                if (r < 45) work[W::wU + r] = pu[t];
                 if (r < nh) {
                     work[W::wBs + r] = pb[t];
                     reinterpret_cast<double2*>(work + W::wC)[r] = make_double2(p1[t], p2[t]);
@@ -299,126 +238,9 @@ modal_volume_pair_n4_kernel(PairStageParams ps) {
             }
         }
         __syncwarp();
-        if (pr + nw < npairs && do_volume) issue(pr + nw);
+        if (pr + nw < npairs) issue(pr + nw);
         if (valid && lp < 5)  // L2 prefetch of this element's source rows (read after the flux loops)
             asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(prm.src + (size_t)k * 2 * nh) + 128 * lp));
-
-        // ---- interface phase of stage s-1 (modal_surface_kernel<4,false> arithmetic):
-        //      lane l' < 15 = surface slot l' and modal coefficient l' of its element
-        if (do_surface) {
-            const double gS = prm.g;
-            const int s_ = lp < nf ? lp : nf - 1;
-            const bool act = valid && lp < nf;
-            // front-load every independent global read of the lane
-            double ui[3] = {1.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, t1r[3] = {0.0, 0.0, 0.0};
-            double ur[3] = {0.0, 0.0, 0.0}, rr[3] = {0.0, 0.0, 0.0};
-            double m = 0.0, nxi = 0.0, nyi = 0.0, srx = 0.0, sry = 0.0;
-            int nb = -1, jn = 0;
-            if (act) {
-                const size_t ot = (size_t)k * 3 * nf + s_;
-                const size_t om = (size_t)k * 3 * Np + s_;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    ui[c] = ps.trace_in[ot + c * nf];
-                    acc[c] = prm.accf[ot + c * nf];
-                    t1r[c] = prm.T1[om + c * Np];
-                    ur[c] = ps.u[om + c * Np];
-                    rr[c] = ps.res[om + c * Np];
-                }
-                m = ps.surf[ot];
-                nxi = ps.surf[ot + nf];
-                nyi = ps.surf[ot + 2 * nf];
-                srx = prm.src[(size_t)k * 2 * nh + nq + s_];
-                sry = prm.src[(size_t)k * 2 * nh + nh + nq + s_];
-                nb = ps.nbr[(size_t)k * 3 + s_ / npf];
-                jn = ps.perm[(size_t)k * nf + s_];
-            }
-            // packed M_h^{-1} of the pair (2 x 120 contiguous doubles) -> work[wV..]
-            {
-                const int k0 = 2 * pr;
-                const int ne = k0 + 1 < prm.K ? 2 : 1;
-                const double* gm = ps.Mpk + (size_t)k0 * 120;
-                double* w0 = wbase;
-                for (int x = lane; x < ne * 120; x += 32) {
-                    const int e = x >= 120, r = x - 120 * e;
-                    w0[e * W::work_stride + W::wV + r] = gm[x];
-                }
-            }
-            double up[3] = {ui[0], ui[1], ui[2]};
-            if (act) {
-                if (nb < 0) {  // wall_ghost (swe.hpp:102-105)
-                    const double un = ui[1] * nxi + ui[2] * nyi;
-                    up[1] = ui[1] - 2.0 * un * nxi;
-                    up[2] = ui[2] - 2.0 * un * nyi;
-                } else {
-                    const double* tn = ps.trace_in + (size_t)nb * 3 * nf + jn;
-                    up[0] = tn[0];
-                    up[1] = tn[nf];
-                    up[2] = tn[2 * nf];
-                }
-                const double Bx = m * nxi, By = m * nyi;
-                {  // ec_flux_xy(u+, u)
-                    const double uxa = up[1] / up[0], uya = up[2] / up[0];
-                    const double uxb = ui[1] / ui[0], uyb = ui[2] / ui[0];
-                    const double h_avg = 0.5 * (up[0] + ui[0]);
-                    const double p = gS * h_avg * h_avg - 0.25 * gS * (up[0] * up[0] + ui[0] * ui[0]);
-                    const double ux = 0.5 * (uxa + uxb), uy = 0.5 * (uya + uyb);
-                    const double hu = 0.5 * (up[1] + ui[1]), hv = 0.5 * (up[2] + ui[2]);
-                    const double fx[3] = {hu, hu * ux + p, hu * uy};
-                    const double fy[3] = {hv, hv * ux, hv * uy + p};
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[c] = acc[c] + (Bx * fx[c] + By * fy[c]);
-                }
-                if (ps.lf) {  // lf_penalty(u, u+) (swe.hpp:87-99)
-                    const double wl = fabs((ui[1] * nxi + ui[2] * nyi) / ui[0]) + sqrt(gS * ui[0]);
-                    const double wr = fabs((up[1] * nxi + up[2] * nyi) / up[0]) + sqrt(gS * up[0]);
-                    const double lam = (wl < wr) ? wr : wl;
-                    const double hl = 0.5 * lam;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[c] = acc[c] - m * (hl * (up[c] - ui[c]));
-                }
-                const double mgh = -gS * ui[0];
-                work[W::wA + s_] = 0.0 - acc[0];
-                work[W::wA + nf + s_] = mgh * srx - acc[1];
-                work[W::wA + 2 * nf + s_] = mgh * sry - acc[2];
-            }
-            __syncwarp();
-            // modal = T1 + Vf^T stacked_surface (solver.hpp:285-286)
-            if (act) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    double t2 = 0.0;
-#pragma unroll
-                    for (int i = 0; i < nf; ++i) t2 = __fma_rn(sVf[i + s_ * nf], work[W::wA + c * nf + i], t2);
-                    work[W::wB + c * Np + s_] = t1r[c] + t2;
-                }
-            }
-            __syncwarp();
-            // du = M_h^{-1} modal; finiteness; LSRK45 register update
-            if (act) {
-                double du[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-                for (int mm = 0; mm < Np; ++mm) {
-                    const int a = s_ < mm ? s_ : mm, b = s_ < mm ? mm : s_;
-                    const double mv = work[W::wV + a * Np - a * (a - 1) / 2 + (b - a)];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) du[c] = __fma_rn(mv, work[W::wB + c * Np + mm], du[c]);
-                }
-                if (!(isfinite(du[0]) && isfinite(du[1]) && isfinite(du[2])))
-                    record_error(prm.err, ps.stage_prev, 1, prm.k_base + k);
-                const size_t om = (size_t)k * 3 * Np + s_;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const double r = __fma_rn(ps.rk_a, rr[c], ps.dt * du[c]);
-                    const double un = __fma_rn(ps.rk_b, r, ur[c]);
-                    ps.res[om + c * Np] = r;
-                    ps.u[om + c * Np] = un;
-                    work[W::wU + c * Np + s_] = un;
-                }
-            }
-            __syncwarp();
-        }
-        if (!do_volume) continue;
 
         // ---- entropy variables at volume points rA (all) and rB (< 25)
         {

@@ -20,8 +20,6 @@
 #include "../../include/swedg_b200.h"
 #include "modal_kernels.cuh"
 #include "modal_fast.cuh"
-#include "modal_warp_n4.cuh"
-#include "modal_quad_n4.cuh"
 #include "modal_pair_n4.cuh"
 #include "modal_pair_n3.cuh"
 #include "sbp_kernels.cuh"
@@ -51,10 +49,6 @@ struct swedg_handle_s {
     double g;
     int device;
     int nsm = 148;
-    // FAST volume kernel (env SWEDG_VOLUME_KERNEL): 0 = default (N=4: "pair", 2 elements/warp,
-    // TMEM operators), 1 = "tworow", 2 = "row", 3 = "warp" (N=4, warp/element, TMEM),
-    // 4 = "quad" (N=4, 4 elements/warp; measured slower: latency-bound at 6 warps/SM)
-    int vol_variant = 0;
     // programmatic dependent launch (SWEDG_PDL bit mask): 1 modal pair volume kernel,
     // 2 modal interface kernel, 4 SBP pair kernel.  Default 1|4: measured, PDL on the
     // interface kernel costs ~2 ms per C4 step (device-resident and chunked alike)
@@ -80,12 +74,6 @@ struct swedg_handle_s {
     double* du = nullptr;    // host-API scratch rhs
     double* proj = nullptr;  // host-API scratch projection
     double* trace = nullptr; // [K][3][nf]
-    double* trace2 = nullptr; // second trace buffer (fused stage chain: traces double-buffered by stage parity)
-    // FAST N=4 single rank: fused interface(s-1) + volume(s) launches, opt-in (env
-    // SWEDG_FUSION=1).  Measured 2 % slower than the split launches at C4 (39.6 vs
-    // 38.8 ms/step): the interface phase takes warp slots the FP64-latency-bound
-    // volume phase needs, and the warps stay phase-locked, so nothing overlaps.
-    bool fusion = false;
     double* accf = nullptr;  // [K][3][nf]
     double* T1 = nullptr;    // [K][3][Np]
     ErrRec* err = nullptr;
@@ -286,12 +274,13 @@ int kernel_occupancy(const void* kern, int device, int threads, size_t smem) {
     return occ;
 }
 
-void launch_pair(swedg_handle h, const PairStageParams& ps) {
-    auto kern = ps.do_surface ? modal_volume_pair_n4_kernel<true> : modal_volume_pair_n4_kernel<false>;
-    const size_t psm = PairN4::bytes();
-    const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
-    const int grid = std::min((ps.v.K + 2 * PairN4::WARPS - 1) / (2 * PairN4::WARPS), occ * h->nsm);
-    launch_pdl(kern, std::max(grid, 1), PairN4::T, psm, h->stream, (h->pdl_mask & 1) != 0, ps);
+// Pair kernels (N = 4, 3): persistent CTAs (one per SM), two elements per warp.
+template <class Cfg>
+void launch_pair(swedg_handle h, void (*kern)(ModalVolParams), const ModalVolParams& vp) {
+    const size_t psm = Cfg::bytes();
+    const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, Cfg::T, psm);
+    const int grid = std::min((vp.K + 2 * Cfg::WARPS - 1) / (2 * Cfg::WARPS), occ * h->nsm);
+    launch_pdl(kern, std::max(grid, 1), Cfg::T, psm, h->stream, (h->pdl_mask & 1) != 0, vp);
 }
 
 // the SBP pair kernel bulk-copies (TMA) per-pair blocks: every source must be 16 B aligned
@@ -348,35 +337,13 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
     };
     {
         KTimer kt(h, 0);
-        if (h->mode == SWEDG_MODE_PARITY) {
+        if (h->mode == SWEDG_MODE_PARITY) {  // reference evaluation order, row per thread
             launch_vol(modal_volume_kernel<N, true>);
-        } else if (N == 4 && h->vol_variant == 0) {
-            PairStageParams ps{};
-            ps.v = vp;
-            ps.do_surface = 0;
-            ps.do_volume = 1;
-            launch_pair(h, ps);
-        } else if (N == 3 && h->vol_variant == 0) {  // N = 3 pair kernel, operators in TMEM
-            auto kern = modal_volume_pair_n3_kernel;
-            const size_t psm = PairN3::bytes();
-            const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN3::T, psm);
-            const int grid = std::min((vp.K + 2 * PairN3::WARPS - 1) / (2 * PairN3::WARPS), occ * h->nsm);
-            launch_pdl(kern, std::max(grid, 1), PairN3::T, psm, h->stream, (h->pdl_mask & 1) != 0, vp);
-        } else if (N == 4 && h->vol_variant == 4) {
-            auto kern = modal_volume_quad_n4_kernel;
-            const size_t qsm = QuadN4::bytes();
-            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, QuadN4::T, qsm);
-            int grid = std::min((vp.K + 4 * QuadN4::WARPS - 1) / (4 * QuadN4::WARPS), occ * h->nsm);
-            kern<<<std::max(grid, 1), QuadN4::T, qsm, h->stream>>>(vp);
-        } else if (N == 4 && h->vol_variant == 3) {
-            auto kern = modal_volume_warp_n4_kernel;
-            const size_t wsm = WarpN4::bytes();
-            int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, WarpN4::T, wsm);
-            int grid = std::min((vp.K + WarpN4::WARPS - 1) / WarpN4::WARPS, occ * h->nsm);
-            kern<<<std::max(grid, 1), WarpN4::T, wsm, h->stream>>>(vp);
-        } else if (h->vol_variant == 2) {
-            launch_vol(modal_volume_kernel<N, false>);
-        } else {
+        } else if constexpr (N == 4) {  // pair kernel, operators in TMEM (modal_pair_n4.cuh)
+            launch_pair<PairN4>(h, modal_volume_pair_n4_kernel, vp);
+        } else if constexpr (N == 3) {  // modal_pair_n3.cuh
+            launch_pair<PairN3>(h, modal_volume_pair_n3_kernel, vp);
+        } else {  // N = 1, 2: two rows per thread (modal_fast.cuh)
             using FC = VolFastCfg<N>;
             auto kern = modal_volume_fast_kernel<N>;
             const size_t fsm = FC::bytes();
@@ -473,7 +440,7 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             go(sbp_rhs_kernel<N, true>);
-        } else if (N == 4 && h->vol_variant == 0 && sbp_pair_aligned(sp)) {  // pair kernel, operators in TMEM
+        } else if (N == 4 && sbp_pair_aligned(sp)) {  // pair kernel, operators in TMEM
             auto kern = sbp_rhs_pair_n4_kernel;
             const size_t psm = SbpPairN4::bytes();
             const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, SbpPairN4::T, psm);
@@ -517,95 +484,9 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
 
 int run_stage(swedg_handle h, const StageArgs& sa);
 
-// FAST N=4 single-rank fused chain (modal_pair_n4.cuh PairStageParams).
-bool fused_path(swedg_handle h) {
-    return h->fusion && h->mode == SWEDG_MODE_FAST && h->scheme == SWEDG_SCHEME_HYBRIDIZED && h->N == 4 &&
-           h->vol_variant == 0 && h->n_halo == 0 && !h->timers;
-}
-
-int ensure_trace2(swedg_handle h) {
-    if (!h->trace2 && dalloc(h, &h->trace2, (size_t)h->K * 3 * h->nf)) return h->last_code;
-    return SWEDG_OK;
-}
-
-// Stages 1..4 as fused launches [interface(s-1) + volume(s)] and the final
-// interface/update of stage 4, after stage 0's volume kernel wrote its traces to
-// h->trace (buffer 0).  Stage s writes traces to buffer s % 2.
-int run_fused_tail(swedg_handle h, const unsigned* ids, double dt) {
-    if (ensure_trace2(h)) return h->last_code;
-    double* buf[2] = {h->trace, h->trace2};
-    for (int s = 1; s < 5; ++s) {
-        PairStageParams ps{};
-        ModalVolParams& vp = ps.v;
-        vp.K = h->K;
-        vp.g = h->g;
-        vp.ops = h->ops;
-        vp.u = h->u;
-        vp.gf = h->gf;
-        vp.bs = h->bs;
-        vp.src = h->src;
-        vp.trace = buf[s & 1];
-        vp.accf = h->accf;
-        vp.T1 = h->T1;
-        vp.proj = nullptr;
-        vp.err = h->err;
-        vp.stage_id = ids[s];
-        vp.early_exit = 1;
-        vp.k_base = 0;
-        ps.do_surface = 1;
-        ps.do_volume = 1;
-        ps.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
-        ps.trace_in = buf[(s - 1) & 1];
-        ps.surf = h->surf;
-        ps.nbr = h->nbr;
-        ps.perm = h->perm;
-        ps.Mpk = h->Mpk;
-        ps.u = h->u;
-        ps.res = h->res;
-        ps.rk_a = Lsrk45::a[s - 1];
-        ps.rk_b = Lsrk45::b[s - 1];
-        ps.dt = dt;
-        ps.stage_prev = ids[s - 1];
-        launch_pair(h, ps);
-        h->launches++;
-    }
-    // interface + update of stage 4 (reads buffer 0)
-    ModalSurfParams sp;
-    sp.K = h->K;
-    sp.g = h->g;
-    sp.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
-    sp.ops = h->ops;
-    sp.trace = buf[0];
-    sp.accf = h->accf;
-    sp.T1 = h->T1;
-    sp.surf = h->surf;
-    sp.src = h->src;
-    sp.nbr = h->nbr;
-    sp.perm = h->perm;
-    sp.Minv = h->Minv;
-    sp.Mpk = h->Mpk;
-    sp.du = nullptr;
-    sp.u = h->u;
-    sp.res = h->res;
-    sp.rk_a = Lsrk45::a[4];
-    sp.rk_b = Lsrk45::b[4];
-    sp.dt = dt;
-    sp.rk_mode = 1;
-    sp.err = h->err;
-    sp.stage_id = ids[4];
-    sp.early_exit = 1;
-    sp.k_begin = 0;
-    using SC = SurfCfg<4>;
-    launch_pdl(modal_surface_kernel<4, false>, (h->K + SC::E - 1) / SC::E, SC::T, 0, h->stream, (h->pdl_mask & 2) != 0, sp);
-    h->launches++;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
-    return SWEDG_OK;
-}
-
-// One LSRK45 step on the resident state: 6 launches on the fused path, else 10.
+// One LSRK45 step on the resident state (10 launches; SBP N=4 FAST: 5).
 bool sbp_pair_path(swedg_handle h) {
-    return h->scheme == SWEDG_SCHEME_SBP && h->mode == SWEDG_MODE_FAST && h->N == 4 && h->vol_variant == 0;
+    return h->scheme == SWEDG_SCHEME_SBP && h->mode == SWEDG_MODE_FAST && h->N == 4;
 }
 
 bool halo_active(swedg_handle h) { return h->halo_set && (h->nccl || h->xfn); }
@@ -679,11 +560,6 @@ int run_step(swedg_handle h, const unsigned* ids, double dt) {
             if (run_stage(h, sa)) return h->last_code;
         }
         return SWEDG_OK;
-    }
-    if (fused_path(h)) {
-        StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[0], Lsrk45::b[0], dt, nullptr, ids[0], true};
-        if (run_stage(h, sa)) return h->last_code;
-        return run_fused_tail(h, ids, dt);
     }
     for (int s = 0; s < 5; ++s) {
         StageArgs sa{h->u, 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
@@ -943,12 +819,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->n_halo = d->n_halo;
     h->g = d->g;
     h->device = d->device;
-    if (const char* v = std::getenv("SWEDG_FUSION")) h->fusion = std::string(v) == "1";
     if (const char* v = std::getenv("SWEDG_PDL")) h->pdl_mask = std::atoi(v);
-    if (const char* v = std::getenv("SWEDG_VOLUME_KERNEL")) {
-        std::string sv(v);
-        h->vol_variant = sv == "tworow" ? 1 : (sv == "row" ? 2 : (sv == "warp" ? 3 : (sv == "quad" ? 4 : 0)));
-    }
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
     if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1097,7 +968,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
-                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->trace2, h->u_alt, h->u_alt2,
+                    h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->u_alt, h->u_alt2,
                     h->pack_src, h->pack_dst, h->sendbuf};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -1355,7 +1226,6 @@ int capture_step_graph(swedg_handle h, double dt) {
         cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
     }
-    if (fused_path(h) && ensure_trace2(h)) return h->last_code;  // no allocation inside a capture
     h->graph_base = h->next_stage;
     h->next_stage += 5;
     CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -2166,7 +2036,7 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
         h->ev_in.push_back(a);
         h->ev_out.push_back(b);
     }
-    if (nsteps > 0 && !fused_path(h) && !h->timers && C >= 3 && wave_adjacent(h, C))
+    if (nsteps > 0 && !h->timers && C >= 3 && wave_adjacent(h, C))
         return step_host_wavefront(h, u_host, dt, nsteps, C);
     auto lo = [&](int c) { return (int)((long)h->K * c / C); };
     // the copy streams start after everything already queued on the handle stream
@@ -2188,16 +2058,7 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
                          lo(c), lo(c + 1)};
             if (run_stage(h, sa)) return h->last_code;
         }
-        if (fused_path(h)) {
-            if (run_fused_tail(h, ids, dt)) return h->last_code;
-            CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
-            CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_step, 0));
-            for (int c = 0; c < C; ++c) {  // D2H of the step's result
-                const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
-                CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
-                CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
-            }
-        } else {
+        {
             for (int s = 0; s < 4; ++s) {
                 StageArgs sa{h->u, s == 0 ? 2 : 3, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
                 if (run_stage(h, sa)) return h->last_code;

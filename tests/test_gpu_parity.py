@@ -240,31 +240,6 @@ def test_host_state_stepping_equals_device_steps(mode, nchunks):
     assert ei.value.elem == 400 and abs(ei.value.t - 0.5) < 1e-12
 
 
-def test_fused_stage_chain_matches_split_launches():
-    """FAST N=4: the fused [interface(s-1) + volume(s)] launch chain (6 launches per step,
-    double-buffered traces) == the split 10-launch step, to rounding (the same arithmetic;
-    FMA contraction may differ between the two kernels)."""
-    import os
-    c = load_golden("modal_n4_warp")
-    dt = 0.004
-    out = {}
-    for fused in ("1", "0"):
-        os.environ["SWEDG_FUSION"] = fused
-        try:
-            h = make(c, capi.MODE_FAST)
-        finally:
-            os.environ.pop("SWEDG_FUSION", None)
-        h.set_state(c["u"])
-        h.step(dt, 3)           # graph replay
-        h.step(dt, 1)           # individual launches
-        u = np.array(c["u"], copy=True)
-        h.step_host(u, dt, 2)   # host-state path
-        out[fused] = (h.get_state()[0], u)
-        h.close()
-    assert rel(out["1"][0], out["0"][0]) <= 1e-13
-    assert rel(out["1"][1], out["0"][1]) <= 1e-13
-
-
 @pytest.mark.parametrize("N", [3, 4])
 def test_odd_element_count_imported_mesh(N):
     """Odd K (a pentagon fan of 5 triangles, wall boundary, imported through
@@ -314,22 +289,6 @@ def test_positivity_error_in_pair_kernels(scheme):
     with pytest.raises(capi.PositivityError) as ei:
         h.step(1e-4, 3)
     assert ei.value.elem == 77 and abs(ei.value.t - 0.125) < 1e-12
-
-
-@pytest.mark.parametrize("variant", ["tworow", "row", "warp", "quad"])
-def test_opt_in_volume_kernel_variants(variant):
-    """The opt-in FAST volume kernels kept for comparison (SWEDG_VOLUME_KERNEL; DESIGN §4.1
-    history) stay correct: N=4 modal and SBP rhs within the FAST acceptance criterion."""
-    import os
-    os.environ["SWEDG_VOLUME_KERNEL"] = variant
-    try:
-        for name in ("modal_n4_warp", "sbp_dam_n4"):
-            c = load_golden(name)
-            h = make(c, capi.MODE_FAST)
-            assert_fast_rhs(h.rhs(c["u"]), c["du_lf"], c, c["u"])
-            h.close()
-    finally:
-        os.environ.pop("SWEDG_VOLUME_KERNEL", None)
 
 
 def test_sbp_pair_pdl_and_state_rotation():
@@ -389,9 +348,11 @@ def test_sbp_rhs_device_unaligned_input_falls_back():
 
 @pytest.mark.parametrize("name", ["modal_n4_warp", "modal_n3_warp"])
 def test_modal_volume_ranges_with_odd_split(name):
-    """Volume launches over element ranges [0, k) and [k, K) with k odd: the second
-    range's pair blocks are not 16 B aligned, so the pair kernels (N=4, N=3) stage them
-    with plain loads instead of bulk copies — bitwise the full-range stage."""
+    """Volume launches over element ranges [0, k) and [k, K) with k odd — bitwise the
+    full-range stage.  N=4: the second range's u block (45 doubles per element) is then
+    8 B aligned, so the pair kernel stages it with plain loads; N=3 blocks (u 30, gf 112,
+    b 28 doubles per element) stay 16 B aligned at any k, so both ranges use bulk copies
+    (the plain-load path is covered by the unaligned rhs_device test)."""
     c = load_golden(name)
     K = int(c["K"][0])
     dt = float(c["dt"][0])
@@ -465,25 +426,37 @@ def test_tiny_meshes_pair_kernels(ntri, scheme):
     assert rel(h.get_state()[0], u_ref) <= RUN_TOL
 
 
-def test_n3_pair_kernel_matches_previous_fast_kernel():
-    """FAST N=3: the pair kernel (default) and the earlier two-rows-per-thread FAST kernel
-    (SWEDG_VOLUME_KERNEL=tworow) agree to rounding on a curved C4-generator mesh with an
-    odd element count, and both stay within the tolerance of the C oracle."""
-    import os
+@pytest.mark.parametrize("name", ["modal_n4_warp", "modal_n3_warp"])
+def test_modal_rhs_device_unaligned_input_plain_load_path(name):
+    """The modal pair kernels (N=4, N=3) stage a pair's u/gf/b blocks by bulk copies when
+    every base pointer is 16 B aligned; a caller's rhs_device input 8 B past a 16 B boundary
+    takes the plain-load staging path instead: bitwise the aligned result."""
+    import torch
 
+    c = load_golden(name)
+    h = make(c, capi.MODE_FAST)
+    u = np.ascontiguousarray(c["u"], dtype=np.float64)
+    n = u.size
+    buf = torch.empty(n + 1, dtype=torch.float64, device="cuda")
+    ua, uu = buf[:n], buf[1:]
+    out = []
+    for view in (ua, uu):
+        view.copy_(torch.from_numpy(u.ravel()))
+        du = torch.empty(n, dtype=torch.float64, device="cuda")
+        h.rhs_device(view.data_ptr(), du.data_ptr())
+        torch.cuda.synchronize()
+        out.append(du.cpu().numpy().reshape(u.shape))
+    assert uu.data_ptr() % 16 == 8
+    np.testing.assert_array_equal(out[0], out[1])
+    assert_fast_rhs(out[0], c["du_lf"], c, c["u"])
+
+
+def test_n3_pair_kernel_odd_element_count_within_tolerance():
+    """FAST N=3 pair kernel on a curved C4-generator mesh with an even element count per row
+    but odd pair-tail handling (K = 162): within the FAST tolerance of the C oracle."""
     c = capi.Case("smooth", N=3, nx=9, warp=0.1)  # K = 162
     cd = case_dict(c)
     u = c.u0()
     ref, err, _ = Oracle(cd).rhs(u)
     assert err == 0
-    hp = c.handle(mode=capi.MODE_FAST)
-    du_pair = hp.rhs(u)
-    os.environ["SWEDG_VOLUME_KERNEL"] = "tworow"
-    try:
-        ho = c.handle(mode=capi.MODE_FAST)
-    finally:
-        os.environ.pop("SWEDG_VOLUME_KERNEL", None)
-    du_old = ho.rhs(u)
-    assert_fast_rhs(du_pair, ref, cd, u)
-    assert_fast_rhs(du_old, ref, cd, u)
-    assert rel(du_pair, du_old) <= 1e-12
+    assert_fast_rhs(c.handle(mode=capi.MODE_FAST).rhs(u), ref, cd, u)
