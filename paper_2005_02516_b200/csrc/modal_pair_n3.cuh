@@ -40,7 +40,11 @@ struct PairN3 {
     // the pair's raw blocks, landed by bulk copies: u [2][30] | gf [2][112] | b [2][28]
     static constexpr int sU = 0, sG = 60, sB = 284, stage_len = 340;
     static constexpr int per_warp = 2 * work_stride + stage_len;
-    static constexpr int ops_len = 160 + 120;  // Vq (16 x 10) for the lift, Vf (12 x 10)
+    // Vq (16 x 10) for the lift with column stride 18 (the lift's lanes read one column each:
+    // a stride of 16 doubles put all ten columns in one bank, a 10-way conflict per load),
+    // then Vf (12 x 10)
+    static constexpr int vq_stride = 18;
+    static constexpr int ops_len = vq_stride * 10 + 120;
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
 };
 
@@ -53,8 +57,9 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
     extern __shared__ __align__(16) double smem[];
     __shared__ uint32_t tmem_base_sh;
     __shared__ __align__(8) uint64_t mbar[W::WARPS];
-    double* sVq = smem;        // 16 x 10
-    double* sVf = smem + 160;  // 12 x 10
+    constexpr int VS = W::vq_stride;
+    double* sVq = smem;                // 16 x 10, column stride VS
+    double* sVf = smem + VS * Np;      // 12 x 10
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int half = lane >> 4, lp = lane & 15;
     double* wbase = smem + W::ops_len + warp * W::per_warp;
@@ -68,7 +73,7 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
 
     // ---- CTA setup: launch-invariant operators only (overlaps the previous kernel's
     //      tail under programmatic dependent launch)
-    for (int x = threadIdx.x; x < nq * Np; x += W::T) sVq[x] = prm.ops[O::Vq + x];
+    for (int x = threadIdx.x; x < nq * Np; x += W::T) sVq[(x % nq) + (x / nq) * VS] = prm.ops[O::Vq + x];
     for (int x = threadIdx.x; x < nf * Np; x += W::T) sVf[x] = prm.ops[O::Vf + x];
     double* sQA = smem + W::ops_len;  // staged in the (still unused) work area
     double* sQB = sQA + nh * nh;
@@ -102,7 +107,7 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
         for (int j = cph; j < nq; j += W::WARPS / 4)
             tmem_st4(tbase + W::tB + 4 * j, bok ? sQA[rB + j * nh] : 0.0, bok ? sQB[rB + j * nh] : 0.0);
         for (int m = cph; m < Np; m += W::WARPS / 4) {
-            tmem_st2(tbase + W::tV + 2 * m, sVq[rA + m * nq]);
+            tmem_st2(tbase + W::tV + 2 * m, sVq[rA + m * VS]);
             tmem_st2(tbase + W::tV + 20 + 2 * m, bok ? sVf[lp + m * nf] : 0.0);
         }
         for (int i = cph; i < nq; i += W::WARPS / 4) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? sPq[lp + i * Np] : 0.0);
@@ -345,7 +350,7 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll
             for (int i = 0; i < nq; i += 2) {
-                const double v = sVq[i + m * nq], w = sVq[i + 1 + m * nq];
+                const double v = sVq[i + m * VS], w = sVq[i + 1 + m * VS];
                 s0 = __fma_rn(v, stk[i], s0);
                 s1 = __fma_rn(v, stk[nq + i], s1);
                 s2 = __fma_rn(v, stk[2 * nq + i], s2);

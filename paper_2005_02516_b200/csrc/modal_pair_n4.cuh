@@ -49,6 +49,14 @@ __device__ __forceinline__ void pair6(Row6& r, const double2 q, const double2 A,
     r.b2 = __fma_rn(qy, hj, r.b2);
 }
 
+// FP64 tensor-core step D += A B (m8n8k4; A 8x4 row-major: lane holds A[lane/4][lane%4];
+// B 4x8 col-major: lane holds B[lane%4][lane/4]; D 8x8: lane holds D[lane/4][2(lane%4) + {0,1}])
+__device__ __forceinline__ void dmma884(double& d0, double& d1, const double a, const double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
 // row-constant parts of the factored accumulation (u_i, v_i, gh4_i = 2 g h_i)
 __device__ __forceinline__ void row_finish(Row6& r, const double ui, const double vi, const double gh4) {
     r.a1 = __fma_rn(gh4, r.b1, __fma_rn(ui, r.a0, r.a1));
@@ -155,7 +163,14 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             const int q = x / Np, m = x - q * Np, r = rows[q];
             tmem_st2(tbase + W::tV + 30 * q + 2 * m, r < nq ? sVq[r + m * nq] : sVf[(r - nq) + m * nf]);
         }
+#ifdef SWEDG_N4_DMMA_PQ  // Pq as 14 DMMA A fragments (2 m-tiles x 7 k-steps) per lane
+        for (int f = cph; f < 14; f += W::WARPS / 4) {
+            const int m = 8 * (f / 7) + (lane >> 2), kk = 4 * (f % 7) + (lane & 3);
+            tmem_st2(tbase + W::tP + 2 * f, (m < Np && kk < nq) ? sPq[m + kk * Np] : 0.0);
+        }
+#else
         for (int i = cph; i < nq; i += W::WARPS / 4) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? sPq[lp + i * Np] : 0.0);
+#endif
         asm volatile("tcgen05.wait::st.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -275,6 +290,33 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             }
         }
         __syncwarp();
+#ifdef SWEDG_N4_DMMA_PQ
+        // ---- vh = Pq v on the FP64 tensor cores: both elements at once, D (15 x 6) =
+        //      Pq (15 x 25) [v_e, c] (25 x 6), columns n = c + 3e, 2 m-tiles x 7 k-steps
+        {
+            double Af[16];
+            tmem_ld32d(tbase + W::tP, Af);
+            const int gid = lane >> 2, tig = lane & 3;
+            const double* vb = wbase + (gid / 3) * W::work_stride + W::wV + (gid % 3) * nq;
+            double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 7; ++ks) {
+                const int i = 4 * ks + tig;
+                const double b = (gid < 6 && i < nq) ? vb[i] : 0.0;
+                dmma884(d00, d01, Af[ks], b);
+                dmma884(d10, d11, Af[7 + ks], b);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int n = 2 * tig + q;
+                if (n < 6) {
+                    double* o = wbase + (n / 3) * W::work_stride + W::wVh + (n % 3) * Np;
+                    o[gid] = q ? d01 : d00;
+                    if (8 + gid < Np) o[8 + gid] = q ? d11 : d10;
+                }
+            }
+        }
+#else
         // ---- vh = Pq v (lane l' = output m)
         {
             double Pa[16], Pb[16];
@@ -303,6 +345,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             }
         }
         __syncwarp();
+#endif
         // ---- projected states at rows rA, rB, rC (rC only lanes l' < 8 store)
         Row6 RA, RB, RC;
         {
@@ -489,6 +532,35 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             }
         }
         __syncwarp();
+#ifdef SWEDG_N4_DMMA_LIFT
+        // T1 = Vq^T stacked on the FP64 tensor cores: both elements, D (15 x 6) = Vq^T (15 x 25)
+        // [stk_e, c] (25 x 6); A fragments from shared memory
+        {
+            const int gid = lane >> 2, tig = lane & 3;
+            const double* sb = wbase + (gid / 3) * W::work_stride + W::wU + (gid % 3) * nq;
+            double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 7; ++ks) {
+                const int i = 4 * ks + tig;
+                const bool iok = i < nq;
+                const double b = (gid < 6 && iok) ? sb[i] : 0.0;
+                const double a0 = iok ? sVq[i + gid * nq] : 0.0;
+                const double a1 = (iok && 8 + gid < Np) ? sVq[i + (8 + gid) * nq] : 0.0;
+                dmma884(d00, d01, a0, b);
+                dmma884(d10, d11, a1, b);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int n = 2 * tig + q, e = n / 3;
+                const int ke = 2 * pr + e;
+                if (n < 6 && ke < prm.K) {
+                    double* out = prm.T1 + (size_t)ke * 3 * Np + (n % 3) * Np;
+                    out[gid] = q ? d01 : d00;
+                    if (8 + gid < Np) out[8 + gid] = q ? d11 : d10;
+                }
+            }
+        }
+#else
         {
             const double* stk = work + W::wU;
             const int m = lp < Np ? lp : Np - 1;
@@ -516,6 +588,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 out[2 * Np + lp] = s2;
             }
         }
+#endif
         __syncwarp();
     }
     // the interface kernel's CTAs cannot be resident beside this CTA anyway (shared
