@@ -16,7 +16,14 @@
 
 #include <stdint.h>
 
-#include "modal_pair_n4.cuh"  // Row6 / pair6 / row_finish, TMEM, mbarrier and bulk-copy helpers
+#include "modal_pair_n4.cuh"  // Row6 / pair6 / row_finish, dmma884, TMEM, mbarrier and bulk-copy helpers
+
+// vh = Pq v and the lift Vq^T (src - acc) on the FP64 tensor cores (m8n8k4, both elements of
+// the warp in one MMA chain): fewer shared-memory wavefronts in this L1-heavy kernel, measured
+// 1.5 % faster than the DFMA loops (profiles/r2_n3_dmma_full.md); -DSWEDG_N3_NO_DMMA for the A/B
+#ifndef SWEDG_N3_NO_DMMA
+#define SWEDG_N3_DMMA
+#endif
 
 namespace swedg {
 
@@ -27,7 +34,11 @@ struct PairN3 {
     static constexpr int tA = 0;     // Q row rA : 28 columns j
     static constexpr int tB = 112;   // Q row rB : 16 volume columns j
     static constexpr int tV = 176;   // V rows of rA (Vq) and rB (Vf): 2 x 10 doubles
+#ifdef SWEDG_N3_DMMA
+    static constexpr int tP = 216;   // DMMA A fragments: Pq (2 m-tiles x 4 k-steps) | Vq^T (8): 16 doubles
+#else
     static constexpr int tP = 216;   // Pq row l' (l' < 10): 16 doubles
+#endif
     static constexpr int tcols = 256;
     // per-element work block (doubles)
     static constexpr int wA = 0, wB = 56, wC = 112, wD = 168;  // double2[28]: (hu,hv) (u,v) (g1,g2) (g3,g4)
@@ -110,7 +121,15 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
             tmem_st2(tbase + W::tV + 2 * m, sVq[rA + m * VS]);
             tmem_st2(tbase + W::tV + 20 + 2 * m, bok ? sVf[lp + m * nf] : 0.0);
         }
+#ifdef SWEDG_N3_DMMA  // per lane: A fragments of Pq (8) and of Vq^T (8) for m8n8k4 FP64 MMAs
+        for (int f = cph; f < 16; f += W::WARPS / 4) {
+            const int ff = f & 7, m = 8 * (ff >> 2) + (lane >> 2), kk = 4 * (ff & 3) + (lane & 3);
+            const double v = m >= Np ? 0.0 : (f < 8 ? sPq[m + kk * Np] : sVq[kk + m * VS]);
+            tmem_st2(tbase + W::tP + 2 * f, v);
+        }
+#else
         for (int i = cph; i < nq; i += W::WARPS / 4) tmem_st2(tbase + W::tP + 2 * i, lp < Np ? sPq[lp + i * Np] : 0.0);
+#endif
         asm volatile("tcgen05.wait::st.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -208,6 +227,31 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
             work[W::wV + 2 * nq + rA] = vy;
         }
         __syncwarp();
+#ifdef SWEDG_N3_DMMA
+        // ---- vh = Pq v on the FP64 tensor cores, both elements: D (10 x 6) = Pq (10 x 16) [v] (16 x 6)
+        {
+            double Af[16];  // A fragments: Pq (0..7), Vq^T for the lift (8..15)
+            tmem_ld32d(tbase + W::tP, Af);
+            const int gid = lane >> 2, tig = lane & 3;
+            const double* vb = wbase + (gid / 3) * W::work_stride + W::wV + (gid % 3) * nq;
+            double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const double b = gid < 6 ? vb[4 * ks + tig] : 0.0;
+                dmma884(d00, d01, Af[ks], b);
+                dmma884(d10, d11, Af[4 + ks], b);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int n = 2 * tig + q;
+                if (n < 6) {
+                    double* o = wbase + (n / 3) * W::work_stride + W::wVh + (n % 3) * Np;
+                    o[gid] = q ? d01 : d00;
+                    if (8 + gid < Np) o[8 + gid] = q ? d11 : d10;
+                }
+            }
+        }
+#else
         // ---- vh = Pq v (lane l' = output m < 10)
         {
             double Pa[16];
@@ -229,6 +273,7 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
             }
         }
         __syncwarp();
+#endif
         // ---- projected states at rows rA and rB
         Row6 RA, RB;
         {
@@ -344,6 +389,30 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
             stk[2 * nq + rA] = valid ? mgh * srcA[1] - RA.a2 : 0.0;
         }
         __syncwarp();
+#ifdef SWEDG_N3_DMMA
+        {  // T1 = Vq^T stacked on the FP64 tensor cores, both elements: D (10 x 6)
+            double Af[16];
+            tmem_ld32d(tbase + W::tP, Af);
+            const int gid = lane >> 2, tig = lane & 3;
+            const double* sb = wbase + (gid / 3) * W::work_stride + W::wU + (gid % 3) * nq;
+            double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const double b = gid < 6 ? sb[4 * ks + tig] : 0.0;
+                dmma884(d00, d01, Af[8 + ks], b);
+                dmma884(d10, d11, Af[12 + ks], b);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int n = 2 * tig + q, ke = 2 * pr + n / 3;
+                if (n < 6 && ke < prm.K) {
+                    double* out = prm.T1 + (size_t)ke * 3 * Np + (n % 3) * Np;
+                    out[gid] = q ? d01 : d00;
+                    if (8 + gid < Np) out[8 + gid] = q ? d11 : d10;
+                }
+            }
+        }
+#else
         {
             const double* stk = work + W::wU;
             const int m = lp < Np ? lp : Np - 1;
@@ -365,6 +434,7 @@ modal_volume_pair_n3_kernel(ModalVolParams prm) {
                 out[2 * Np + lp] = s2 + e2;
             }
         }
+#endif
         __syncwarp();
     }
     asm volatile("griddepcontrol.launch_dependents;");
