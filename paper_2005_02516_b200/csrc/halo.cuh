@@ -7,6 +7,9 @@
 // format packs three faces per [3][nf] pseudo-element (face i of a message at
 // pseudo-element i/3, face position i%3), which is exactly the layout of the
 // receiver's halo slots in the trace buffer — a received message needs no unpack.
+// The SBP scheme reads the neighbours' face-node STATES instead (solver.hpp:405-407):
+// its pseudo-elements are [3][nq] state blocks holding three faces' node values at the
+// volume nodes face_index[position npf + node], the halo slots of the state buffers.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -19,23 +22,20 @@
 
 namespace swedg {
 
-// One thread per (sent face, field, node): buf[dst + c nf + s] = trace[src + c nf + s]
-// with src = (e 3 + 0) nf + f npf and dst the face's wire position.
+// One thread per (sent face, field, node): buf[dst[i]] = base[src[i]].  Modal: base is
+// the face-trace buffer ([K][3][nf]); SBP: the stage's input state ([K][3][nq], face
+// node values, solver.hpp:405-407).  The index lists are built once by swedg_set_halo.
 struct HaloPackParams {
-    const double* trace;
-    const long long* src;  // [n] trace offset of face (e, f), field 0, node 0
-    const long long* dst;  // [n] send-buffer offset of the face, field 0, node 0
+    const double* base;
+    const long long* src;  // [n] offsets into base
+    const long long* dst;  // [n] offsets into buf (wire format)
     double* buf;
-    int n, nf, npf;
+    long long n;
 };
 
 __global__ void halo_pack_kernel(HaloPackParams p) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int per = 3 * p.npf;
-    if (i >= (long long)p.n * per) return;
-    const int face = (int)(i / per), r = (int)(i - (long long)face * per);
-    const int c = r / p.npf, s = r - c * p.npf;
-    p.buf[p.dst[face] + c * p.nf + s] = p.trace[p.src[face] + c * p.nf + s];
+    if (i < p.n) p.buf[p.dst[i]] = p.base[p.src[i]];
 }
 
 // ---- NCCL, resolved at run time ---------------------------------------------

@@ -45,6 +45,11 @@ struct SbpParams {
     ErrRec* err;
     unsigned stage_id;
     int early_exit;
+    // element range launches (multi-rank interior / boundary split): the per-element
+    // pointers above are offset to the range's first element k_base; neighbour states
+    // are read from u_nb (the whole buffer: owned elements, then halo slots)
+    const double* u_nb;
+    int k_base;
 };
 
 template <int N>
@@ -113,7 +118,7 @@ sbp_rhs_kernel(SbpParams prm) {
             hi = el[S::su + mi];
             Ui = el[S::su + nq + mi];
             Vi = el[S::su + 2 * nq + mi];
-            if (!(hi > 0.0)) record_error(prm.err, prm.stage_id, 0, k);  // check_positive (:381)
+            if (!(hi > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);  // check_positive (:381)
             ui = A::div(Ui, hi);
             vi = A::div(Vi, hi);
             el[S::svel + mi] = ui;
@@ -197,7 +202,7 @@ sbp_rhs_kernel(SbpParams prm) {
                 up[2] = A::sub(Vi, A::mul(A::mul(2.0, un), nyi));
             } else {
                 const int j = prm.fidx[prm.perm[(size_t)k * nf + i]];
-                const double* un = prm.u + (size_t)nb * 3 * nq + j;
+                const double* un = prm.u_nb + (size_t)nb * 3 * nq + j;
                 up[0] = un[0];
                 up[1] = un[nq];
                 up[2] = un[2 * nq];
@@ -258,7 +263,7 @@ sbp_rhs_kernel(SbpParams prm) {
         const double r2 = A::sub(-acc2, A::mul(gh, sr[nq + mi]));
         const double mv = prm.minv[(size_t)k * nq + mi];
         const double d0 = A::mul(mv, r0), d1 = A::mul(mv, r1), d2 = A::mul(mv, r2);
-        if (!(isfinite(d0) && isfinite(d1) && isfinite(d2))) record_error(prm.err, prm.stage_id, 1, k);
+        if (!(isfinite(d0) && isfinite(d1) && isfinite(d2))) record_error(prm.err, prm.stage_id, 1, prm.k_base + k);
         double* out = (prm.rk_mode ? prm.du_scratch : prm.du) + (size_t)k * 3 * nq + mi;
         out[0] = d0;
         out[nq] = d1;

@@ -219,7 +219,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 const int j = lp + 16 * t;
                 if (j < nq) {
                     const double h = ph[t], hu = pu[t], hv = pv[t];
-                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, k);  // check_positive (:381)
+                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);  // check_positive (:381)
                     const double ih = 1.0 / h;
                     reinterpret_cast<double2*>(work + W::wA)[j] = make_double2(hu, hv);
                     reinterpret_cast<double2*>(work + W::wB)[j] = make_double2(hu * ih, hv * ih);
@@ -286,7 +286,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 if (valid && slot >= 0) {
                     const int nb = ri[half * 3 + slot / npf];
                     if (nb >= 0) {
-                        const double* un = prm.u + (size_t)nb * 3 * nq + prm.fidx[ri[6 + half * nf + slot]];
+                        const double* un = prm.u_nb + (size_t)nb * 3 * nq + prm.fidx[ri[6 + half * nf + slot]];
                         nb3[q][0] = un[0];
                         nb3[q][1] = un[nq];
                         nb3[q][2] = un[2 * nq];
@@ -370,7 +370,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             const double d0 = mv * -acc0;
             const double d1 = mv * (-acc1 - gh * sr[row]);
             const double d2 = mv * (-acc2 - gh * sr[nq + row]);
-            if (!(isfinite(d0) && isfinite(d1) && isfinite(d2))) record_error(prm.err, prm.stage_id, 1, k);
+            if (!(isfinite(d0) && isfinite(d1) && isfinite(d2))) record_error(prm.err, prm.stage_id, 1, prm.k_base + k);
             const size_t o = (size_t)k * 3 * nq + row;
             if (prm.u_next) {  // fused LSRK45 update into the other state buffer (neighbours read u)
                 const double uo[3] = {hi, Ui, Vi}, dd[3] = {d0, d1, d2};

@@ -1265,8 +1265,7 @@ void build_case(swedg_case_s& c) {
         if (part == SWEDG_PARTITION_WEAK) dom.Ly *= P;
         c.mesh = uniform_tri_mesh(cfg.nx, part == SWEDG_PARTITION_WEAK ? cfg.ny * P : cfg.ny, dom, false);
     } else if (part != SWEDG_PARTITION_NONE) {
-        if (dam || cfg.scheme != SWEDG_SCHEME_HYBRIDIZED)
-            throw std::invalid_argument("strip partitions need a periodic problem and the hybridized scheme");
+        if (dam) throw std::invalid_argument("strip partitions need a periodic problem");
         if (cfg.strip < 0 || cfg.strip >= P) throw std::invalid_argument("strip index out of range");
         // weak: P strips of ny rows on a domain stretched P times in y (fixed work per rank);
         // strong: the problem's nx x ny mesh cut into P strips of ny/P rows (+-1)

@@ -128,7 +128,8 @@ struct swedg_handle_s {
     std::vector<int> send_peer, recv_peer;
     std::vector<size_t> send_off, send_len, recv_off, recv_len;  // doubles, wire format
     int n_send_faces = 0;
-    long long* pack_src = nullptr;  // [n_send_faces]
+    long long n_pack = 0;           // pack entries: n_send_faces x 3 x npf
+    long long* pack_src = nullptr;  // [n_pack]
     long long* pack_dst = nullptr;
     double* sendbuf = nullptr;
     size_t send_doubles = 0;
@@ -138,6 +139,7 @@ struct swedg_handle_s {
     void* xuser = nullptr;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
+    std::vector<int> fidx_host;  // SBP face_index (halo pack: face node -> volume node)
     int nstate() const { return scheme == SWEDG_SCHEME_SBP ? nq : Np; }
 };
 
@@ -404,22 +406,29 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
 
 template <int N>
 int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
+    // sa.parts bit 0: the RHS kernel on elements [k0, k1) (all K when k1 < 0); bit 1: the
+    // separate LSRK45 update kernel (non-pair paths, after every element's du is known)
+    const int k0 = sa.k0, k1 = sa.k1 < 0 ? h->K : sa.k1;
+    const size_t b = (size_t)k0;
+    const int nq = h->nq, nf = h->nf;
     SbpParams sp;
-    sp.K = h->K;
+    sp.K = k1 - k0;
     sp.g = h->g;
     sp.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
     sp.ops = h->ops;
     sp.fidx = h->fidx;
-    sp.u = sa.u_in;
-    sp.gf = h->gf;
-    sp.surf = h->surf;
-    sp.src = h->src;
-    sp.minv = h->Minv;
-    sp.nbr = h->nbr;
-    sp.perm = h->perm;
-    sp.du = sa.du_out;
+    sp.u = sa.u_in + b * 3 * nq;
+    sp.u_nb = sa.u_in;
+    sp.k_base = k0;
+    sp.gf = h->gf + b * 4 * sbp_gstride(nq);
+    sp.surf = h->surf + b * 3 * nf;
+    sp.src = h->src + b * 2 * nq;
+    sp.minv = h->Minv + b * nq;
+    sp.nbr = h->nbr + b * 3;
+    sp.perm = h->perm + b * nf;
+    sp.du = sa.du_out ? sa.du_out + b * 3 * nq : nullptr;
     sp.uo = h->u;
-    sp.res = h->res;
+    sp.res = h->res + b * 3 * nq;
     sp.rk_a = sa.a;
     sp.rk_b = sa.b;
     sp.dt = sa.dt;
@@ -427,24 +436,24 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
     sp.err = h->err;
     sp.stage_id = sa.stage_id;
     sp.early_exit = sa.early_exit ? 1 : 0;
-    sp.du_scratch = h->du;
-    sp.u_next = sa.u_next;
+    sp.du_scratch = h->du ? h->du + b * 3 * nq : nullptr;
+    sp.u_next = sa.u_next ? sa.u_next + b * 3 * nq : nullptr;
     using C = SbpCfg<N>;
     const size_t smem = SbpSmem<N>::bytes(C::E);
-    const int grid = (h->K + C::E - 1) / C::E;
+    const int grid = (sp.K + C::E - 1) / C::E;
     auto go = [&](void (*kern)(SbpParams)) {  // persistent: resident CTAs x SMs
         const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, C::T, smem);
         kern<<<std::max(1, std::min(grid, occ * h->nsm)), C::T, smem, h->stream>>>(sp);
     };
-    {
+    if ((sa.parts & 1) && sp.K > 0) {
         KTimer kt(h, 0);
         if (h->mode == SWEDG_MODE_PARITY) {
             go(sbp_rhs_kernel<N, true>);
-        } else if (N == 4 && sbp_pair_aligned(sp)) {  // pair kernel, operators in TMEM
+        } else if (N == 4 && sbp_pair_aligned(sp) && (k0 & 1) == 0) {  // pair kernel, operators in TMEM
             auto kern = sbp_rhs_pair_n4_kernel;
             const size_t psm = SbpPairN4::bytes();
             const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, SbpPairN4::T, psm);
-            const int blocks = (h->K + 2 * SbpPairN4::WARPS - 1) / (2 * SbpPairN4::WARPS);
+            const int blocks = (sp.K + 2 * SbpPairN4::WARPS - 1) / (2 * SbpPairN4::WARPS);
             // programmatic dependent launch: the CTAs' operator staging and TMEM fill
             // overlap the previous kernel's tail (the kernel waits on griddepcontrol
             // before touching the state)
@@ -452,9 +461,9 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
         } else {
             go(sbp_rhs_kernel<N, false>);
         }
+        h->launches++;
     }
-    h->launches++;
-    if (sa.rk && !sa.u_next) {
+    if ((sa.parts & 2) && sa.rk && !sa.u_next) {
         // the SBP RHS reads neighbour states: the RK update runs after all du are known
         SbpUpdateParams up;
         up.n = (size_t)h->K * 3 * h->nq;
@@ -491,22 +500,29 @@ bool sbp_pair_path(swedg_handle h) {
 
 bool halo_active(swedg_handle h) { return h->halo_set && (h->nccl || h->xfn); }
 
-// Pack the cut-face traces (halo.cuh) on stream st.
-int halo_pack_on(swedg_handle h, cudaStream_t st) {
-    if (h->n_send_faces == 0) return SWEDG_OK;
-    HaloPackParams p{h->trace, h->pack_src, h->pack_dst, h->sendbuf, h->n_send_faces, h->nf, h->npf};
-    const long long n = (long long)h->n_send_faces * 3 * h->npf;
-    halo_pack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p);
+// Pack the cut faces (halo.cuh) on stream st: modal from the trace buffer, SBP from
+// the stage's input state `sbp_in`.
+int halo_pack_on(swedg_handle h, cudaStream_t st, const double* sbp_in = nullptr) {
+    if (h->n_pack == 0) return SWEDG_OK;
+    const double* base = h->scheme == SWEDG_SCHEME_SBP ? (sbp_in ? sbp_in : h->u) : h->trace;
+    HaloPackParams p{base, h->pack_src, h->pack_dst, h->sendbuf, h->n_pack};
+    halo_pack_kernel<<<(unsigned)((h->n_pack + 255) / 256), 256, 0, st>>>(p);
     h->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("halo pack: ") + cudaGetErrorString(e));
     return SWEDG_OK;
 }
 
+// halo slots: modal in the trace buffer, SBP in the given state buffer
+double* halo_recv(swedg_handle h, double* sbp_state = nullptr) {
+    if (h->scheme == SWEDG_SCHEME_SBP) return (sbp_state ? sbp_state : h->u) + (size_t)h->K * 3 * h->nq;
+    return h->trace + (size_t)h->K * 3 * h->nf;
+}
+
 // One stage's exchange on the comm stream: pack, then NCCL send/recv or the caller's transport.
-int halo_exchange(swedg_handle h, int stage) {
-    if (halo_pack_on(h, h->comm)) return h->last_code;
-    double* recv = h->trace + (size_t)h->K * 3 * h->nf;
+int halo_exchange(swedg_handle h, int stage, double* sbp_state = nullptr) {
+    if (halo_pack_on(h, h->comm, sbp_state)) return h->last_code;
+    double* recv = halo_recv(h, sbp_state);
     if (h->nccl) {
         NcclApi& api = nccl_api();
         int rc = api.GroupStart();
@@ -526,7 +542,10 @@ int halo_exchange(swedg_handle h, int stage) {
 
 // Multi-rank stage schedule: boundary volume -> pack + exchange on the comm stream,
 // overlapped with the interior volume kernel -> interface/update kernel.
+int run_step_halo_sbp(swedg_handle h, const unsigned* ids, double dt);
+
 int run_step_halo(swedg_handle h, const unsigned* ids, double dt) {
+    if (h->scheme == SWEDG_SCHEME_SBP) return run_step_halo_sbp(h, ids, dt);
     for (int s = 0; s < 5; ++s) {
         for (const auto& r : h->bnd_ranges) {
             StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
@@ -543,6 +562,36 @@ int run_step_halo(swedg_handle h, const unsigned* ids, double dt) {
         CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
         StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
         if (run_stage(h, ss)) return h->last_code;
+    }
+    return SWEDG_OK;
+}
+
+// SBP: the RHS reads the neighbours' stage-input states (solver.hpp:405-407), so each
+// stage packs the cut-face node values of its input state, exchanges them on the comm
+// stream while the RHS kernel runs on the interior elements (no halo neighbours), and
+// runs the elements owning cut faces after the exchange.  Pair path (FAST N=4): the
+// stage's input rotates u -> A -> B -> A -> B -> u, each buffer with its own halo slots.
+int run_step_halo_sbp(swedg_handle h, const unsigned* ids, double dt) {
+    const bool pair = sbp_pair_path(h);
+    double* const seq[6] = {h->u, h->u_alt, h->u_alt2, h->u_alt, h->u_alt2, h->u};
+    for (int s = 0; s < 5; ++s) {
+        double* in = pair ? seq[s] : h->u;
+        CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));  // the previous stage wrote `in`
+        CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
+        if (halo_exchange(h, s, in)) return h->last_code;
+        CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+        for (int pass = 0; pass < 2; ++pass) {  // interior ranges, then (after the exchange) boundary ranges
+            if (pass == 1) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+            for (const auto& r : pass == 0 ? h->int_ranges : h->bnd_ranges) {
+                StageArgs sa{in, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
+                if (pair) sa.u_next = seq[s + 1];
+                if (run_stage(h, sa)) return h->last_code;
+            }
+        }
+        if (!pair) {  // LSRK45 update once every element's du is known
+            StageArgs su{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
+            if (run_stage(h, su)) return h->last_code;
+        }
     }
     return SWEDG_OK;
 }
@@ -780,8 +829,6 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     *out = nullptr;
     if (d->abi_version != SWEDG_ABI_VERSION) return fail(nullptr, SWEDG_ERR_INVALID, "ABI version mismatch");
     if (d->n_halo < 0) return fail(nullptr, SWEDG_ERR_INVALID, "n_halo must be >= 0");
-    if (d->n_halo > 0 && d->scheme == SWEDG_SCHEME_SBP)
-        return fail(nullptr, SWEDG_ERR_UNSUPPORTED, "halo (multi-rank) elements are supported for the hybridized scheme");
     if (d->scheme != SWEDG_SCHEME_HYBRIDIZED && d->scheme != SWEDG_SCHEME_SBP)
         return fail(nullptr, SWEDG_ERR_INVALID, "unknown scheme");
     if (d->N < 1 || d->N > 4) return fail(nullptr, SWEDG_ERR_UNSUPPORTED, "degree must be 1..4");
@@ -945,18 +992,24 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
         if (dalloc(h, &h->src, K * 2 * nq)) return bail(h->last_code);
     }
     const size_t ns = K * 3 * h->nstate();
-    if (dalloc(h, &h->u, ns) || dalloc(h, &h->res, ns)) return bail(h->last_code);
-    if (h->scheme == SWEDG_SCHEME_SBP && (dalloc(h, &h->du, ns) || dalloc(h, &h->u_alt, ns) || dalloc(h, &h->u_alt2, ns)))
+    // SBP reads the neighbours' states: every state buffer carries the halo slots
+    const size_t nsh = h->scheme == SWEDG_SCHEME_SBP ? (K + (size_t)h->n_halo) * 3 * h->nq : ns;
+    if (dalloc(h, &h->u, nsh) || dalloc(h, &h->res, ns)) return bail(h->last_code);
+    if (h->scheme == SWEDG_SCHEME_SBP && (dalloc(h, &h->du, ns) || dalloc(h, &h->u_alt, nsh) || dalloc(h, &h->u_alt2, nsh)))
         return bail(h->last_code);
+    if (h->scheme == SWEDG_SCHEME_SBP) h->fidx_host.assign(d->face_index, d->face_index + nf);
     if (dalloc(h, &h->err, 1)) return bail(h->last_code);
     ErrRec none_rec{kNoError, 0ull};
     if (cudaMemcpyAsync(h->err, &none_rec, sizeof(none_rec), cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
-        cudaMemsetAsync(h->u, 0, ns * sizeof(double), h->stream) != cudaSuccess ||
+        cudaMemsetAsync(h->u, 0, nsh * sizeof(double), h->stream) != cudaSuccess ||
         cudaMemsetAsync(h->res, 0, ns * sizeof(double), h->stream) != cudaSuccess ||
         cudaMemsetAsync(h->src, 0, K * 2 * (h->scheme == SWEDG_SCHEME_SBP ? nq : nh) * sizeof(double), h->stream) != cudaSuccess)
         return bail(fail(h, SWEDG_ERR_CUDA, "initialisation failed"));
     if (h->bs && cudaMemsetAsync(h->bs, 0, K * nh * sizeof(double), h->stream) != cudaSuccess)
         return bail(fail(h, SWEDG_ERR_CUDA, "initialisation failed"));
+    for (double* b : {h->u_alt, h->u_alt2})
+        if (b && cudaMemsetAsync(b, 0, nsh * sizeof(double), h->stream) != cudaSuccess)
+            return bail(fail(h, SWEDG_ERR_CUDA, "initialisation failed"));
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return bail(fail(h, SWEDG_ERR_CUDA, "sync failed"));
     *out = h;
     return SWEDG_OK;
@@ -1388,12 +1441,13 @@ int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, l
 // ---- multi-rank halo exchange (halo.cuh) --------------------------------------
 int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
     if (!h || !d) return SWEDG_ERR_INVALID;
-    if (h->scheme != SWEDG_SCHEME_HYBRIDIZED) return fail(h, SWEDG_ERR_UNSUPPORTED, "halo exchange is hybridized-only");
     if (d->n_send_msgs < 0 || d->n_recv_msgs < 0 || (d->n_send_msgs && (!d->send_peer || !d->send_count)) ||
         (d->n_recv_msgs && (!d->recv_peer || !d->recv_count)))
         return fail(h, SWEDG_ERR_INVALID, "bad halo descriptor");
     cudaSetDevice(h->device);
-    const size_t per = (size_t)3 * h->nf;  // one pseudo-element
+    const bool sbp = h->scheme == SWEDG_SCHEME_SBP;
+    const int blk = sbp ? h->nq : h->nf;   // field stride of a pseudo-element
+    const size_t per = (size_t)3 * blk;    // one pseudo-element: modal [3][nf] traces, SBP [3][nq] states
     auto slots = [](int n) { return (size_t)((n + 2) / 3); };
     std::vector<int> sp, rp;
     std::vector<size_t> so, sl, ro, rl;
@@ -1418,17 +1472,23 @@ int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
     if (off != (size_t)h->n_halo * per)
         return fail(h, SWEDG_ERR_INVALID, "receive messages do not fill the descriptor's n_halo slots");
     if (nsend && (!d->send_elem || !d->send_face)) return fail(h, SWEDG_ERR_INVALID, "missing send faces");
-    // per sent face: trace offset and wire offset; the volume ranges that own sent faces
-    std::vector<long long> src(nsend), dst(nsend);
+    // per (sent face, field, node): source and wire offsets; the volume ranges that own sent faces
+    const int npf = h->npf;
+    auto node = [&](int slot) { return sbp ? h->fidx_host[slot] : slot; };  // SBP: face node -> volume node
+    std::vector<long long> src(nsend * 3 * npf), dst(nsend * 3 * npf);
     std::vector<int> owners;
-    size_t i = 0;
+    size_t i = 0, x = 0;
     for (int m = 0; m < d->n_send_msgs; ++m)
         for (int j = 0; j < d->send_count[m]; ++j, ++i) {
             const int e = d->send_elem[i], f = d->send_face[i];
             if (e < 0 || e >= h->K || f < 0 || f > 2)
                 return fail(h, SWEDG_ERR_INVALID, "sent face out of range (element " + std::to_string(e) + ")");
-            src[i] = ((long long)e * 3) * h->nf + (long long)f * h->npf;
-            dst[i] = (long long)(so[m] + (size_t)(j / 3) * per) + (long long)(j % 3) * h->npf;
+            const long long wire = (long long)(so[m] + (size_t)(j / 3) * per);
+            for (int c = 0; c < 3; ++c)
+                for (int sn = 0; sn < npf; ++sn, ++x) {
+                    src[x] = ((long long)e * 3 + c) * blk + node(f * npf + sn);
+                    dst[x] = wire + (long long)c * blk + node((j % 3) * npf + sn);
+                }
             owners.push_back(e);
         }
     std::sort(owners.begin(), owners.end());
@@ -1454,13 +1514,20 @@ int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
     if (h->sendbuf) cudaFree(h->sendbuf);
     h->pack_src = h->pack_dst = nullptr;
     h->sendbuf = nullptr;
-    if (dalloc(h, &h->pack_src, nsend) || dalloc(h, &h->pack_dst, nsend) || dalloc(h, &h->sendbuf, send_doubles))
+    const size_t npk = src.size();
+    if (dalloc(h, &h->pack_src, npk) || dalloc(h, &h->pack_dst, npk) || dalloc(h, &h->sendbuf, send_doubles))
         return h->last_code;
-    if (nsend && (upload(h, h->pack_src, src.data(), nsend) || upload(h, h->pack_dst, dst.data(), nsend)))
+    if (npk && (upload(h, h->pack_src, src.data(), npk) || upload(h, h->pack_dst, dst.data(), npk)))
         return h->last_code;
     // padding face positions of the wire format stay zero
     CUDA_TRY(h, cudaMemsetAsync(h->sendbuf, 0, std::max<size_t>(1, send_doubles) * 8, h->stream));
-    if (h->n_halo > 0) CUDA_TRY(h, cudaMemsetAsync(h->trace + (size_t)h->K * per, 0, (size_t)h->n_halo * per * 8, h->stream));
+    if (h->n_halo > 0) {
+        if (sbp)
+            for (double* b : {h->u, h->u_alt, h->u_alt2})
+                CUDA_TRY(h, cudaMemsetAsync(b + (size_t)h->K * per, 0, (size_t)h->n_halo * per * 8, h->stream));
+        else
+            CUDA_TRY(h, cudaMemsetAsync(h->trace + (size_t)h->K * per, 0, (size_t)h->n_halo * per * 8, h->stream));
+    }
     if (!h->comm) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
     if (!h->ev_bnd) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming));
     if (!h->ev_halo) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
@@ -1472,6 +1539,7 @@ int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
     h->recv_off = ro;
     h->recv_len = rl;
     h->n_send_faces = (int)nsend;
+    h->n_pack = (long long)npk;
     h->send_doubles = send_doubles;
     h->bnd_ranges = bnd;
     h->int_ranges = inner;
@@ -1511,8 +1579,8 @@ int swedg_halo_buffers(swedg_handle h, double** send, size_t* n_send, double** r
     if (!h) return SWEDG_ERR_INVALID;
     if (send) *send = h->sendbuf;
     if (n_send) *n_send = h->send_doubles;
-    if (recv) *recv = h->trace ? h->trace + (size_t)h->K * 3 * h->nf : nullptr;
-    if (n_recv) *n_recv = (size_t)h->n_halo * 3 * h->nf;
+    if (recv) *recv = halo_recv(h);
+    if (n_recv) *n_recv = (size_t)h->n_halo * 3 * (h->scheme == SWEDG_SCHEME_SBP ? h->nq : h->nf);
     return SWEDG_OK;
 }
 

@@ -45,19 +45,23 @@ def message_offsets(counts, nf: int):
 
 # ---------------------------------------------------------------------------
 # wire format on host arrays (CPU reference of the pack kernel, halo.cuh)
-def pack_faces(traces, halo: dict, npf: int) -> np.ndarray:
-    """traces [K][3][nf] -> the send buffer (messages back to back, wire format)."""
-    nf = traces.shape[2]
-    offs = message_offsets(halo["send_count"], nf)
+def pack_faces(blocks, halo: dict, npf: int, face_index=None) -> np.ndarray:
+    """Cut faces -> the send buffer (messages back to back, wire format).  Modal: blocks =
+    face traces [K][3][nf]; SBP: blocks = states [K][3][nq] and face_index maps a face
+    slot to its volume node (the pseudo-element keeps the state layout)."""
+    blk = blocks.shape[2]
+    node = (lambda x: x) if face_index is None else (lambda x: int(face_index[x]))
+    offs = message_offsets(halo["send_count"], blk)
     buf = np.zeros(sum(ln for _, ln in offs))
     i = 0
     for (off, _), n in zip(offs, halo["send_count"]):
         for j in range(int(n)):
             e, f = int(halo["send_elem"][i]), int(halo["send_face"][i])
             i += 1
-            base = off + (j // 3) * 3 * nf + (j % 3) * npf
+            base = off + (j // 3) * 3 * blk
             for c in range(3):
-                buf[base + c * nf: base + c * nf + npf] = traces[e, c, f * npf:(f + 1) * npf]
+                for s in range(npf):
+                    buf[base + c * blk + node((j % 3) * npf + s)] = blocks[e, c, node(f * npf + s)]
     return buf
 
 
@@ -98,12 +102,12 @@ def attach_nccl(h, halo: dict, world: int, rank: int, device: int, group=None) -
 def attach_gloo(h, halo: dict, nf: int, group=None) -> None:
     """Host-staged exchange over gloo as the handle's transport callback (blocking:
     the stream is synchronised before the send buffer is read).  A functional path for
-    several ranks on one device, not a performance path."""
+    several ranks on one device, not a performance path.  nf: field stride of a
+    pseudo-element (modal: nf; SBP: nq)."""
     import torch
 
-    send_ptr, ns, recv_ptr, nr = h.halo_buffers()
+    send_ptr, ns, _, nr = h.halo_buffers()
     send_dev = _view(send_ptr, (ns,))
-    recv_dev = _view(recv_ptr, (nr,))
 
     def xfn(stage, send, recv, stream):
         st = torch.cuda.ExternalStream(stream)
@@ -112,7 +116,7 @@ def attach_gloo(h, halo: dict, nf: int, group=None) -> None:
         host_recv = torch.zeros(nr, dtype=torch.float64)
         exchange_messages(host_send, host_recv, halo, nf, group)
         with torch.cuda.stream(st):
-            recv_dev.copy_(host_recv, non_blocking=False)
+            _view(recv, (nr,)).copy_(host_recv, non_blocking=False)
 
     h.set_exchange(xfn)
 
@@ -126,10 +130,12 @@ class LocalExchange:
     rank's interface kernel starts after every copy into its slots."""
 
     def __init__(self, handles, halos, nf: int):
+        """nf: field stride of a pseudo-element (modal: nf; SBP: nq)."""
         import torch
 
         self.h, self.halos, self.nf, self.P = handles, halos, nf, len(handles)
         self.bufs = [h.halo_buffers() for h in handles]
+        self.recv = [b[2] for b in self.bufs]  # this stage's halo slots (SBP: the stage's input buffer)
         self.barrier = threading.Barrier(self.P)
         self.ready = [torch.cuda.Event() for _ in range(self.P)]
         self.copied = [torch.cuda.Event() for _ in range(self.P)]
@@ -159,12 +165,13 @@ class LocalExchange:
 
         def xfn(stage, send, recv, stream):
             st = torch.cuda.ExternalStream(stream)
+            self.recv[r] = recv
             self.ready[r].record(st)
             self.barrier.wait()
             for off, dst, doff, ln in self.routes[r]:
                 st.wait_event(self.ready[dst])
                 src = _view(self.bufs[r][0] + 8 * off, (ln,))
-                dstv = _view(self.bufs[dst][2] + 8 * doff, (ln,))
+                dstv = _view(self.recv[dst] + 8 * doff, (ln,))
                 with torch.cuda.stream(st):
                     dstv.copy_(src, non_blocking=True)
             self.copied[r].record(st)

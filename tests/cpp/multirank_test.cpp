@@ -2,8 +2,8 @@
 // INFRASTRUCTURE; built by __graft_entry__.build() into tests/cpp/, run on the GPU
 // by tests/test_multirank_cpp.py).
 //
-//  1. P = 2, 3 logical partitions of one mesh on one GPU (strong y-strips from the
-//     native setup), one host thread per rank, each stepping its DeviceSolverOps with
+//  1. P = 1, 2, 3 logical partitions of one mesh on one GPU (strong y-strips from the
+//     native setup; modal and SBP schemes, N = 3, 4), one host thread per rank, each stepping its DeviceSolverOps with
 //     swedg_step_lsrk45.  The transport is a swedg_exchange_fn that pushes the
 //     rank's packed cut-face messages into its peers' halo slots with device copies,
 //     ordered by CUDA events (a copy into a peer starts once the peer reached the
@@ -45,10 +45,10 @@ struct Case {
     const double* u0() const { return swedg_case_array(c, "u0", nullptr); }
 };
 
-static swedg_case_config config(int N, int nx, int ny, int P, int strip) {
+static swedg_case_config config(int N, int nx, int ny, int P, int strip, int scheme = SWEDG_SCHEME_HYBRIDIZED) {
     swedg_case_config cfg{};
     cfg.problem = SWEDG_PROBLEM_SMOOTH;
-    cfg.scheme = SWEDG_SCHEME_HYBRIDIZED;
+    cfg.scheme = scheme;
     cfg.N = N;
     cfg.nx = nx;
     cfg.ny = ny;
@@ -101,10 +101,11 @@ struct Group {
     std::unique_ptr<std::barrier<>> bar;
 };
 
-static int push_exchange(void* user, int, const double*, double*, void* stream) {
+static int push_exchange(void* user, int, const double*, double* recv, void* stream) {
     Rank& me = *static_cast<Rank*>(user);
     Group& g = *me.g;
     auto st = static_cast<cudaStream_t>(stream);
+    me.recv = recv;  // this stage's halo slots (SBP: in the stage's input state buffer)
     if (cudaEventRecord(me.ready, st) != cudaSuccess) return 1;
     g.bar->arrive_and_wait();  // every rank's "ready" of this stage is recorded
     for (const Route& rt : me.routes) {
@@ -131,21 +132,34 @@ static std::vector<std::pair<size_t, size_t>> msg_offsets(const int* counts, int
     return o;
 }
 
-static void logical_partitions(int N, int P) {
+// per element: state doubles per field (Np modal, nq SBP) and pseudo-element field stride
+static void sizes(const Case& c, int* nstate, int* stride) {
+    swedg_desc d{};
+    swedg_case_fill_desc(c.c, &d);
+    *nstate = d.scheme == SWEDG_SCHEME_SBP ? d.nq : d.Np;
+    *stride = d.scheme == SWEDG_SCHEME_SBP ? d.nq : d.nf;
+}
+
+static std::string tag(int scheme, int N, int P) {
+    return std::string(scheme == SWEDG_SCHEME_SBP ? "SBP" : "modal") + " N=" + std::to_string(N) + " P=" +
+           std::to_string(P);
+}
+
+static void logical_partitions(int scheme, int N, int P) {
     const int nx = 8, ny = 9, nsteps = 3;
-    Case global(config(N, nx, ny, 1, -1));
+    Case global(config(N, nx, ny, 1, -1, scheme));
     auto gops = make_ops(global);
     std::vector<std::unique_ptr<Case>> cases;
     std::vector<swedg_b200::DeviceSolverOps> ops;
     double dt = 1e300;
     for (int r = 0; r < P; ++r) {
-        cases.emplace_back(new Case(config(N, nx, ny, P, r)));
+        cases.emplace_back(new Case(config(N, nx, ny, P, r, scheme)));
         ops.push_back(make_ops(*cases.back()));
         dt = std::min(dt, swedg_case_dt(cases.back()->c));
     }
-    const int Np = (N + 1) * (N + 2) / 2, nf = 3 * (N + 1);
-    check(dt == swedg_case_dt(global.c), "N=" + std::to_string(N) + " P=" + std::to_string(P) +
-                                             " min over ranks of the owned dt == global dt");
+    int Np, nf;  // state doubles per field, pseudo-element field stride
+    sizes(global, &Np, &nf);
+    check(dt == swedg_case_dt(global.c), tag(scheme, N, P) + " min over ranks of the owned dt == global dt");
     auto ug = run_steps(gops.handle(), global.u0(), (size_t)global.K() * 3 * Np, dt, nsteps);
 
     Group g;
@@ -203,20 +217,21 @@ static void logical_partitions(int N, int P) {
         same = same && std::memcmp(out[r].data(), ug.data() + off, out[r].size() * 8) == 0;
         off += out[r].size();
     }
-    check(same && off == ug.size(), "N=" + std::to_string(N) + " P=" + std::to_string(P) +
-                                        " logical partitions (exchange callback, device copies) == global, bitwise");
+    check(same && off == ug.size(),
+          tag(scheme, N, P) + " logical partitions (exchange callback, device copies) == global, bitwise");
     for (auto& rk : g.ranks) {
         cudaEventDestroy(rk.ready);
         cudaEventDestroy(rk.copied);
     }
 }
 
-static void nccl_self(int N) {
-    Case global(config(N, 8, 9, 1, -1));
-    Case strip(config(N, 8, 9, 1, 0));
+static void nccl_self(int scheme, int N) {
+    Case global(config(N, 8, 9, 1, -1, scheme));
+    Case strip(config(N, 8, 9, 1, 0, scheme));
     auto gops = make_ops(global);
     auto sops = make_ops(strip);
-    const int Np = (N + 1) * (N + 2) / 2;
+    int Np, stride;
+    sizes(global, &Np, &stride);
     const double dt = swedg_case_dt(global.c);
     auto ug = run_steps(gops.handle(), global.u0(), (size_t)global.K() * 3 * Np, dt, 4);
     char id[128];
@@ -236,7 +251,7 @@ static void nccl_self(int N) {
         std::printf("%s\n", e.what());
     }
     check(u.size() == ug.size() && std::memcmp(u.data(), ug.data(), u.size() * 8) == 0,
-          "N=" + std::to_string(N) + " one-rank NCCL self exchange across the periodic cut == global, bitwise");
+          tag(scheme, N, 1) + " one-rank NCCL self exchange across the periodic cut == global, bitwise");
     swedg_b200::set_nccl_comm(sops, nullptr);  // drops the captured graph (NCCL work) before the comm goes
     swedg_nccl_comm_destroy(comm);
 }
@@ -246,13 +261,16 @@ int main(int argc, char** argv) {
     // multirank_test [--no-nccl | --nccl-only N...]
     const std::string mode = argc > 1 ? argv[1] : "";
     try {
+        const int schemes[2] = {SWEDG_SCHEME_HYBRIDIZED, SWEDG_SCHEME_SBP};
         if (mode == "--nccl-only") {
-            for (int a = 2; a < argc; ++a) nccl_self(std::atoi(argv[a]));
+            for (int a = 2; a < argc; ++a) nccl_self(SWEDG_SCHEME_HYBRIDIZED, std::atoi(argv[a]));
         } else {
-            for (int N : {3, 4})
-                for (int P : {1, 2, 3}) logical_partitions(N, P);
+            for (int sc : schemes)
+                for (int N : {3, 4})
+                    for (int P : {1, 2, 3}) logical_partitions(sc, N, P);
             if (mode != "--no-nccl")
-                for (int N : {3, 4}) nccl_self(N);
+                for (int sc : schemes)
+                    for (int N : {3, 4}) nccl_self(sc, N);
         }
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());

@@ -42,6 +42,11 @@ def case(scaling, P, r, N=N, **kw):
     return capi.Case("smooth", N=N, nx=NX, ny=ny, warp=0.1, strips=P, strip=r, scaling=scaling, threads=1, **kw)
 
 
+def stride(c):
+    """Field stride of a halo pseudo-element: modal face traces [3][nf], SBP states [3][nq]."""
+    return c.nq if c.scheme == capi.SCHEME_SBP else c.nf
+
+
 def owned_slice(scaling, P, r):
     j0, j1 = rows(scaling, P, r)
     return slice(2 * NX * j0, 2 * NX * j1)
@@ -64,14 +69,15 @@ def halo_source(halos, P, r, slot_face):
     raise AssertionError("halo slot outside the receive messages")
 
 
+@pytest.mark.parametrize("scheme", [capi.SCHEME_HYBRIDIZED, capi.SCHEME_SBP])
 @pytest.mark.parametrize("scaling,P", [("weak", 2), ("weak", 3), ("strong", 1), ("strong", 2), ("strong", 3)])
-def test_strip_setup_matches_global_mesh(scaling, P):
-    g = case(scaling, P, -1)
+def test_strip_setup_matches_global_mesh(scaling, P, scheme):
+    g = case(scaling, P, -1, scheme=scheme)
     Kg = g.K
     assert g.n_halo == 0
     gnbr = g.iarray("nbr").reshape(Kg, 3)
     gperm = g.iarray("perm").reshape(Kg, -1)
-    strips = [case(scaling, P, r) for r in range(P)]
+    strips = [case(scaling, P, r, scheme=scheme) for r in range(P)]
     halos = [s.halo_desc() for s in strips]
     dt = min(s.dt for s in strips)
     assert dt == g.dt  # owned minimum edges: the global dt exactly
@@ -81,8 +87,9 @@ def test_strip_setup_matches_global_mesh(scaling, P):
         sl = owned_slice(scaling, P, r)
         assert K == sl.stop - sl.start
         assert s.n_halo == 2 * ((NX + 2) // 3)  # nx cut faces per side, 3 per halo slot
-        for name, per in [("gf", 4 * (s.nq + s.nf)), ("Mh_inv", s.Np * s.Np), ("sJ", s.nf), ("nx", s.nf),
-                          ("u0", 3 * s.Np), ("b", s.Np)]:
+        ns = s.nstate
+        extra = [("J_vol", s.nq)] if scheme == capi.SCHEME_SBP else [("Mh_inv", s.Np * s.Np)]
+        for name, per in [("gf", 4 * (s.nq + s.nf)), ("sJ", s.nf), ("nx", s.nf), ("u0", 3 * ns), ("b", ns)] + extra:
             np.testing.assert_array_equal(s.array(name).reshape(K, per), g.array(name).reshape(Kg, per)[sl],
                                           err_msg=name)
         lnbr = s.iarray("nbr").reshape(K, 3)
@@ -109,33 +116,39 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, P, scaling, port, dt, nsteps, q):
+def _rank_main(rank, P, scaling, port, dt, nsteps, q, scheme=capi.SCHEME_HYBRIDIZED):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=P)
     try:
-        s = case(scaling, P, rank)
+        s = case(scaling, P, rank, scheme=scheme)
         c = case_dict(s)
         halo = s.halo_desc()
         orc = Oracle(c)
         K, nq, nf, npf, nh = s.K, s.nq, s.nf, s.npf, s.nq + s.nf
-        nrecv = sum(ln for _, ln in message_offsets(halo["recv_count"], nf))
-        assert nrecv == s.n_halo * 3 * nf
+        blk = stride(s)
+        nrecv = sum(ln for _, ln in message_offsets(halo["recv_count"], blk))
+        assert nrecv == s.n_halo * 3 * blk
         u = np.array(c["u"], copy=True)
         res = np.zeros_like(u)
         for _ in range(nsteps):
             for st in range(5):
-                proj, err, _ = orc.entropy_projection(u)
-                assert err == 0
-                send = torch.from_numpy(pack_faces(proj[:, :, nq:], halo, npf))
                 recv = torch.zeros(nrecv, dtype=torch.float64)
-                exchange_messages(send, recv, halo, nf)  # cut-face traces only, wire format
-                proj_all = np.zeros((K + s.n_halo, 3, nh))
-                proj_all[:K] = proj
-                proj_all[K:, :, nq:] = recv.numpy().reshape(s.n_halo, 3, nf)
-                du, err, _ = orc.rhs_from_proj(proj_all)
+                if scheme == capi.SCHEME_SBP:  # the neighbours' states at the cut faces' nodes
+                    send = torch.from_numpy(pack_faces(u, halo, npf, s.iarray("face_index")))
+                    exchange_messages(send, recv, halo, blk)
+                    du, err, _ = orc.rhs(np.concatenate([u, recv.numpy().reshape(s.n_halo, 3, nq)]))
+                else:
+                    proj, err, _ = orc.entropy_projection(u)
+                    assert err == 0
+                    send = torch.from_numpy(pack_faces(proj[:, :, nq:], halo, npf))
+                    exchange_messages(send, recv, halo, nf)  # cut-face traces only, wire format
+                    proj_all = np.zeros((K + s.n_halo, 3, nh))
+                    proj_all[:K] = proj
+                    proj_all[K:, :, nq:] = recv.numpy().reshape(s.n_halo, 3, nf)
+                    du, err, _ = orc.rhs_from_proj(proj_all)
                 assert err == 0
                 res = LSRK_A[st] * res + dt * du  # step_lsrk45 (solver.hpp:479-480)
                 u = u + LSRK_B[st] * res
@@ -144,17 +157,19 @@ def _rank_main(rank, P, scaling, port, dt, nsteps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scaling,P", [("strong", 2), ("strong", 3), ("weak", 2)])
-def test_gloo_partitioned_steps_equal_global_bitwise(scaling, P):
-    """World size P over gloo: 2 LSRK45 steps with per-stage cut-face exchanges; the gathered
-    state equals the single-process global run (C oracle = the reference's arithmetic) bitwise."""
+@pytest.mark.parametrize("scaling,P,scheme", [("strong", 2, 0), ("strong", 3, 0), ("weak", 2, 0), ("strong", 2, 1),
+                                              ("strong", 3, 1)])
+def test_gloo_partitioned_steps_equal_global_bitwise(scaling, P, scheme):
+    """World size P over gloo: 2 LSRK45 steps with per-stage cut-face exchanges (modal: face
+    traces; SBP: face-node states); the gathered state equals the single-process global run
+    (C oracle = the reference's arithmetic) bitwise."""
     import torch.multiprocessing as mp
 
     dt, nsteps = 1e-3, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, P, scaling, port, dt, nsteps, q)) for r in range(P)]
+    procs = [ctx.Process(target=_rank_main, args=(r, P, scaling, port, dt, nsteps, q, scheme)) for r in range(P)]
     for p in procs:
         p.start()
     got = {}
@@ -164,19 +179,19 @@ def test_gloo_partitioned_steps_equal_global_bitwise(scaling, P):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    g = case(scaling, P, -1)
+    g = case(scaling, P, -1, scheme=scheme)
     gc = case_dict(g)
     ug, _, err = Oracle(gc).step_lsrk45(gc["u"], np.zeros_like(gc["u"]), dt, nsteps)
     assert err == 0
     for r in range(P):
         np.testing.assert_array_equal(got[r][0], ug[owned_slice(scaling, P, r)])
-        # only the cut faces travel: 2 messages of nx faces, 3 faces per [3][nf] block
-        assert got[r][1] == 2 * ((NX + 2) // 3) * 3 * g.nf
+        # only the cut faces travel: 2 messages of nx faces, 3 faces per pseudo-element
+        assert got[r][1] == 2 * ((NX + 2) // 3) * 3 * stride(g)
 
 
 # ---------------------------------------------------------------------------- GPU
-def _global_steps(g, dt, nsteps, N):
-    hg = g.handle(mode=capi.MODE_FAST)
+def _global_steps(g, dt, nsteps, N, mode=capi.MODE_FAST):
+    hg = g.handle(mode=mode)
     hg.set_state(g.u0())
     hg.step(dt, nsteps)
     ug, _, tg = hg.get_state()
@@ -185,20 +200,24 @@ def _global_steps(g, dt, nsteps, N):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("N", [3, 4])
+@pytest.mark.parametrize("scheme,N,mode", [(0, 3, "fast"), (0, 4, "fast"), (0, 4, "parity"), (1, 4, "fast"),
+                                           (1, 3, "fast"), (1, 4, "parity")])
 @pytest.mark.parametrize("scaling,P", [("strong", 1), ("strong", 2), ("strong", 3), ("weak", 2)])
-def test_native_multirank_step_logical_partitions(scaling, P, N):
+def test_native_multirank_step_logical_partitions(scaling, P, scheme, N, mode):
     """swedg_step_lsrk45 on P strip handles (one host thread each, exchange callback pushing
     the packed cut faces into the peers' halo slots by device copies) == the global steps,
-    bitwise (boundary-first volume ranges, comm stream, interior overlap included)."""
+    bitwise (modal: boundary-first volume ranges, comm stream, interior overlap; SBP:
+    interior RHS during the exchange, then the cut-face elements; FAST pair kernels and
+    PARITY kernels)."""
     dt, nsteps = 1e-3, 3
-    g = case(scaling, P, -1, N=N)
-    ug, tg = _global_steps(g, dt, nsteps, N)
-    cases = [case(scaling, P, r, N=N) for r in range(P)]
-    hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
+    m = capi.MODE_FAST if mode == "fast" else capi.MODE_PARITY
+    g = case(scaling, P, -1, N=N, scheme=scheme)
+    ug, tg = _global_steps(g, dt, nsteps, N, m)
+    cases = [case(scaling, P, r, N=N, scheme=scheme) for r in range(P)]
+    hs = [c.handle(mode=m) for c in cases]
     for h, c in zip(hs, cases):
         h.set_state(c.u0())
-    LocalExchange(hs, [c.halo_desc() for c in cases], cases[0].nf).step(dt, nsteps)
+    LocalExchange(hs, [c.halo_desc() for c in cases], stride(cases[0])).step(dt, nsteps)
     for r, h in enumerate(hs):
         u, _, t = h.get_state()
         np.testing.assert_array_equal(u, ug[owned_slice(scaling, P, r)])
@@ -211,10 +230,10 @@ def test_nccl_self_exchange_single_rank_graph():
     communicator: ncclSend/ncclRecv to itself inside the captured step graph (the
     production multi-GPU code path on one device) == the unpartitioned steps, bitwise."""
     dt = 1e-3
-    for N in (3, 4):
-        g = case("strong", 1, -1, N=N)
+    for scheme, N in ((0, 3), (0, 4), (1, 4)):
+        g = case("strong", 1, -1, N=N, scheme=scheme)
         ug, tg = _global_steps(g, dt, 4, N)
-        c = case("strong", 1, 0, N=N)
+        c = case("strong", 1, 0, N=N, scheme=scheme)
         h = c.handle(mode=capi.MODE_FAST)
         comm = capi.nccl_comm_init(1, capi.nccl_unique_id(), 0, 0)
         try:
