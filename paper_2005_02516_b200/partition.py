@@ -182,23 +182,52 @@ class LocalExchange:
 
         return xfn
 
-    def step(self, dt: float, nsteps: int) -> None:
-        errs = []
+    def _threads(self, fn):
+        errs, out = [], [None] * self.P
 
-        def run(h):
+        def body(r):
             try:
-                h.step(dt, nsteps, sync=True)
+                out[r] = fn(self.h[r])
             except Exception as e:  # noqa: BLE001 - re-raised below
                 errs.append(e)
                 self.barrier.abort()
 
-        ts = [threading.Thread(target=run, args=(h,)) for h in self.h]
+        ts = [threading.Thread(target=body, args=(r,)) for r in range(self.P)]
         for t in ts:
             t.start()
         for t in ts:
             t.join()
         if errs:
             raise errs[0]
+        return out
+
+    def step(self, dt: float, nsteps: int) -> None:
+        self._threads(lambda h: h.step(dt, nsteps, sync=True))
+
+    def run(self, dt: float, tfinal: float, sample_every: int = 0):
+        """run() (run.hpp:226-262) on every rank: the device time loop with invariant
+        sampling; the ranks' exact raw invariant records are merged (swedg_diag_from_raw),
+        so the series equals the single-GPU run's bit for bit.  Returns (series, steps)."""
+        from . import capi
+
+        res = self._threads(lambda h: h.run(dt, tfinal, sample_every))
+        n = len(res[0][0])
+        raws = [h.read_invariants_raw(n) for h in self.h]
+        return capi.diag_from_raw(raws, n), res[0][1]
+
+
+def merge_invariants(h, n: int, group=None):
+    """Multi-process counterpart of LocalExchange.run's merge: every rank's raw invariant
+    records of its last run() (n samples) gathered over torch.distributed and merged
+    exactly; returns the global series [n][6] on every rank."""
+    import torch.distributed as dist
+
+    from . import capi
+
+    raw = h.read_invariants_raw(n)
+    allraw = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allraw, raw, group=group)
+    return capi.diag_from_raw(allraw, n)
 
 
 class _CudaArray:
