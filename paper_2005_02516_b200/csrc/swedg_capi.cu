@@ -2023,7 +2023,9 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
     }
     auto h2d = [&](int c) -> int {
         const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
+#ifndef SWEDG_E2E_NOCOPY  // A/B: the wavefront's launch cost without the copies
         CUDA_TRY(h, cudaMemcpyAsync(h->u + a, u_host + a, (e - a) * 8, cudaMemcpyHostToDevice, h->cp_in));
+#endif
         CUDA_TRY(h, cudaEventRecord(h->ev_in[c], h->cp_in));
         return SWEDG_OK;
     };
@@ -2031,11 +2033,12 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
     CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_step, 0));
     for (int p = 0; p < C; ++p)
         if (h2d(A[p])) return h->last_code;
-    const int ticks = 6 * (G - 1) + C + 3;
+    auto t0 = [](int g) { return 6 * g; };
+    const int ticks = t0(G - 1) + C + 3;
     for (int tau = 0; tau < ticks; ++tau) {
         for (int g = 0; g < G; ++g) {
             const int s = g % 5;
-            const int pv = tau - 6 * g;  // volume(g, pv)
+            const int pv = tau - t0(g);  // volume(g, pv)
             if (pv >= 0 && pv < C) {
                 const int c = A[pv];
                 if (s == 0) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
@@ -2043,7 +2046,7 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
                              lo(c), lo(c + 1)};
                 if (run_stage(h, sa)) return h->last_code;
             }
-            const int ps = tau - 6 * g - 3;  // interface(g, ps)
+            const int ps = tau - t0(g) - 3;  // interface(g, ps)
             if (ps >= 0 && ps < C) {
                 const int c = A[ps];
                 StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
@@ -2053,7 +2056,9 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
                     const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
                     CUDA_TRY(h, cudaEventRecord(h->ev_s4[c], h->stream));
                     CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_s4[c], 0));
+#ifndef SWEDG_E2E_NOCOPY
                     CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
+#endif
                     CUDA_TRY(h, cudaEventRecord(h->ev_out[c], h->cp_out));
                     if (g / 5 + 1 < nsteps) {
                         CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_out[c], 0));
