@@ -128,3 +128,35 @@ def test_nonfinite_sbp_rhs_message(mode):
         h.rhs(u, t=0.5)
     assert ei.value.elem == bad
     assert str(ei.value) == f"non-finite SBP RHS in element {bad} at t = 0.500000"
+
+
+def test_c5_strong_two_partitions_bitwise_k1d2048():
+    """C5's strong-scaling mesh (K1D = 2048, K = 8,388,608) cut into 2 y-strips, both ranks
+    on one GPU (one host thread each, device-copy exchange callback through the native
+    multi-rank schedule): 2 LSRK45 steps bitwise equal to the unpartitioned run."""
+    import gc
+
+    from paper_2005_02516_b200.partition import LocalExchange
+
+    g = capi.Case("smooth", N=4, nx=2048, warp=0.1, seed=23)
+    dt = g.dt
+    hg = g.handle(mode=capi.MODE_FAST, diagnostics=False)
+    hg.set_state(g.view("u0").reshape(g.K, 3, g.Np))
+    hg.step(dt, 2)
+    ug = hg.get_state(with_res=False)[0]
+    hg.close()
+    g.close()
+    del hg, g
+    gc.collect()
+    cases = [capi.Case("smooth", N=4, nx=2048, warp=0.1, seed=23, strips=2, strip=r, scaling="strong")
+             for r in range(2)]
+    assert min(c.dt for c in cases) == dt
+    hs = [c.handle(mode=capi.MODE_FAST, diagnostics=False) for c in cases]
+    for h, c in zip(hs, cases):
+        h.set_state(c.view("u0").reshape(c.K, 3, c.Np))
+    LocalExchange(hs, [c.halo_desc() for c in cases], cases[0].nf).step(dt, 2)
+    off = 0
+    for h, c in zip(hs, cases):
+        np.testing.assert_array_equal(h.get_state(with_res=False)[0], ug[off:off + c.K])
+        off += c.K
+    assert off == ug.shape[0]
