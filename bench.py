@@ -314,15 +314,15 @@ SBP_FLOP_N4 = 55 * 666 + 33 * 15 + 7 * 37  # SURVEY §8(d) SBP N=4 (volume + sur
 def secondary_rooflines(args, fp64_peak):
     """Driver-visible fractions of the two other FP64-bound kernels:
     C3's SBP N=4 pair kernel (dam break, K1D=128, the config's own size) and the modal
-    N=3 pair kernel (the C1/C2 degree) on the C4 generator at K1D=512."""
+    N=3 pair kernel (the C1/C2 degree) on the C4 generator at K1D=1024."""
     from paper_2005_02516_b200 import capi
 
     out = {}
     runs = [("roofline_c3", "sbp_rhs_pair_n4_kernel (C3: SBP N=4 dam break K1D=128, RHS + fused LSRK45 update)",
              lambda: capi.Case("dambreak", scheme=capi.SCHEME_SBP, N=4, nx=128, cfl=0.0625), SBP_FLOP_N4, 60),
-            ("roofline_n3", "modal_volume_pair_n3_kernel (modal N=3, C4 generator K1D=512: projection + flux "
-             "differencing + volume lift)", lambda: capi.Case("smooth", N=3, nx=512, warp=args.warp, seed=23),
-             flops_bytes_per_element(3)["vol_flops"], 10)]
+            ("roofline_n3", "modal_volume_pair_n3_kernel (modal N=3, the C4 generator at K1D=1024: projection + "
+             "flux differencing + volume lift)", lambda: capi.Case("smooth", N=3, nx=1024, warp=args.warp, seed=23),
+             flops_bytes_per_element(3)["vol_flops"], 5)]
     for key, kname, mk, flop, steps in runs:
         try:
             c = mk()
