@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -541,28 +542,50 @@ int halo_exchange(swedg_handle h, int stage, double* sbp_state = nullptr) {
 }
 
 // Multi-rank stage schedule: boundary volume -> pack + exchange on the comm stream,
-// overlapped with the interior volume kernel -> interface/update kernel.
+// overlapped with the interior volume kernel -> interface/update kernel.  Host-state
+// stepping hooks: wait_in(k0) before a volume range of stage 0 (its H2D), and the last
+// stage's interface kernel by `out_ranges` with done(range index) after each.
+struct HaloHooks {
+    std::vector<std::pair<int, int>> inner;  // interior volume ranges (default: h->int_ranges)
+    std::function<int(int, int)> wait_in;    // (k0, k1) -> status
+    std::vector<std::pair<int, int>> out_ranges;
+    std::function<int(int)> done;
+};
+
+int run_stage_halo(swedg_handle h, int s, const unsigned* ids, double dt, const HaloHooks* hk) {
+    for (const auto& r : h->bnd_ranges) {
+        if (hk && s == 0 && hk->wait_in(r.first, r.second)) return h->last_code;
+        StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
+        if (run_stage(h, sa)) return h->last_code;
+    }
+    CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
+    if (halo_exchange(h, s)) return h->last_code;
+    CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+    for (const auto& r : hk ? hk->inner : h->int_ranges) {
+        if (hk && s == 0 && hk->wait_in(r.first, r.second)) return h->last_code;
+        StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
+        if (run_stage(h, sa)) return h->last_code;
+    }
+    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    if (hk && s == 4) {
+        for (size_t i = 0; i < hk->out_ranges.size(); ++i) {
+            const auto& r = hk->out_ranges[i];
+            StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
+            if (run_stage(h, ss) || hk->done((int)i)) return h->last_code;
+        }
+        return SWEDG_OK;
+    }
+    StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
+    return run_stage(h, ss);
+}
+
 int run_step_halo_sbp(swedg_handle h, const unsigned* ids, double dt);
 
 int run_step_halo(swedg_handle h, const unsigned* ids, double dt) {
     if (h->scheme == SWEDG_SCHEME_SBP) return run_step_halo_sbp(h, ids, dt);
-    for (int s = 0; s < 5; ++s) {
-        for (const auto& r : h->bnd_ranges) {
-            StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
-            if (run_stage(h, sa)) return h->last_code;
-        }
-        CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));
-        CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
-        if (halo_exchange(h, s)) return h->last_code;
-        CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
-        for (const auto& r : h->int_ranges) {
-            StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
-            if (run_stage(h, sa)) return h->last_code;
-        }
-        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
-        StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
-        if (run_stage(h, ss)) return h->last_code;
-    }
+    for (int s = 0; s < 5; ++s)
+        if (run_stage_halo(h, s, ids, dt, nullptr)) return h->last_code;
     return SWEDG_OK;
 }
 
@@ -2074,6 +2097,81 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
 }
 }  // namespace
 
+namespace {
+// Host-state steps of a multi-rank (modal) handle: each step's H2D goes by element
+// ranges — the ranges owning sent faces first, then the interior in `C` chunks — and the
+// stage-0 volume kernel of a range waits only for that range's copy; the last stage's
+// interface kernel runs by the same ranges, each range's D2H starting right after it,
+// and the next step's H2D of a range waits only for its D2H.  The halo exchanges run as
+// in swedg_step_lsrk45.  Bitwise the device-resident steps.
+int step_host_halo(swedg_handle h, double* u_host, double dt, int nsteps, int C) {
+    const size_t per = (size_t)3 * h->Np;
+    HaloHooks hk;
+    for (const auto& r : h->int_ranges) {  // interior split into ~C chunks (even bounds)
+        const int n = std::max(1, std::min(C, (r.second - r.first) / 2));
+        for (int i = 0; i < n; ++i) {
+            int a = r.first + (int)((long)(r.second - r.first) * i / n), b = r.first + (int)((long)(r.second - r.first) * (i + 1) / n);
+            if (i > 0) a &= ~1;
+            if (i + 1 < n) b &= ~1;
+            if (b > a) hk.inner.push_back({a, b});
+        }
+    }
+    std::vector<std::pair<int, int>> R = h->bnd_ranges;  // copy ranges: boundary first, then the interior
+    R.insert(R.end(), hk.inner.begin(), hk.inner.end());
+    hk.out_ranges = R;
+    if (!h->cp_in) {
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_in, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_out, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_step, cudaEventDisableTiming));
+    }
+    while (h->ev_in.size() < R.size() || h->ev_s4.size() < R.size()) {
+        cudaEvent_t a, b, c;
+        CUDA_TRY(h, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+        h->ev_in.push_back(a);
+        h->ev_out.push_back(b);
+        h->ev_s4.push_back(c);
+    }
+    auto index_of = [&](int k0) {
+        for (size_t i = 0; i < R.size(); ++i)
+            if (R[i].first == k0) return (int)i;
+        return -1;
+    };
+    hk.wait_in = [&](int k0, int) -> int {
+        const int i = index_of(k0);
+        if (i >= 0) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[i], 0));
+        return SWEDG_OK;
+    };
+    hk.done = [&](int i) -> int {
+        const size_t a = (size_t)R[i].first * per, e = (size_t)R[i].second * per;
+        CUDA_TRY(h, cudaEventRecord(h->ev_s4[i], h->stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->cp_out, h->ev_s4[i], 0));
+        CUDA_TRY(h, cudaMemcpyAsync(u_host + a, h->u + a, (e - a) * 8, cudaMemcpyDeviceToHost, h->cp_out));
+        CUDA_TRY(h, cudaEventRecord(h->ev_out[i], h->cp_out));
+        return SWEDG_OK;
+    };
+    CUDA_TRY(h, cudaEventRecord(h->ev_step, h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_step, 0));
+    for (int n = 0; n < nsteps; ++n) {
+        for (size_t i = 0; i < R.size(); ++i) {
+            if (n > 0) CUDA_TRY(h, cudaStreamWaitEvent(h->cp_in, h->ev_out[i], 0));
+            const size_t a = (size_t)R[i].first * per, e = (size_t)R[i].second * per;
+            CUDA_TRY(h, cudaMemcpyAsync(h->u + a, u_host + a, (e - a) * 8, cudaMemcpyHostToDevice, h->cp_in));
+            CUDA_TRY(h, cudaEventRecord(h->ev_in[i], h->cp_in));
+        }
+        const double t0 = h->t;
+        unsigned ids[5];
+        for (int s = 0; s < 5; ++s) ids[s] = new_stage(h, t0 + Lsrk45::c[s] * dt);
+        for (int s = 0; s < 5; ++s)
+            if (run_stage_halo(h, s, ids, dt, &hk)) return h->last_code;
+        h->t = t0 + dt;
+    }
+    for (size_t i = 0; i < R.size(); ++i) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_out[i], 0));
+    return check_errors(h);
+}
+}  // namespace
+
 // The reference's step_lsrk45 on a HOST-resident state (solver.hpp:466-484 called
 // in a loop with state.u on the host): every step's input is read from u_host
 // and its result written back to u_host.  The copies are pipelined with the
@@ -2087,6 +2185,8 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
     if (nsteps < 0) return fail(h, SWEDG_ERR_INVALID, "nsteps must be >= 0");
     cudaSetDevice(h->device);
     const size_t per = (size_t)3 * h->nstate();
+    if (h->scheme == SWEDG_SCHEME_HYBRIDIZED && halo_active(h) && nsteps > 0)
+        return step_host_halo(h, u_host, dt, nsteps, nchunks > 0 ? nchunks : 16);
     if (h->scheme != SWEDG_SCHEME_HYBRIDIZED || h->n_halo > 0) {  // unchunked: copy, step, copy
         for (int n = 0; n < nsteps; ++n) {
             CUDA_TRY(h, cudaMemcpyAsync(h->u, u_host, per * h->K * 8, cudaMemcpyHostToDevice, h->stream));

@@ -204,6 +204,12 @@ class LocalExchange:
     def step(self, dt: float, nsteps: int) -> None:
         self._threads(lambda h: h.step(dt, nsteps, sync=True))
 
+    def step_host(self, states, dt: float, nsteps: int, nchunks: int = 0) -> None:
+        """swedg_step_lsrk45_host on every rank: states[r] (host, C-contiguous float64,
+        updated in place) round-trips through host memory every step."""
+        hs = list(self.h)
+        self._threads(lambda h: h.step_host(states[hs.index(h)], dt, nsteps, nchunks))
+
     def run(self, dt: float, tfinal: float, sample_every: int = 0):
         """run() (run.hpp:226-262) on every rank: the device time loop with invariant
         sampling; the ranks' exact raw invariant records are merged (swedg_diag_from_raw),

@@ -225,6 +225,29 @@ def test_native_multirank_step_logical_partitions(scaling, P, scheme, N, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P,nchunks", [(1, 3), (2, 4), (3, 16)])
+def test_multirank_host_state_steps_equal_global(P, nchunks):
+    """swedg_step_lsrk45_host on strip handles (H2D by element ranges, the ranges owning
+    sent faces first; stage-0 volume kernels wait per range; the last interface kernel by
+    ranges, each range's D2H right after it) == the global device-resident steps, bitwise;
+    the host buffers hold every step's result."""
+    dt, nsteps = 1e-3, 3
+    g = case("strong", P, -1, N=4)
+    ug, tg = _global_steps(g, dt, nsteps, 4)
+    cases = [case("strong", P, r, N=4) for r in range(P)]
+    hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
+    us = [np.ascontiguousarray(c.u0()) for c in cases]
+    for h, u in zip(hs, us):
+        h.set_state(u)
+    LocalExchange(hs, [c.halo_desc() for c in cases], stride(cases[0])).step_host(us, dt, nsteps, nchunks)
+    for r, (h, u) in enumerate(zip(hs, us)):
+        np.testing.assert_array_equal(u, ug[owned_slice("strong", P, r)])
+        ud, _, t = h.get_state()
+        np.testing.assert_array_equal(ud, u)
+        assert t == tg
+
+
+@pytest.mark.gpu
 def test_nccl_self_exchange_single_rank_graph():
     """One rank whose halos are its own periodic cut (strong, P = 1) with a one-rank NCCL
     communicator: ncclSend/ncclRecv to itself inside the captured step graph (the
