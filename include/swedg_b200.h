@@ -137,8 +137,9 @@ typedef struct {
 } swedg_halo_desc;
 
 /* Custom transport: called once per RK stage on the host while the stage is
- * enqueued, after the boundary elements' traces were packed into `send` (device,
- * the send messages back to back in wire format).  It must enqueue on `stream`
+ * enqueued, after the cut faces were packed into `send` (device, the send messages
+ * back to back in wire format; modal: projected traces, [3][nf] pseudo-elements;
+ * SBP: the stage input's face-node states, [3][nq] pseudo-elements).  It must enqueue on `stream`
  * (cudaStream_t) whatever fills `recv` (device, the halo slots = receive messages
  * back to back) and return 0; the interface kernel waits on `stream`. */
 typedef int (*swedg_exchange_fn)(void* user, int stage, const double* send, double* recv, void* stream);
@@ -220,7 +221,9 @@ int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d);
  * communicator is destroyed. */
 int swedg_set_nccl_comm(swedg_handle h, void* comm);
 int swedg_set_exchange(swedg_handle h, swedg_exchange_fn fn, void* user);
-/* Device pointers and sizes (doubles) of the packed send messages and the halo slots. */
+/* Device pointers and sizes (doubles) of the packed send messages and the halo slots
+ * (modal: in the face-trace buffer; SBP: in the state buffer — the SBP FAST path rotates
+ * the stage input over three buffers, so its callbacks receive each stage's `recv`). */
 int swedg_halo_buffers(swedg_handle h, double** send, size_t* n_send, double** recv, size_t* n_recv);
 /* Pack the cut-face traces of the current stage into the send buffer (stage-level
  * API: after the volume ranges that own sent faces, before the exchange). */
