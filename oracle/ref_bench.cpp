@@ -11,6 +11,9 @@
 //
 //   swedg_refbench N K1D warmup steps threads [warp]
 //   swedg_refbench ratio K threads     (bench.hpp ratio_sweep: the R_CPU study, CSV)
+//   swedg_refbench run PROBLEM N SCHEME K1D warp cfl tfinal threads
+//       the reference's build_case + run() (run.hpp:214-284) on lake|vortex|dambreak,
+//       SCHEME hybridized|sbp (Gauss-Legendre edges): time to solution, one JSON line
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -28,6 +31,36 @@ int main(int argc, char** argv) {
     if (argc >= 2 && std::string(argv[1]) == "ratio") {
         int K = argc > 2 ? std::atoi(argv[2]) : 64, threads = argc > 3 ? std::atoi(argv[3]) : 1;
         std::fputs(ratios_csv(ratio_sweep(default_bench_sizes(), K, threads, 0)).c_str(), stdout);
+        return 0;
+    }
+    if (argc >= 2 && std::string(argv[1]) == "run") {
+        if (argc < 10) {
+            std::fprintf(stderr, "usage: swedg_refbench run PROBLEM N SCHEME K1D warp cfl tfinal threads\n");
+            return 2;
+        }
+        RunConfig cfg;
+        const std::string prob = argv[2], scheme = argv[4];
+        cfg.problem = prob == "lake" ? ProblemId::Lake : prob == "vortex" ? ProblemId::Vortex : ProblemId::DamBreak;
+        cfg.degree = std::atoi(argv[3]);
+        cfg.scheme = scheme == "sbp" ? Scheme::SbpLegendre : Scheme::Hybridized;
+        cfg.nx = cfg.ny = std::atoi(argv[5]);
+        cfg.warp = std::atof(argv[6]);
+        cfg.cfl = std::atof(argv[7]);
+        cfg.tfinal = std::atof(argv[8]);
+        cfg.threads = std::atoi(argv[9]);
+        if (cfg.threads <= 0) cfg.threads = (int)std::thread::hardware_concurrency();
+        cfg.validate();
+        auto t0 = std::chrono::steady_clock::now();
+        Case c = build_case(cfg);
+        auto t1 = std::chrono::steady_clock::now();
+        RunResult r = run(c);
+        auto t2 = std::chrono::steady_clock::now();
+        std::printf("{\"problem\": \"%s\", \"K\": %d, \"steps\": %d, \"dt\": %.17g, \"t\": %.17g, "
+                    "\"run_s\": %.6g, \"setup_s\": %.6g, \"threads\": %d, \"samples\": %zu, "
+                    "\"l2_h\": %.17g}\n",
+                    prob.c_str(), c.num_elements(), r.steps, r.dt, c.time(),
+                    std::chrono::duration<double>(t2 - t1).count(), std::chrono::duration<double>(t1 - t0).count(),
+                    cfg.threads, r.series.size(), r.has_error ? r.error.err_h : -1.0);
         return 0;
     }
     if (argc < 6) {

@@ -110,10 +110,11 @@ constexpr int kDiagBatch = 8;  // elements per warp batch: N=4 -> 8 x 36 = 288 (
 template <int N>
 struct DiagDims {
     static constexpr int Np = (N + 1) * (N + 2) / 2;
-    static constexpr int nq_max = 64;  // SBP nodes staged (N <= 4: 37)
-    // per-warp staging: per element u (3 Np), b (Np), map (2 Np); SBP nodal scratch (4 nq_max)
+    // per-warp staging (dynamic shared memory): per element u (3 Np), b (Np), map (2 Np);
+    // SBP: the batch's nodal u and b, [kDiagBatch][4][nq]
     static constexpr int elem_doubles = 6 * Np;
-    static constexpr int warp_doubles = kDiagBatch * elem_doubles + 4 * nq_max;
+    static constexpr int nq_max = 128;  // SBP staging of 4 warps stays within the shared memory
+    static size_t warp_doubles(int sbp_nq) { return (size_t)kDiagBatch * (elem_doubles + 4 * sbp_nq); }
 };
 
 // Warp-cooperative exact accumulation: every lane offers one term x (0 = none);
@@ -181,15 +182,15 @@ __global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
     constexpr int Np = D::Np;
     constexpr int L = exact::kLimbs;
     __shared__ long long acc[kDiagWarps][4][L];
-    __shared__ double stage[kDiagWarps][D::warp_doubles];
+    extern __shared__ __align__(16) double stage[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kDiagWarps * 4 * L; i += blockDim.x) (&acc[0][0][0])[i] = 0;
     __syncthreads();
 
-    long long(*W)[L] = acc[wid];
-    double* sw = stage[wid];                         // [batch][6 Np]: u (3 Np) | b (Np) | map (2 Np)
-    double* sn = sw + kDiagBatch * D::elem_doubles;  // SBP nodal scratch [4][nq]
     const int nfine = P.nfine, nq = P.nq;
+    long long(*W)[L] = acc[wid];
+    double* sw = stage + (size_t)wid * kDiagBatch * (D::elem_doubles + (P.sbp ? 4 * nq : 0));  // [batch][6 Np]: u | b | map
+    double* sn = sw + kDiagBatch * D::elem_doubles;  // SBP: the batch's nodal u | b, [batch][4][nq]
     const double* V = P.fine + nfine;
     const bool inv = P.what == kDiagInvariants;
     const bool exact_sol = P.what == kDiagL2Vortex || P.what == kDiagL2Lake;
@@ -202,23 +203,34 @@ __global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
         const int ne = (int)min((long)kDiagBatch, (long)P.K - k0);
         // ---- stage the batch (coalesced: consecutive elements are contiguous)
         if (P.sbp) {
-            for (int e = 0; e < ne; ++e) {
-                const long k = k0 + e;
-                double* se = sw + e * D::elem_doubles;
-                __syncwarp();
-                for (int x = lane; x < 3 * nq; x += 32) sn[x] = P.u[(size_t)k * 3 * nq + x];
-                if (inv)
-                    for (int x = lane; x < nq; x += 32) sn[3 * nq + x] = P.b[(size_t)k * nq + x];
-                __syncwarp();
-                // project_nodal: (Pq u)(n, c) = sum_q Pq(n, q) u(q, c), q ascending (diagnostics.hpp:226-230)
-                const int ncol = inv ? 4 : 3;
-                for (int x = lane; x < ncol * Np; x += 32) {
-                    const int c = x / Np, m = x - c * Np;
-                    double s = 0.0;
-                    for (int q = 0; q < nq; ++q)
-                        s = __dadd_rn(s, __dmul_rn(__ldg(P.Pq + m + (size_t)q * Np), sn[c * nq + q]));
-                    se[x] = s;  // c = 3 lands in the b slot (3 Np)
+            // the batch's nodal blocks in one pass (contiguous: coalesced, all loads in flight)
+            for (int x = lane; x < ne * 3 * nq; x += 32) {
+                const int e = x / (3 * nq);
+                sn[e * 4 * nq + (x - e * 3 * nq)] = P.u[(size_t)k0 * 3 * nq + x];
+            }
+            if (inv)
+                for (int x = lane; x < ne * nq; x += 32) {
+                    const int e = x / nq;
+                    sn[e * 4 * nq + 3 * nq + (x - e * nq)] = P.b[(size_t)k0 * nq + x];
                 }
+            __syncwarp();
+            // project_nodal: (Pq u)(n, c) = sum_q Pq(n, q) u(q, c), q ascending (diagnostics.hpp:226-230);
+            // lane -> (c, n), one Pq load feeds the batch's elements (independent chains)
+            const int ncol = inv ? 4 : 3;
+            for (int x = lane; x < ncol * Np; x += 32) {
+                const int c = x / Np, m = x - c * Np;
+                double sacc[kDiagBatch];
+#pragma unroll
+                for (int e = 0; e < kDiagBatch; ++e) sacc[e] = 0.0;
+                for (int q = 0; q < nq; ++q) {
+                    const double pq = __ldg(P.Pq + m + (size_t)q * Np);
+#pragma unroll
+                    for (int e = 0; e < kDiagBatch; ++e)
+                        sacc[e] = __dadd_rn(sacc[e], __dmul_rn(pq, sn[e * 4 * nq + c * nq + q]));
+                }
+#pragma unroll
+                for (int e = 0; e < kDiagBatch; ++e)
+                    if (e < ne) sw[e * D::elem_doubles + x] = sacc[e];  // c = 3 lands in the b slot (3 Np)
             }
         } else {
             for (int x = lane; x < ne * 3 * Np; x += 32) {

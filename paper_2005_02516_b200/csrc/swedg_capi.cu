@@ -70,6 +70,7 @@ struct swedg_handle_s {
     double* u = nullptr;     // resident state
     double* u_alt = nullptr;  // SBP pair path: state buffers of the fused RK stages (u -> A -> B -> A -> B -> u)
     double* u_alt2 = nullptr;
+    int diag_occ = 0;  // resident diag_kernel CTAs per SM (its staging size depends on the scheme)
     double* res = nullptr;   // LSRK register
     double* utmp = nullptr;  // host-API scratch state
     double* du = nullptr;    // host-API scratch rhs
@@ -746,9 +747,17 @@ void launch_diag_n(swedg_handle h, const double* u, int what, double t, const do
     P.rec = rec;
     auto kern = diag_kernel<N>;
     const int threads = 32 * kDiagWarps;
-    int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, threads, 0);
-    int grid = std::min((h->K + kDiagWarps - 1) / kDiagWarps, occ * h->nsm);
-    kern<<<std::max(grid, 1), threads, 0, h->stream>>>(P);
+    const size_t smem = sizeof(double) * kDiagWarps * DiagDims<N>::warp_doubles(P.sbp ? h->nq : 0);
+    if (h->diag_occ == 0) {  // per handle: the staging size depends on the scheme
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        h->diag_occ = std::max(occ, 1);
+    } else {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    int grid = std::min((h->K + kDiagWarps - 1) / kDiagWarps, h->diag_occ * h->nsm);
+    kern<<<std::max(grid, 1), threads, smem, h->stream>>>(P);
     h->launches += 2;
 }
 
