@@ -66,10 +66,17 @@ def parse():
     # functional check of the multi-rank orchestration on a single-GPU box (no timing
     # claims): every rank on device 0, halos exchanged over gloo through host memory
     p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
+    # halo transport: peer-memory stores + stream flags (one node; default), NCCL, or the
+    # host-staged gloo callback (default with --shared-device / --dist-backend gloo)
+    p.add_argument("--transport", choices=["p2p", "nccl", "gloo"], default=None)
     p.add_argument("--shared-device", action="store_true")
     a = p.parse_args()
     if a.k1d is None:
         a.k1d = 2048 if a.scaling == "strong" else 1024
+    if a.shared_device:  # NCCL refuses two ranks on one GPU: plumbing over gloo
+        a.dist_backend = "gloo"
+    if a.transport is None:
+        a.transport = "gloo" if (a.shared_device or a.dist_backend == "gloo") else "p2p"
     return a
 
 
@@ -409,15 +416,28 @@ def run_ours(args, rank, world, local):
     comm = None
     transport = "none (one rank)"
     if world > 1:
-        from paper_2005_02516_b200.partition import attach_gloo, attach_nccl
+        from paper_2005_02516_b200.partition import attach_gloo, attach_nccl, attach_p2p
 
         halo = case.halo_desc()
-        if args.shared_device or args.dist_backend == "gloo":
+        if args.transport == "gloo":
             attach_gloo(h, halo, case.nf)  # functional check only (ranks share a GPU)
             transport = "gloo (host-staged exchange callback; functional, not a performance path)"
         else:
-            comm = attach_nccl(h, halo, world, rank, local)
-            transport = "NCCL send/recv of packed cut-face traces (library-owned communicator)"
+            if args.transport == "p2p":
+                ok = 1.0
+                try:
+                    attach_p2p(h, rank, world)
+                except capi.SwedgError as e:  # e.g. no peer access between these GPUs
+                    print(f"[bench] rank {rank}: peer-memory transport unavailable ({e})", file=sys.stderr)
+                    ok = 0.0
+                if allreduce(ok, dist.ReduceOp.MIN) == 1.0:  # every rank attached, or none uses it
+                    transport = ("peer memory: cut-face traces stored into the peers' halo slots over NVLink "
+                                 "(CUDA IPC), stream-ordered flags, in the step graph")
+                else:
+                    h.set_p2p(rank, None)
+            if not transport.startswith("peer"):
+                comm = attach_nccl(h, halo, world, rank, local)
+                transport = "NCCL send/recv of packed cut-face traces (library-owned communicator)"
         dt = allreduce(dt, dist.ReduceOp.MIN)  # the global mesh's dt (owned minimum edges)
     dof_total = int(allreduce(float(dof), dist.ReduceOp.SUM)) if dist else dof
     setup_s = time.time() - t0

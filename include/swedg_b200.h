@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define SWEDG_ABI_VERSION 4
+#define SWEDG_ABI_VERSION 5
 
 /* status codes */
 #define SWEDG_OK 0
@@ -207,11 +207,11 @@ int swedg_stage_surface_range(swedg_handle h, int stage, double dt, int k0, int 
 int swedg_trace_device_ptr(swedg_handle h, double** trace, long long* n_owned, long long* n_halo);
 
 /* ---- multi-rank stepping ------------------------------------------------------
- * With a halo map and a transport (NCCL communicator or exchange callback),
+ * With a halo map and a transport (NCCL communicator, peer memory or exchange callback),
  * swedg_step_lsrk45 runs every stage as: projection+volume kernel on the elements
  * owning sent faces -> pack -> exchange on a second stream, overlapped with the
- * interior volume kernel -> interface/update kernel after the exchange.  With NCCL
- * the step is captured once into a CUDA graph and replayed.  Results are bitwise
+ * interior volume kernel -> interface/update kernel after the exchange.  With NCCL or
+ * peer memory the step is captured once into a CUDA graph and replayed.  Results are bitwise
  * independent of the partition (per-element arithmetic is unchanged). */
 int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d);
 /* NCCL transport: comm is an ncclComm_t whose ranks are the peers of the halo map
@@ -237,6 +237,24 @@ int swedg_halo_ranges(swedg_handle h, int* ranges, int max_ranges, int* n_bounda
 int swedg_nccl_unique_id(void* id);
 int swedg_nccl_comm_init(int nranks, const void* id, int rank, int device, void** comm);
 int swedg_nccl_comm_destroy(void* comm);
+/* Peer-memory transport (the ranks of one node, NVLink / NVSwitch): instead of a send
+ * buffer and NCCL, the pack kernel stores each cut-face trace straight into the
+ * destination rank's halo slot over peer memory, and 32-bit flags in the ranks' memory,
+ * written and waited on by the streams themselves (cuStreamWriteValue32 /
+ * cuStreamWaitValue32), order every stage's exchange: the sender waits until the
+ * receiver consumed the previous stage's halo, stores, then raises the receiver's
+ * "ready" flag; the receiver's interface (SBP: boundary RHS) kernel waits for it, then
+ * raises the sender's "free" flag.  No host synchronisation; captured into the step graph.
+ * swedg_p2p_export writes this rank's descriptor (SWEDG_P2P_BLOB_BYTES bytes: IPC
+ * handles and addresses of its halo slots and flags, its receive table) and initialises
+ * its flags; every rank gathers all descriptors (e.g. torch.distributed all_gather) and
+ * passes them, concatenated in rank order, to swedg_set_p2p (after swedg_set_halo).
+ * Peers in the same process are addressed directly, others through
+ * cudaIpcOpenMemHandle.  Every rank must run the same stages; after an error, export
+ * and attach again.  blobs NULL detaches. */
+#define SWEDG_P2P_BLOB_BYTES 4096
+int swedg_p2p_export(swedg_handle h, int rank, void* blob);
+int swedg_set_p2p(swedg_handle h, int rank, int nranks, const void* blobs);
 /* Check the device error record (syncs the stream). */
 int swedg_check(swedg_handle h);
 

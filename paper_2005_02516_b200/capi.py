@@ -71,7 +71,7 @@ class _Desc(C.Structure):
     ]
 
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 _lib = None
 
 
@@ -158,6 +158,8 @@ def lib() -> C.CDLL:
     L.swedg_nccl_unique_id.argtypes = [vp]
     L.swedg_nccl_comm_init.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
     L.swedg_nccl_comm_destroy.argtypes = [vp]
+    L.swedg_p2p_export.argtypes = [vp, C.c_int, vp]
+    L.swedg_set_p2p.argtypes = [vp, C.c_int, C.c_int, vp]
     _lib = L
     return L
 
@@ -176,7 +178,9 @@ EXPORTED = [
     "swedg_step_lsrk45_host", "swedg_stage_volume_range", "swedg_stage_surface_range",
     "swedg_set_halo", "swedg_set_nccl_comm", "swedg_set_exchange", "swedg_halo_buffers", "swedg_halo_pack",
     "swedg_halo_ranges", "swedg_nccl_unique_id", "swedg_nccl_comm_init", "swedg_nccl_comm_destroy",
+    "swedg_p2p_export", "swedg_set_p2p",
 ]
+P2P_BLOB_BYTES = 4096  # SWEDG_P2P_BLOB_BYTES
 
 
 def _f64(a) -> np.ndarray:
@@ -368,6 +372,23 @@ class Handle:
 
     def set_nccl_comm(self, comm: int | None):
         self._check(self._lib.swedg_set_nccl_comm(self._h, C.c_void_p(comm) if comm else None))
+
+    def p2p_export(self, rank: int) -> bytes:
+        """This rank's peer-memory descriptor (swedg_p2p_export; resets its exchange flags)."""
+        buf = C.create_string_buffer(P2P_BLOB_BYTES)
+        self._check(self._lib.swedg_p2p_export(self._h, int(rank), buf))
+        return buf.raw
+
+    def set_p2p(self, rank: int, blobs):
+        """Peer-memory transport from every rank's descriptor (a list in rank order, or
+        their concatenation); None detaches."""
+        if blobs is None:
+            self._check(self._lib.swedg_set_p2p(self._h, int(rank), 0, None))
+            return
+        raw = b"".join(blobs) if isinstance(blobs, (list, tuple)) else bytes(blobs)
+        n = len(raw) // P2P_BLOB_BYTES
+        buf = C.create_string_buffer(raw, len(raw))
+        self._check(self._lib.swedg_set_p2p(self._h, int(rank), n, buf))
 
     def set_exchange(self, fn):
         """fn(stage, send_ptr, recv_ptr, stream_ptr) -> None, called at enqueue time on the

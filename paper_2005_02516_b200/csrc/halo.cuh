@@ -38,6 +38,68 @@ __global__ void halo_pack_kernel(HaloPackParams p) {
     if (i < p.n) p.buf[p.dst[i]] = p.base[p.src[i]];
 }
 
+// Peer-memory variant: the entry goes straight to the destination rank's halo slot,
+// rbase[rpeer[i]] + rdst[i] (the peer's buffer, mapped into this process).
+struct HaloPackP2PParams {
+    const double* base;
+    const long long* src;    // [n] offsets into base
+    const long long* rdst;   // [n] offsets into the destination buffer
+    const int* rpeer;        // [n] index into rbase
+    double* const* rbase;    // destination buffers (peer memory)
+    long long n;
+};
+
+__global__ void halo_pack_p2p_kernel(HaloPackP2PParams p) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < p.n) p.rbase[p.rpeer[i]][p.rdst[i]] = p.base[p.src[i]];
+}
+
+// Stream memory operations (driver API, resolved through the runtime: no libcuda link).
+struct StreamMemOps {
+    int (*wait32)(cudaStream_t, unsigned long long, unsigned int, unsigned int) = nullptr;
+    int (*write32)(cudaStream_t, unsigned long long, unsigned int, unsigned int) = nullptr;
+    bool ok = false;
+};
+constexpr unsigned kWaitEq = 0x1;     // CU_STREAM_WAIT_VALUE_EQ
+constexpr unsigned kWaitFlush = 1u << 30;  // CU_STREAM_WAIT_VALUE_FLUSH
+
+inline StreamMemOps& stream_mem_ops() {
+    static StreamMemOps ops;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q1, q2;
+        void* w = nullptr;
+        void* x = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &x, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && x) {
+            ops.wait32 = reinterpret_cast<int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int)>(w);
+            ops.write32 = reinterpret_cast<int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int)>(x);
+            ops.ok = true;
+        }
+    });
+    return ops;
+}
+
+// This rank's descriptor for the peer-memory transport (swedg_p2p_export): the halo
+// slots' buffers (modal: the trace buffer; SBP: the three state buffers) and the flag
+// array by IPC handle and by address, and the receive table (message pairing).
+constexpr int kP2pMaxRanks = 1024;  // flags: [0, R) ready from rank r, [R, 2R) free from rank r
+constexpr int kP2pMaxMsgs = 64;
+struct P2pBlob {
+    uint32_t magic, version;
+    int rank, pid, device, nbuf;
+    cudaIpcMemHandle_t buf_ipc[3];
+    unsigned long long buf_ptr[3];
+    long long halo_off;  // doubles from a buffer's base to its halo slots
+    cudaIpcMemHandle_t flag_ipc;
+    unsigned long long flag_ptr;
+    int n_recv;
+    int recv_peer[kP2pMaxMsgs];
+    long long recv_off[kP2pMaxMsgs], recv_len[kP2pMaxMsgs];  // doubles from the halo slots
+};
+constexpr uint32_t kP2pMagic = 0x50325053u;  // "SP2P"
+
 // ---- NCCL, resolved at run time ---------------------------------------------
 // The library does not link libnccl: it binds the symbols of the libnccl.so.2 the
 // process already has (torch's, when called from Python) or loads it, so the

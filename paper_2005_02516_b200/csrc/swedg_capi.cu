@@ -7,6 +7,7 @@
 // stream-ordered on the handle's stream; host-pointer entry points copy in,
 // launch, copy out and check the device error record.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -142,6 +143,17 @@ struct swedg_handle_s {
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
     std::vector<int> fidx_host;  // SBP face_index (halo pack: face node -> volume node)
+    // peer-memory transport (swedg_p2p_export / swedg_set_p2p, halo.cuh)
+    bool p2p = false;
+    int p2p_rank = -1;
+    unsigned* p2p_flags = nullptr;               // own flags [2 kP2pMaxRanks]: ready from r | free from r
+    std::vector<int> p2p_send_peers, p2p_recv_peers;  // distinct destination / source ranks
+    std::vector<unsigned long long> p2p_ready_at;     // per send peer: its ready[rank]
+    std::vector<unsigned long long> p2p_free_at;      // per recv peer: its free[rank]
+    long long* p2p_rdst = nullptr;               // [n_pack] offsets in the destination buffer
+    int* p2p_rpeer = nullptr;                    // [n_pack] destination (index into p2p_rbase)
+    double** p2p_rbase[3] = {nullptr, nullptr, nullptr};  // per state buffer: peers' halo-slot buffers
+    std::vector<void*> p2p_opened;               // IPC mappings to close
     int nstate() const { return scheme == SWEDG_SCHEME_SBP ? nq : Np; }
 };
 
@@ -500,7 +512,39 @@ bool sbp_pair_path(swedg_handle h) {
     return h->scheme == SWEDG_SCHEME_SBP && h->mode == SWEDG_MODE_FAST && h->N == 4;
 }
 
-bool halo_active(swedg_handle h) { return h->halo_set && (h->nccl || h->xfn); }
+bool halo_active(swedg_handle h) { return h->halo_set && (h->nccl || h->xfn || h->p2p); }
+
+void p2p_detach(swedg_handle h) {
+    for (void* p : h->p2p_opened) cudaIpcCloseMemHandle(p);
+    h->p2p_opened.clear();
+    for (void* p : {(void*)h->p2p_rdst, (void*)h->p2p_rpeer, (void*)h->p2p_rbase[0], (void*)h->p2p_rbase[1],
+                    (void*)h->p2p_rbase[2]})
+        if (p) cudaFree(p);
+    h->p2p_rdst = nullptr;
+    h->p2p_rpeer = nullptr;
+    h->p2p_rbase[0] = h->p2p_rbase[1] = h->p2p_rbase[2] = nullptr;
+    h->p2p_send_peers.clear();
+    h->p2p_recv_peers.clear();
+    h->p2p_ready_at.clear();
+    h->p2p_free_at.clear();
+    h->p2p = false;
+    if (h->graph_exec) {
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+}
+
+// the halo-slot buffers of a handle: modal the face traces, SBP the three state buffers
+int p2p_buffers(swedg_handle h, double** b) {
+    if (h->scheme == SWEDG_SCHEME_SBP) {
+        b[0] = h->u;
+        b[1] = h->u_alt;
+        b[2] = h->u_alt2;
+        return 3;
+    }
+    b[0] = h->trace;
+    return 1;
+}
 
 // Pack the cut faces (halo.cuh) on stream st: modal from the trace buffer, SBP from
 // the stage's input state `sbp_in`.
@@ -521,8 +565,49 @@ double* halo_recv(swedg_handle h, double* sbp_state = nullptr) {
     return h->trace + (size_t)h->K * 3 * h->nf;
 }
 
+// Peer-memory exchange of one stage on the comm stream (swedg_set_p2p): wait until every
+// destination consumed the previous stage's halo (its "free" flag), store the cut-face
+// entries straight into the destinations' halo slots, raise their "ready" flags, then
+// wait for every source's data.  Flag values are the stage codes 1..5, so the captured
+// graph replays the same operations every step; the two handshakes keep the ranks within
+// one stage of each other, so an equality wait cannot miss its value.
+int halo_exchange_p2p(swedg_handle h, int stage, double* sbp_state) {
+    StreamMemOps& mo = stream_mem_ops();
+    const unsigned code = (unsigned)stage + 1u, prev = stage == 0 ? 5u : (unsigned)stage;
+    auto flag = [&](int i) { return reinterpret_cast<unsigned long long>(h->p2p_flags + i); };
+    for (int q : h->p2p_send_peers)
+        if (mo.wait32(h->comm, flag(kP2pMaxRanks + q), prev, kWaitEq) != 0)
+            return fail(h, SWEDG_ERR_CUDA, "peer halo: stream wait failed");
+    if (h->n_pack > 0) {
+        const bool sbp = h->scheme == SWEDG_SCHEME_SBP;
+        const double* base = sbp ? (sbp_state ? sbp_state : h->u) : h->trace;
+        const int b = !sbp || base == h->u ? 0 : (base == h->u_alt ? 1 : 2);
+        HaloPackP2PParams p{base, h->pack_src, h->p2p_rdst, h->p2p_rpeer, h->p2p_rbase[b], h->n_pack};
+        halo_pack_p2p_kernel<<<(unsigned)((h->n_pack + 255) / 256), 256, 0, h->comm>>>(p);
+        h->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("peer halo pack: ") + cudaGetErrorString(e));
+    }
+    for (unsigned long long a : h->p2p_ready_at)  // default write: fenced after the stores above
+        if (mo.write32(h->comm, a, code, 0) != 0) return fail(h, SWEDG_ERR_CUDA, "peer halo: stream write failed");
+    for (int r : h->p2p_recv_peers)
+        if (mo.wait32(h->comm, flag(r), code, kWaitEq) != 0) return fail(h, SWEDG_ERR_CUDA, "peer halo: stream wait failed");
+    return SWEDG_OK;
+}
+
+// After the stage's halo consumers were enqueued on `st`: tell every source rank its
+// destination slots here are free again.
+int halo_consumed(swedg_handle h, int stage, cudaStream_t st) {
+    if (!h->p2p) return SWEDG_OK;
+    StreamMemOps& mo = stream_mem_ops();
+    for (unsigned long long a : h->p2p_free_at)
+        if (mo.write32(st, a, (unsigned)stage + 1u, 0) != 0) return fail(h, SWEDG_ERR_CUDA, "peer halo: stream write failed");
+    return SWEDG_OK;
+}
+
 // One stage's exchange on the comm stream: pack, then NCCL send/recv or the caller's transport.
 int halo_exchange(swedg_handle h, int stage, double* sbp_state = nullptr) {
+    if (h->p2p) return halo_exchange_p2p(h, stage, sbp_state);
     if (halo_pack_on(h, h->comm, sbp_state)) return h->last_code;
     double* recv = halo_recv(h, sbp_state);
     if (h->nccl) {
@@ -575,10 +660,11 @@ int run_stage_halo(swedg_handle h, int s, const unsigned* ids, double dt, const 
             StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true, r.first, r.second};
             if (run_stage(h, ss) || hk->done((int)i)) return h->last_code;
         }
-        return SWEDG_OK;
+        return halo_consumed(h, s, h->stream);
     }
     StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
-    return run_stage(h, ss);
+    if (run_stage(h, ss)) return h->last_code;
+    return halo_consumed(h, s, h->stream);
 }
 
 int run_step_halo_sbp(swedg_handle h, const unsigned* ids, double dt);
@@ -612,6 +698,7 @@ int run_step_halo_sbp(swedg_handle h, const unsigned* ids, double dt) {
                 if (run_stage(h, sa)) return h->last_code;
             }
         }
+        if (halo_consumed(h, s, h->stream)) return h->last_code;
         if (!pair) {  // LSRK45 update once every element's du is known
             StageArgs su{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[s], true};
             if (run_stage(h, su)) return h->last_code;
@@ -1051,6 +1138,9 @@ int swedg_destroy(swedg_handle h) {
     if (!h) return SWEDG_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm) cudaStreamSynchronize(h->comm);
+    p2p_detach(h);
+    if (h->p2p_flags) cudaFree(h->p2p_flags);
     void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
                     h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->u_alt, h->u_alt2,
@@ -1540,7 +1630,8 @@ int swedg_set_halo(swedg_handle h, const swedg_halo_desc* d) {
         at = r.second;
     }
     if (at < h->K) inner.push_back({at, h->K});
-    // device buffers
+    // device buffers (a peer-memory attachment refers to the old layout)
+    p2p_detach(h);
     if (h->pack_src) cudaFree(h->pack_src);
     if (h->pack_dst) cudaFree(h->pack_dst);
     if (h->sendbuf) cudaFree(h->sendbuf);
@@ -1587,7 +1678,10 @@ int swedg_set_nccl_comm(swedg_handle h, void* comm) {
     if (!h) return SWEDG_ERR_INVALID;
     if (comm && !nccl_api().ok) return fail(h, SWEDG_ERR_UNSUPPORTED, nccl_api().error);
     h->nccl = comm;
-    if (comm) h->xfn = nullptr;
+    if (comm) {
+        h->xfn = nullptr;
+        h->p2p = false;
+    }
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
@@ -1599,7 +1693,10 @@ int swedg_set_exchange(swedg_handle h, swedg_exchange_fn fn, void* user) {
     if (!h) return SWEDG_ERR_INVALID;
     h->xfn = fn;
     h->xuser = user;
-    if (fn) h->nccl = nullptr;
+    if (fn) {
+        h->nccl = nullptr;
+        h->p2p = false;
+    }
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
@@ -1667,6 +1764,170 @@ int swedg_nccl_comm_destroy(void* comm) {
     NcclApi& api = nccl_api();
     if (!api.ok) return SWEDG_ERR_UNSUPPORTED;
     return api.CommDestroy(comm) == 0 ? SWEDG_OK : SWEDG_ERR_CUDA;
+}
+
+// ---- peer-memory transport ----------------------------------------------------
+static_assert(sizeof(P2pBlob) <= SWEDG_P2P_BLOB_BYTES, "P2pBlob exceeds SWEDG_P2P_BLOB_BYTES");
+
+
+int swedg_p2p_export(swedg_handle h, int rank, void* blob) {
+    if (!h || !blob || rank < 0 || rank >= kP2pMaxRanks) return SWEDG_ERR_INVALID;
+    if (!h->halo_set) return fail(h, SWEDG_ERR_INVALID, "swedg_p2p_export needs swedg_set_halo first");
+    if ((int)h->recv_peer.size() > kP2pMaxMsgs) return fail(h, SWEDG_ERR_UNSUPPORTED, "more halo messages than the peer descriptor holds");
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (h->comm) CUDA_TRY(h, cudaStreamSynchronize(h->comm));
+    const size_t nflag = 2 * (size_t)kP2pMaxRanks;
+    if (!h->p2p_flags) CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(&h->p2p_flags), nflag * sizeof(unsigned)));
+    // protocol start: no data from anyone yet, every destination slot free ("stage 5 consumed")
+    std::vector<unsigned> init(nflag, 0u);
+    for (int r = 0; r < kP2pMaxRanks; ++r) init[kP2pMaxRanks + r] = 5u;
+    CUDA_TRY(h, cudaMemcpy(h->p2p_flags, init.data(), nflag * sizeof(unsigned), cudaMemcpyHostToDevice));
+    P2pBlob b;
+    std::memset(&b, 0, sizeof(b));
+    b.magic = kP2pMagic;
+    b.version = 1;
+    b.rank = rank;
+    b.pid = (int)getpid();
+    b.device = h->device;
+    double* bufs[3];
+    b.nbuf = p2p_buffers(h, bufs);
+    for (int i = 0; i < b.nbuf; ++i) {
+        b.buf_ptr[i] = reinterpret_cast<unsigned long long>(bufs[i]);
+        if (cudaIpcGetMemHandle(&b.buf_ipc[i], bufs[i]) != cudaSuccess) cudaGetLastError();  // same-process use only
+    }
+    b.halo_off = (long long)h->K * 3 * (h->scheme == SWEDG_SCHEME_SBP ? h->nq : h->nf);
+    b.flag_ptr = reinterpret_cast<unsigned long long>(h->p2p_flags);
+    if (cudaIpcGetMemHandle(&b.flag_ipc, h->p2p_flags) != cudaSuccess) cudaGetLastError();
+    b.n_recv = (int)h->recv_peer.size();
+    for (int m = 0; m < b.n_recv; ++m) {
+        b.recv_peer[m] = h->recv_peer[m];
+        b.recv_off[m] = (long long)h->recv_off[m];
+        b.recv_len[m] = (long long)h->recv_len[m];
+    }
+    std::memset(blob, 0, SWEDG_P2P_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof(b));
+    h->p2p_rank = rank;
+    return SWEDG_OK;
+}
+
+int swedg_set_p2p(swedg_handle h, int rank, int nranks, const void* blobs) {
+    if (!h) return SWEDG_ERR_INVALID;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    p2p_detach(h);
+    if (!blobs) return SWEDG_OK;
+    if (!h->halo_set) return fail(h, SWEDG_ERR_INVALID, "swedg_set_p2p needs swedg_set_halo first");
+    if (!h->p2p_flags || h->p2p_rank != rank)
+        return fail(h, SWEDG_ERR_INVALID, "swedg_set_p2p needs this rank's swedg_p2p_export first");
+    if (nranks < 1 || nranks > kP2pMaxRanks || rank < 0 || rank >= nranks) return fail(h, SWEDG_ERR_INVALID, "bad rank / nranks");
+    if (!stream_mem_ops().ok) return fail(h, SWEDG_ERR_UNSUPPORTED, "stream memory operations unavailable");
+    std::vector<P2pBlob> B((size_t)nranks);
+    for (int r = 0; r < nranks; ++r) {
+        std::memcpy(&B[r], static_cast<const char*>(blobs) + (size_t)r * SWEDG_P2P_BLOB_BYTES, sizeof(P2pBlob));
+        if (B[r].magic != kP2pMagic || B[r].version != 1 || B[r].rank != r)
+            return fail(h, SWEDG_ERR_INVALID, "peer descriptor " + std::to_string(r) + " is not a swedg_p2p_export of rank " +
+                                                  std::to_string(r));
+    }
+    double* own[3];
+    const int nbuf = p2p_buffers(h, own);
+    const int me = (int)getpid();
+    // map a peer's allocation: the pointer itself in this process, an IPC mapping otherwise
+    auto map = [&](const P2pBlob& q, const cudaIpcMemHandle_t& ipc, unsigned long long ptr, void** out) -> int {
+        if (q.pid == me) {
+            if (q.device != h->device) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(q.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(h, SWEDG_ERR_UNSUPPORTED, std::string("peer access: ") + cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+            *out = reinterpret_cast<void*>(ptr);
+            return SWEDG_OK;
+        }
+        cudaError_t e = cudaIpcOpenMemHandle(out, ipc, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+            return fail(h, SWEDG_ERR_UNSUPPORTED, std::string("cudaIpcOpenMemHandle (rank ") + std::to_string(q.rank) +
+                                                      "): " + cudaGetErrorString(e));
+        h->p2p_opened.push_back(*out);
+        return SWEDG_OK;
+    };
+    std::vector<void*> flags_of((size_t)nranks, nullptr);
+    auto peer_flags = [&](int q) -> unsigned* {
+        if (!flags_of[q] && map(B[q], B[q].flag_ipc, B[q].flag_ptr, &flags_of[q])) return nullptr;
+        return static_cast<unsigned*>(flags_of[q]);
+    };
+    std::vector<int> sp, rp;
+    for (int q : h->send_peer)
+        if (std::find(sp.begin(), sp.end(), q) == sp.end()) sp.push_back(q);
+    for (int q : h->recv_peer)
+        if (std::find(rp.begin(), rp.end(), q) == rp.end()) rp.push_back(q);
+    for (int q : sp) if (q < 0 || q >= nranks) return fail(h, SWEDG_ERR_INVALID, "halo peer outside nranks");
+    for (int q : rp) if (q < 0 || q >= nranks) return fail(h, SWEDG_ERR_INVALID, "halo peer outside nranks");
+    std::vector<std::vector<double*>> rbase((size_t)nbuf, std::vector<double*>(sp.size(), nullptr));
+    std::vector<unsigned long long> ready_at, free_at;
+    for (size_t i = 0; i < sp.size(); ++i) {
+        const P2pBlob& q = B[sp[i]];
+        if (q.nbuf != nbuf) return fail(h, SWEDG_ERR_INVALID, "peer descriptor of another scheme");
+        for (int bi = 0; bi < nbuf; ++bi) {
+            void* p = nullptr;
+            if (map(q, q.buf_ipc[bi], q.buf_ptr[bi], &p)) return h->last_code;
+            rbase[bi][i] = static_cast<double*>(p) + q.halo_off;
+        }
+        unsigned* f = peer_flags(sp[i]);
+        if (!f) return h->last_code;
+        ready_at.push_back(reinterpret_cast<unsigned long long>(f + rank));
+    }
+    for (int r : rp) {
+        unsigned* f = peer_flags(r);
+        if (!f) return h->last_code;
+        free_at.push_back(reinterpret_cast<unsigned long long>(f + kP2pMaxRanks + rank));
+    }
+    // message pairing: the k-th send to q fills q's k-th receive from this rank
+    std::vector<long long> moff(h->send_peer.size());
+    std::vector<int> mpeer(h->send_peer.size());
+    for (size_t m = 0; m < h->send_peer.size(); ++m) {
+        const int q = h->send_peer[m];
+        int k = 0;
+        for (size_t j = 0; j < m; ++j) k += h->send_peer[j] == q;
+        const P2pBlob& Q = B[q];
+        int found = -1;
+        for (int j = 0, c = 0; j < Q.n_recv; ++j)
+            if (Q.recv_peer[j] == rank && c++ == k) {
+                found = j;
+                break;
+            }
+        if (found < 0 || Q.recv_len[found] != (long long)h->send_len[m])
+            return fail(h, SWEDG_ERR_INVALID, "halo maps of rank " + std::to_string(rank) + " and rank " + std::to_string(q) +
+                                                  " disagree");
+        moff[m] = Q.recv_off[found];
+        mpeer[m] = (int)(std::find(sp.begin(), sp.end(), q) - sp.begin());
+    }
+    const size_t npk = (size_t)h->n_pack;
+    std::vector<long long> dst(npk), rdst(npk);
+    std::vector<int> rpeer(npk);
+    if (npk) CUDA_TRY(h, cudaMemcpy(dst.data(), h->pack_dst, npk * sizeof(long long), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < npk; ++i) {
+        size_t m = 0;
+        while (m + 1 < h->send_off.size() && (size_t)dst[i] >= h->send_off[m + 1]) ++m;
+        rdst[i] = moff[m] + (dst[i] - (long long)h->send_off[m]);
+        rpeer[i] = mpeer[m];
+    }
+    if (dalloc(h, &h->p2p_rdst, std::max<size_t>(npk, 1)) || dalloc(h, &h->p2p_rpeer, std::max<size_t>(npk, 1)))
+        return h->last_code;
+    if (npk && (upload(h, h->p2p_rdst, rdst.data(), npk) || upload(h, h->p2p_rpeer, rpeer.data(), npk))) return h->last_code;
+    for (int bi = 0; bi < nbuf; ++bi) {
+        if (dalloc(h, &h->p2p_rbase[bi], std::max<size_t>(sp.size(), 1))) return h->last_code;
+        if (!sp.empty() && upload(h, h->p2p_rbase[bi], rbase[bi].data(), sp.size())) return h->last_code;
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    h->p2p_send_peers = sp;
+    h->p2p_recv_peers = rp;
+    h->p2p_ready_at = ready_at;
+    h->p2p_free_at = free_at;
+    h->p2p = true;
+    h->nccl = nullptr;
+    h->xfn = nullptr;
+    return SWEDG_OK;
 }
 
 int swedg_check(swedg_handle h) {

@@ -13,9 +13,13 @@ pseudo-element, the layout of the receiver's halo slots (no unpack step).
 
 Transports (all drive the same native stage schedule, swedg_capi.cu run_step_halo:
 boundary volume -> pack -> exchange on a comm stream || interior volume -> interface):
+  * peer   `attach_p2p`: the pack kernel stores the cut-face traces straight into the
+             peers' halo slots over NVLink peer memory (IPC-mapped), ordered by stream-
+             written/-waited flags in the ranks' memory, inside the captured step graph
+             (swedg_set_p2p) — the one-node production path (bench.py --gpus N).
   * NCCL   `attach_nccl`: a library-owned communicator (swedg_nccl_comm_init; the
              unique id travels over torch.distributed), ncclSend/ncclRecv inside the
-             captured step graph — the production path (bench.py --gpus N).
+             captured step graph (bench.py --transport nccl).
   * gloo   `attach_gloo`: a host-staged exchange callback (functional check of the
              multi-rank orchestration with several ranks sharing one GPU).
   * local  `LocalExchange`: P handles in one process on one GPU, one host thread per
@@ -97,6 +101,26 @@ def attach_nccl(h, halo: dict, world: int, rank: int, device: int, group=None) -
     comm = capi.nccl_comm_init(world, bytes(t.cpu().tolist()), rank, device)
     h.set_nccl_comm(comm)
     return comm
+
+
+def attach_p2p(h, rank: int, world: int, group=None) -> None:
+    """Peer-memory transport for handle h (ranks of one node): every rank's descriptor
+    (swedg_p2p_export: IPC handles of its halo slots and flags) gathered over
+    torch.distributed, then swedg_set_p2p.  The exchange itself never touches the host."""
+    import torch.distributed as dist
+
+    blob = h.p2p_export(rank)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, blob, group=group)
+    h.set_p2p(rank, blobs)
+
+
+def attach_p2p_local(handles) -> None:
+    """Peer-memory transport between P handles of this process (logical partitions, rank =
+    position in the list); they exchange through each other's buffers directly."""
+    blobs = [h.p2p_export(r) for r, h in enumerate(handles)]
+    for r, h in enumerate(handles):
+        h.set_p2p(r, blobs)
 
 
 def attach_gloo(h, halo: dict, nf: int, group=None) -> None:

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_create_error_without_gpu():
     lib = capi.lib()
-    assert lib.swedg_abi_version() == capi.ABI_VERSION == 4
+    assert lib.swedg_abi_version() == capi.ABI_VERSION == 5
     # with no device, creation fails loudly (no CPU fallback)
     import torch
 

@@ -347,3 +347,111 @@ def test_multirank_run_loop_invariants_equal_global(scheme):
     np.testing.assert_array_equal(s, sg)
     for r, h in enumerate(hs):
         np.testing.assert_array_equal(h.get_state()[0], ug[owned_slice("strong", P, r)])
+
+
+# ---------------------------------------------------------------- peer-memory transport
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("scheme,N,mode", [(0, 3, "fast"), (0, 4, "fast"), (0, 4, "parity"), (1, 4, "fast"),
+                                           (1, 4, "parity")])
+def test_p2p_self_exchange_single_rank(scheme, N, mode):
+    """Peer-memory transport on one rank whose halos are its own periodic cut (strong,
+    P = 1): the pack kernel stores into its own halo slots and the stream flag protocol
+    runs against itself.  3 graph-replayed steps (flag waits/writes are graph nodes) + 1
+    individual step == the global steps, bitwise."""
+    from paper_2005_02516_b200.partition import attach_p2p_local
+
+    dt = 1e-3
+    m = capi.MODE_FAST if mode == "fast" else capi.MODE_PARITY
+    g = case("strong", 1, -1, N=N, scheme=scheme)
+    ug, tg = _global_steps(g, dt, 4, N, m)
+    c = case("strong", 1, 0, N=N, scheme=scheme)
+    h = c.handle(mode=m)
+    h.set_state(c.u0())
+    attach_p2p_local([h])
+    h.step(dt, 3)
+    h.step(dt, 1)
+    u, _, t = h.get_state()
+    np.testing.assert_array_equal(u, ug)
+    assert t == tg
+
+
+def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
+    """One rank per process (the production layout; here every process on device 0): halo
+    slots and flags of the peers mapped through CUDA IPC, descriptors over gloo."""
+    import torch.distributed as dist
+
+    from paper_2005_02516_b200.partition import attach_p2p
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        torch.cuda.set_device(0)
+        c = case(scaling, P, rank, N=4, scheme=scheme)
+        h = c.handle(mode=capi.MODE_FAST if mode == "fast" else capi.MODE_PARITY)
+        u0 = np.ascontiguousarray(c.u0())
+        h.set_state(u0)
+        attach_p2p(h, rank, P)
+        dist.barrier()
+        out = {}
+        if job == "steps":
+            h.step(1e-3, 3)  # captured step graph, replayed
+            h.step(1e-3, 1)  # individual launches
+            out["u"] = h.get_state()[0]
+        elif job == "host":
+            h.step_host(u0, 1e-3, 3, 4)  # range-chunked host-state steps
+            out["u"] = u0
+        else:  # run loop with invariant sampling: raw exact accumulators for the merge
+            series, n = h.run(dt, 8 * dt, 4)  # the global mesh's dt
+            out["raw"] = h.read_invariants_raw(len(series))
+            out["n"] = (len(series), n)
+            out["u"] = h.get_state()[0]
+        dist.barrier()  # no rank unmaps its peers' buffers before their last stores
+        h.close()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("scaling,P,scheme,mode,job", [
+    ("strong", 2, 0, "fast", "steps"), ("strong", 3, 0, "fast", "steps"), ("weak", 2, 0, "fast", "steps"),
+    ("strong", 3, 0, "parity", "steps"), ("strong", 2, 1, "fast", "steps"), ("strong", 3, 1, "fast", "steps"),
+    ("strong", 3, 1, "parity", "steps"), ("strong", 3, 0, "fast", "host"), ("strong", 3, 0, "fast", "run"),
+    ("strong", 3, 1, "fast", "run")])
+def test_p2p_processes_equal_global_bitwise(scaling, P, scheme, mode, job):
+    """Peer-memory transport with one rank per process (CUDA IPC): each rank's pack kernel
+    stores its cut faces straight into the peers' halo slots, the ranks' streams order the
+    stages through flags in each other's memory (no host sync).  Graph-replayed and
+    individual steps, host-state steps and the run loop (raw invariants merged) all equal
+    the single-rank results bit for bit."""
+    import torch.multiprocessing as mp
+
+    m = capi.MODE_FAST if mode == "fast" else capi.MODE_PARITY
+    g = case(scaling, P, -1, N=4, scheme=scheme)
+    hg = g.handle(mode=m)
+    hg.set_state(g.u0())
+    if job == "run":
+        sg, ng = hg.run(g.dt, 8 * g.dt, sample_every=4)
+    else:
+        hg.step(1e-3, 3 if job == "host" else 4)
+    ug = hg.get_state()[0]
+    hg.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_rank_main, args=(r, P, scaling, scheme, mode, job, g.dt, port, q))
+             for r in range(P)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(P))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(P):
+        np.testing.assert_array_equal(got[r]["u"], ug[owned_slice(scaling, P, r)])
+    if job == "run":
+        n = got[0]["n"][0]
+        assert got[0]["n"] == (len(sg), ng)
+        np.testing.assert_array_equal(capi.diag_from_raw([got[r]["raw"] for r in range(P)], n), sg)
