@@ -1,8 +1,9 @@
 #!/usr/bin/env python3
 """Multi-rank code path on one GPU at C4 size: a one-rank strong partition of the
-K1D=1024 mesh (halos = its own periodic cut) with a one-rank NCCL communicator —
-device-resident steps (captured graph with the NCCL exchange) and host-state steps
-(range-chunked copies), ms per step, against the unpartitioned handle."""
+K1D=1024 mesh (halos = its own periodic cut) with a one-rank NCCL communicator or the
+peer-memory transport against itself — device-resident steps (captured graph with the
+exchange) and host-state steps (range-chunked copies), ms per step, against the
+unpartitioned handle."""
 import os
 import sys
 
@@ -25,13 +26,17 @@ def timed(st, fn, n):
     return e0.elapsed_time(e1) / n
 
 
-for label, kw in (("unpartitioned", {}), ("1-rank strip + NCCL self exchange", dict(strips=1, strip=0, scaling="strong"))):
+strip = dict(strips=1, strip=0, scaling="strong")
+for label, kw, tr in (("unpartitioned", {}, None), ("1-rank strip + NCCL self exchange", strip, "nccl"),
+                      ("1-rank strip + peer-memory self exchange", strip, "p2p")):
     c = capi.Case("smooth", N=4, nx=k1d, warp=0.1, seed=23, **kw)
     h = c.handle(diagnostics=False)
     comm = None
-    if kw:
+    if tr == "nccl":
         comm = capi.nccl_comm_init(1, capi.nccl_unique_id(), 0, 0)
         h.set_nccl_comm(comm)
+    elif tr == "p2p":
+        h.set_p2p(0, [h.p2p_export(0)])
     st = torch.cuda.Stream()
     h.set_stream(st.cuda_stream)
     u0 = c.u0()
