@@ -515,8 +515,14 @@ bool sbp_pair_path(swedg_handle h) {
 bool halo_active(swedg_handle h) { return h->halo_set && (h->nccl || h->xfn || h->p2p); }
 
 void p2p_detach(swedg_handle h) {
+    if (h->comm) cudaStreamSynchronize(h->comm);  // no pack kernel still reads the maps below
+    if (h->stream) cudaStreamSynchronize(h->stream);
     for (void* p : h->p2p_opened) cudaIpcCloseMemHandle(p);
     h->p2p_opened.clear();
+    const size_t npk = std::max<size_t>((size_t)h->n_pack, 1), npeer = std::max<size_t>(h->p2p_send_peers.size(), 1);
+    if (h->p2p_rdst) h->dev_bytes -= npk * (sizeof(long long) + sizeof(int));
+    for (double** b : h->p2p_rbase)
+        if (b) h->dev_bytes -= npeer * sizeof(double*);
     for (void* p : {(void*)h->p2p_rdst, (void*)h->p2p_rpeer, (void*)h->p2p_rbase[0], (void*)h->p2p_rbase[1],
                     (void*)h->p2p_rbase[2]})
         if (p) cudaFree(p);
