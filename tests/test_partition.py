@@ -455,3 +455,26 @@ def test_p2p_processes_equal_global_bitwise(scaling, P, scheme, mode, job):
         n = got[0]["n"][0]
         assert got[0]["n"] == (len(sg), ng)
         np.testing.assert_array_equal(capi.diag_from_raw([got[r]["raw"] for r in range(P)], n), sg)
+
+
+@pytest.mark.gpu
+def test_p2p_attach_errors_are_loud():
+    """swedg_set_p2p refuses a rank that did not export its descriptor, descriptors in the
+    wrong rank order and halo maps that disagree; a detached handle steps again only with
+    a transport."""
+    c0, c1 = case("strong", 2, 0, N=4), case("strong", 2, 1, N=4)
+    h0, h1 = c0.handle(mode=capi.MODE_FAST), c1.handle(mode=capi.MODE_FAST)
+    b1 = h1.p2p_export(1)
+    with pytest.raises(capi.InvalidArgument, match="export"):
+        h0.set_p2p(0, [b1, b1])  # rank 0 never exported
+    b0 = h0.p2p_export(0)
+    with pytest.raises(capi.InvalidArgument, match="not a swedg_p2p_export of rank 0"):
+        h0.set_p2p(0, [b1, b0])
+    g = case("strong", 3, 1, N=4).handle(mode=capi.MODE_FAST)  # a 3-strip rank: other message sizes
+    with pytest.raises(capi.InvalidArgument, match="disagree"):
+        h0.set_p2p(0, [b0, g.p2p_export(1)])
+    h0.set_p2p(0, [b0, b1])
+    h0.set_p2p(0, None)
+    h0.set_state(c0.u0())
+    with pytest.raises(capi.InvalidArgument):
+        h0.step(1e-3, 1)
