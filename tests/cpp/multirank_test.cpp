@@ -12,6 +12,9 @@
 //  2. One rank whose halo is its own periodic cut, with a one-rank NCCL communicator
 //     (ncclSend/ncclRecv to itself inside the captured step graph): bitwise equal to
 //     the unpartitioned run.
+//  3. The same rank with the peer-memory transport against itself (swedg_p2p_export +
+//     swedg_set_p2p: pack-and-store into its halo slots, stream-ordered flags, graph
+//     replay): bitwise equal to the unpartitioned run.
 // Exit code = number of failed checks; one PASS/FAIL line per check.
 #include <cuda_runtime.h>
 
@@ -256,6 +259,37 @@ static void nccl_self(int scheme, int N) {
     swedg_nccl_comm_destroy(comm);
 }
 
+static void p2p_self(int scheme, int N) {
+    Case global(config(N, 8, 9, 1, -1, scheme));
+    Case strip(config(N, 8, 9, 1, 0, scheme));
+    auto gops = make_ops(global);
+    auto sops = make_ops(strip);
+    int Np, stride;
+    sizes(global, &Np, &stride);
+    const double dt = swedg_case_dt(global.c);
+    auto ug = run_steps(gops.handle(), global.u0(), (size_t)global.K() * 3 * Np, dt, 4);
+    swedg_halo_desc hd;
+    swedg_case_fill_halo(strip.c, &hd);
+    swedg_b200::set_halo(sops, hd);
+    std::vector<char> blob(SWEDG_P2P_BLOB_BYTES);
+    if (swedg_p2p_export(sops.handle(), 0, blob.data()) != SWEDG_OK ||
+        swedg_set_p2p(sops.handle(), 0, 1, blob.data()) != SWEDG_OK) {
+        char msg[256] = {0};
+        int code = 0;
+        swedg_last_error(sops.handle(), &code, nullptr, nullptr, msg, sizeof(msg));
+        check(false, tag(scheme, N, 1) + " peer-memory attach: " + msg);
+        return;
+    }
+    std::vector<double> u;
+    try {
+        u = run_steps(sops.handle(), strip.u0(), (size_t)strip.K() * 3 * Np, dt, 4);  // graph replay
+    } catch (const std::exception& e) {
+        std::printf("%s\n", e.what());
+    }
+    check(u.size() == ug.size() && std::memcmp(u.data(), ug.data(), u.size() * 8) == 0,
+          tag(scheme, N, 1) + " peer-memory self exchange across the periodic cut == global, bitwise");
+}
+
 int main(int argc, char** argv) {
     std::setvbuf(stdout, nullptr, _IOLBF, 0);
     // multirank_test [--no-nccl | --nccl-only N...]
@@ -268,6 +302,8 @@ int main(int argc, char** argv) {
             for (int sc : schemes)
                 for (int N : {3, 4})
                     for (int P : {1, 2, 3}) logical_partitions(sc, N, P);
+            for (int sc : schemes)
+                for (int N : {3, 4}) p2p_self(sc, N);
             if (mode != "--no-nccl")
                 for (int sc : schemes)
                     for (int N : {3, 4}) nccl_self(sc, N);

@@ -1,5 +1,6 @@
 """The multi-rank path from C++ through the C ABI (tests/cpp/multirank_test.cpp):
-logical partitions with an exchange callback, and a one-rank NCCL communicator."""
+logical partitions with an exchange callback, and one rank exchanging across its own periodic
+cut through the peer-memory transport and through a one-rank NCCL communicator."""
 import os
 import subprocess
 
