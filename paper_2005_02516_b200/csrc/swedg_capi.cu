@@ -142,6 +142,7 @@ struct swedg_handle_s {
     void* xuser = nullptr;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
+    cudaEvent_t ev_cons = nullptr;  // wavefront host stepping: the stage's halo slots were read
     std::vector<int> fidx_host;  // SBP face_index (halo pack: face node -> volume node)
     // peer-memory transport (swedg_p2p_export / swedg_set_p2p, halo.cuh)
     bool p2p = false;
@@ -1168,6 +1169,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->comm) cudaStreamDestroy(h->comm);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+    if (h->ev_cons) cudaEventDestroy(h->ev_cons);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return SWEDG_OK;
@@ -2278,7 +2280,7 @@ bool wave_adjacent(swedg_handle h, int C) {
     for (long e = 0; e < h->K && ok; ++e)
         for (int f = 0; f < 3; ++f) {
             const int nb = nbr[e * 3 + f];
-            if (nb < 0) continue;
+            if (nb < 0 || nb >= h->K) continue;  // wall, or a halo slot (multi-rank: the exchange orders it)
             const int d = ((chunk[nb] - chunk[e]) % C + C) % C;
             if (!(d == 0 || d == 1 || d == C - 1)) ok = false;
         }
@@ -2298,15 +2300,50 @@ bool wave_adjacent(swedg_handle h, int C) {
 // Copies: H2D(n, c) waits for D2H(n-1, c) (host round trip); the stage-0 volume of
 // chunk c waits for H2D(n, c); D2H(n, c) waits for the step's last interface kernel
 // on chunk c.
-int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, int C) {
-    const size_t per = (size_t)3 * h->Np;
-    auto lo = [&](int c) { return (int)((long)h->K * c / C); };
+// Multi-rank (a halo map with a transport): the chunks owning sent faces (the strip's
+// first and last rows: ring positions bmin..bmax) gate the stage's exchange — it is
+// enqueued on the comm stream right after volume(g, bmax), the interface kernels wait for
+// it from position bmin on (bmin + 3 > bmax keeps that after the exchange in the tick
+// order), and after interface(g, bmax) the halo slots are released (peer memory: the
+// sources' "free" flags; NCCL / callback: the next exchange waits for that point).
+std::vector<int> wave_ring(int C) {
     std::vector<int> A;
     A.push_back(0);
     for (int k = 1; (int)A.size() < C; ++k) {
         A.push_back(k);
         if ((int)A.size() < C) A.push_back(C - k);
     }
+    return A;
+}
+
+// ring positions [bmin, bmax] of the chunks owning sent faces; false if the wavefront
+// cannot order the exchange (boundary chunks too far apart in the ring)
+bool wave_halo_positions(swedg_handle h, int C, int* bmin, int* bmax) {
+    const std::vector<int> A = wave_ring(C);
+    std::vector<int> pos(C);
+    for (int p = 0; p < C; ++p) pos[A[p]] = p;
+    *bmin = C;
+    *bmax = -1;
+    for (const auto& r : h->bnd_ranges)
+        for (int c = 0; c < C; ++c) {
+            const long a = (long)h->K * c / C, b = (long)h->K * (c + 1) / C;
+            if (a < r.second && r.first < b) {
+                *bmin = std::min(*bmin, pos[c]);
+                *bmax = std::max(*bmax, pos[c]);
+            }
+        }
+    return *bmax < 0 || *bmin + 3 > *bmax;
+}
+
+int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, int C) {
+    const size_t per = (size_t)3 * h->Np;
+    auto lo = [&](int c) { return (int)((long)h->K * c / C); };
+    const std::vector<int> A = wave_ring(C);
+    const bool halo = halo_active(h);
+    int bmin = C, bmax = -1;
+    if (halo && !wave_halo_positions(h, C, &bmin, &bmax))
+        return fail(h, SWEDG_ERR_INVALID, "wavefront: boundary chunks not orderable");
+    if (halo && !h->ev_cons) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_cons, cudaEventDisableTiming));
     while ((int)h->ev_s4.size() < C) {
         cudaEvent_t e;
         CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -2344,13 +2381,25 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
                 StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
                              lo(c), lo(c + 1)};
                 if (run_stage(h, sa)) return h->last_code;
+                if (halo && pv == bmax) {  // every sent face's trace of stage g is written: exchange
+                    if (g > 0 && !h->p2p) CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_cons, 0));
+                    CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));
+                    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
+                    if (halo_exchange(h, s)) return h->last_code;
+                    CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+                }
             }
             const int ps = tau - t0(g) - 3;  // interface(g, ps)
             if (ps >= 0 && ps < C) {
                 const int c = A[ps];
+                if (halo && ps == bmin) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
                 StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
                              lo(c), lo(c + 1)};
                 if (run_stage(h, ss)) return h->last_code;
+                if (halo && ps == bmax) {  // the stage's halo slots are consumed
+                    if (halo_consumed(h, s, h->stream)) return h->last_code;
+                    if (!h->p2p) CUDA_TRY(h, cudaEventRecord(h->ev_cons, h->stream));
+                }
                 if (s == 4) {  // chunk c finished step g / 5: copy it out, and back in for the next step
                     const size_t a = (size_t)lo(c) * per, e = (size_t)lo(c + 1) * per;
                     CUDA_TRY(h, cudaEventRecord(h->ev_s4[c], h->stream));
@@ -2461,8 +2510,27 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
     if (nsteps < 0) return fail(h, SWEDG_ERR_INVALID, "nsteps must be >= 0");
     cudaSetDevice(h->device);
     const size_t per = (size_t)3 * h->nstate();
-    if (h->scheme == SWEDG_SCHEME_HYBRIDIZED && halo_active(h) && nsteps > 0)
+    const bool halo = h->scheme == SWEDG_SCHEME_HYBRIDIZED && halo_active(h) && nsteps > 0;
+    if (halo) {  // multi-rank: the wavefront with the per-stage exchange, else range-chunked stages
+        const int C = std::max(1, std::min(nchunks > 0 ? nchunks : 16, std::min(64, h->K)));
+        int bmin, bmax;
+        if (!h->timers && C >= 3 && wave_adjacent(h, C) && wave_halo_positions(h, C, &bmin, &bmax)) {
+            if (!h->cp_in) {
+                CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_in, cudaStreamNonBlocking));
+                CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_out, cudaStreamNonBlocking));
+                CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_step, cudaEventDisableTiming));
+            }
+            while ((int)h->ev_in.size() < C) {
+                cudaEvent_t a, b;
+                CUDA_TRY(h, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+                CUDA_TRY(h, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+                h->ev_in.push_back(a);
+                h->ev_out.push_back(b);
+            }
+            return step_host_wavefront(h, u_host, dt, nsteps, C);
+        }
         return step_host_halo(h, u_host, dt, nsteps, nchunks > 0 ? nchunks : 16);
+    }
     if (h->scheme != SWEDG_SCHEME_HYBRIDIZED || h->n_halo > 0) {  // unchunked: copy, step, copy
         for (int n = 0; n < nsteps; ++n) {
             CUDA_TRY(h, cudaMemcpyAsync(h->u, u_host, per * h->K * 8, cudaMemcpyHostToDevice, h->stream));

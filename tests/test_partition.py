@@ -478,3 +478,33 @@ def test_p2p_attach_errors_are_loud():
     h0.set_state(c0.u0())
     with pytest.raises(capi.InvalidArgument):
         h0.step(1e-3, 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,C", [(1, 4), (2, 4), (3, 8)])
+def test_multirank_host_state_wavefront_equal_global(P, C):
+    """swedg_step_lsrk45_host on strip handles tall enough for the wavefront schedule (each
+    rank's first and last rows in the ring's first chunks): the per-stage exchange is
+    enqueued after the boundary chunks' volume kernels inside the wavefront, the boundary
+    interface kernels wait for it.  Bitwise the global device-resident steps; the launch
+    count shows the wavefront ran (C volume + C interface launches + 1 pack per stage)."""
+    ny, dt, nsteps = 16 * P, 1e-3, 3
+
+    def mk(r):
+        return capi.Case("smooth", N=4, nx=6, ny=ny, warp=0.1, strips=P, strip=r, scaling="strong", threads=1)
+
+    g = mk(-1)
+    ug, tg = _global_steps(g, dt, nsteps, 4)
+    cases = [mk(r) for r in range(P)]
+    hs = [c.handle(mode=capi.MODE_FAST) for c in cases]
+    us = [np.ascontiguousarray(c.u0()) for c in cases]
+    for h, u in zip(hs, us):
+        h.set_state(u)
+    l0 = [h.launches for h in hs]
+    LocalExchange(hs, [c.halo_desc() for c in cases], cases[0].nf).step_host(us, dt, nsteps, C)
+    row = 2 * 6
+    for r, (h, u) in enumerate(zip(hs, us)):
+        j0, j1 = ny * r // P, ny * (r + 1) // P
+        np.testing.assert_array_equal(u, ug[row * j0:row * j1])
+        assert h.launches - l0[r] == 5 * nsteps * (2 * C + 1)
+        assert h.get_state()[2] == tg
