@@ -590,6 +590,9 @@ def run_ours(args, rank, world, local):
         "setup_s": round(setup_s, 2),
         "device_bytes": h.device_bytes,
     }
+    if dist:  # every rank's streams drained before any rank unmaps (peer memory) or frees its buffers
+        torch.cuda.synchronize()
+        dist.barrier()
     h.close()
     if comm:
         capi.nccl_comm_destroy(comm)
