@@ -376,6 +376,13 @@ def test_p2p_self_exchange_single_rank(scheme, N, mode):
     assert t == tg
 
 
+def _p2p_case(scaling, P, r, scheme, job):
+    if job == "hostwave":
+        return capi.Case("smooth", N=4, nx=6, ny=16 * P, warp=0.1, strips=P, strip=r, scaling="strong", threads=1,
+                         scheme=scheme)
+    return case(scaling, P, r, N=4, scheme=scheme)
+
+
 def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
     """One rank per process (the production layout; here every process on device 0): halo
     slots and flags of the peers mapped through CUDA IPC, descriptors over gloo."""
@@ -387,7 +394,7 @@ def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=P)
     try:
         torch.cuda.set_device(0)
-        c = case(scaling, P, rank, N=4, scheme=scheme)
+        c = _p2p_case(scaling, P, rank, scheme, job)
         h = c.handle(mode=capi.MODE_FAST if mode == "fast" else capi.MODE_PARITY)
         u0 = np.ascontiguousarray(c.u0())
         h.set_state(u0)
@@ -401,6 +408,11 @@ def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
         elif job == "host":
             h.step_host(u0, 1e-3, 3, 4)  # range-chunked host-state steps
             out["u"] = u0
+        elif job == "hostwave":  # a strip tall enough for the host-state wavefront
+            l0 = h.launches
+            h.step_host(u0, 1e-3, 3, 4)
+            out["u"] = u0
+            out["wavefront"] = h.launches - l0 == 5 * 3 * (2 * 4 + 1)
         else:  # run loop with invariant sampling: raw exact accumulators for the merge
             series, n = h.run(dt, 8 * dt, 4)  # the global mesh's dt
             out["raw"] = h.read_invariants_raw(len(series))
@@ -418,8 +430,8 @@ def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
 @pytest.mark.parametrize("scaling,P,scheme,mode,job", [
     ("strong", 2, 0, "fast", "steps"), ("strong", 3, 0, "fast", "steps"), ("weak", 2, 0, "fast", "steps"),
     ("strong", 3, 0, "parity", "steps"), ("strong", 2, 1, "fast", "steps"), ("strong", 3, 1, "fast", "steps"),
-    ("strong", 3, 1, "parity", "steps"), ("strong", 3, 0, "fast", "host"), ("strong", 3, 0, "fast", "run"),
-    ("strong", 3, 1, "fast", "run")])
+    ("strong", 3, 1, "parity", "steps"), ("strong", 3, 0, "fast", "host"), ("strong", 3, 0, "fast", "hostwave"),
+    ("strong", 3, 0, "fast", "run"), ("strong", 3, 1, "fast", "run")])
 def test_p2p_processes_equal_global_bitwise(scaling, P, scheme, mode, job):
     """Peer-memory transport with one rank per process (CUDA IPC): each rank's pack kernel
     stores its cut faces straight into the peers' halo slots, the ranks' streams order the
@@ -429,13 +441,13 @@ def test_p2p_processes_equal_global_bitwise(scaling, P, scheme, mode, job):
     import torch.multiprocessing as mp
 
     m = capi.MODE_FAST if mode == "fast" else capi.MODE_PARITY
-    g = case(scaling, P, -1, N=4, scheme=scheme)
+    g = _p2p_case(scaling, P, -1, scheme, job)
     hg = g.handle(mode=m)
     hg.set_state(g.u0())
     if job == "run":
         sg, ng = hg.run(g.dt, 8 * g.dt, sample_every=4)
     else:
-        hg.step(1e-3, 3 if job == "host" else 4)
+        hg.step(1e-3, 3 if job.startswith("host") else 4)
     ug = hg.get_state()[0]
     hg.close()
     ctx = mp.get_context("spawn")
@@ -450,7 +462,12 @@ def test_p2p_processes_equal_global_bitwise(scaling, P, scheme, mode, job):
         p.join(timeout=120)
         assert p.exitcode == 0
     for r in range(P):
-        np.testing.assert_array_equal(got[r]["u"], ug[owned_slice(scaling, P, r)])
+        if job == "hostwave":
+            j0, j1 = 16 * P * r // P, 16 * P * (r + 1) // P
+            np.testing.assert_array_equal(got[r]["u"], ug[12 * j0:12 * j1])
+            assert got[r]["wavefront"]
+        else:
+            np.testing.assert_array_equal(got[r]["u"], ug[owned_slice(scaling, P, r)])
     if job == "run":
         n = got[0]["n"][0]
         assert got[0]["n"] == (len(sg), ng)
