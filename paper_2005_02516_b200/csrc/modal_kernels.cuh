@@ -50,6 +50,12 @@ struct ModalVolParams {
     unsigned stage_id;
     int early_exit;
     int k_base;         // global id of element 0 of this launch (chunked launches; error reports)
+    // segmented launch (N = 4 pair kernel, host-state wavefront): element ranges
+    // [seg_k0[s], seg_k1[s]) of different RK stages in one launch, pointers absolute; pair
+    // slots seg_pair0[s] .. seg_pair0[s+1] - 1 (pairs do not straddle ranges)
+    int nseg = 0, seg_pairs = 0;  // seg_pairs: total pair slots
+    int seg_k0[4], seg_k1[4], seg_pair0[4];
+    unsigned seg_stage[4];
 };
 
 template <int N>
@@ -339,6 +345,13 @@ struct ModalSurfParams {
     unsigned stage_id;
     int early_exit;
     int k_begin;          // first element of this launch (K = one past the last)
+    // segmented launch (host-state wavefront): element ranges [seg_k0[s], seg_k1[s]) of
+    // different RK stages, blocks seg_blk0[s] .. seg_blk0[s+1] - 1, with their own LSRK
+    // coefficients and stage ids
+    int nseg = 0;
+    int seg_k0[4], seg_k1[4], seg_blk0[4];
+    double seg_a[4], seg_b[4];
+    unsigned seg_stage[4];
 };
 
 template <int N>
@@ -353,7 +366,7 @@ struct SurfCfg {
 #ifndef SWEDG_SURF_MINB
 #define SWEDG_SURF_MINB 8
 #endif
-template <int N, bool P>
+template <int N, bool P, bool SEG = false>
 __global__ void __launch_bounds__(128, SWEDG_SURF_MINB)
 modal_surface_kernel(ModalSurfParams prm) {
     using D = ModalDims<N>;
@@ -370,8 +383,29 @@ modal_surface_kernel(ModalSurfParams prm) {
     const double* gVf = prm.ops + O::Vf;  // 1.8 KB, read through L1 by every warp
     const int tid = threadIdx.x;
     const int e = tid / L, s = tid % L;
-    const int k = prm.k_begin + blockIdx.x * E + e;  // elements [k_begin, K)
-    const bool act = k < prm.K;
+    // this block's element range, LSRK coefficients and stage id (SEG: its segment's)
+    int kbeg = prm.k_begin, kend = prm.K, blk = blockIdx.x;
+    double rk_a = prm.rk_a, rk_b = prm.rk_b;
+    unsigned sid = prm.stage_id;
+    if constexpr (SEG) {
+        kbeg = prm.seg_k0[0];
+        kend = prm.seg_k1[0];
+        rk_a = prm.seg_a[0];
+        rk_b = prm.seg_b[0];
+        sid = prm.seg_stage[0];
+#pragma unroll
+        for (int i = 1; i < 4; ++i)
+            if (i < prm.nseg && (int)blockIdx.x >= prm.seg_blk0[i]) {
+                kbeg = prm.seg_k0[i];
+                kend = prm.seg_k1[i];
+                rk_a = prm.seg_a[i];
+                rk_b = prm.seg_b[i];
+                sid = prm.seg_stage[i];
+                blk = blockIdx.x - prm.seg_blk0[i];
+            }
+    }
+    const int k = kbeg + blk * E + e;  // elements [kbeg, kend)
+    const bool act = k < kend;
     const double g = prm.g;
     static_assert(32 % L == 0, "an element's lanes must lie in one warp");
     if constexpr (!P) {  // packed M_h^{-1} of the warp's elements: one contiguous copy per warp,
@@ -379,7 +413,7 @@ modal_surface_kernel(ModalSurfParams prm) {
         // neither holds registers nor serialises load -> store; waited for before the M^-1 product
         constexpr int EW = 32 / L;  // elements per warp
         const int lane = tid & 31, ew0 = (tid >> 5) * EW;
-        const int k0 = prm.k_begin + blockIdx.x * E + ew0, ne = max(0, min(EW, prm.K - k0));
+        const int k0 = kbeg + blk * E + ew0, ne = max(0, min(EW, kend - k0));
         const double* src = prm.Mpk + (size_t)k0 * NPK;
         if (NPK % 2 == 0 && (reinterpret_cast<uintptr_t>(prm.Mpk) & 15u) == 0) {  // (N = 1, 4)
             for (int x = lane; x < ne * NPK / 2; x += 32) {
@@ -534,14 +568,14 @@ modal_surface_kernel(ModalSurfParams prm) {
             for (int c = 0; c < 3; ++c) du[c] = A::fma(mm, smod[e][c * Np + m], du[c]);
         }
         if (!(isfinite(du[0]) && isfinite(du[1]) && isfinite(du[2])))
-            record_error(prm.err, prm.stage_id, 1, k);
+            record_error(prm.err, sid, 1, k);
         const size_t o = (size_t)k * 3 * Np + s;
         if (prm.rk_mode) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const double r = A::fma(prm.rk_a, rr[c], A::mul(prm.dt, du[c]));
+                const double r = A::fma(rk_a, rr[c], A::mul(prm.dt, du[c]));
                 prm.res[o + c * Np] = r;
-                prm.u[o + c * Np] = A::fma(prm.rk_b, r, ur[c]);
+                prm.u[o + c * Np] = A::fma(rk_b, r, ur[c]);
             }
         } else {
 #pragma unroll

@@ -93,6 +93,29 @@ struct PairN4 {
     static constexpr size_t bytes() { return sizeof(double) * ((size_t)ops_len + (size_t)WARPS * per_warp) + 16; }
 };
 
+// Pair slot pr -> its first element kb, the end of its element range and its stage id:
+// [0, K) of the launch, or (SEG) the segment holding slot pr.
+template <bool SEG>
+__device__ __forceinline__ void pair_slot(const ModalVolParams& p, int pr, int& kb, int& kend, unsigned& sid) {
+    if constexpr (!SEG) {
+        kb = 2 * pr;
+        kend = p.K;
+        sid = p.stage_id;
+    } else {
+        kb = p.seg_k0[0] + 2 * pr;
+        kend = p.seg_k1[0];
+        sid = p.seg_stage[0];
+#pragma unroll
+        for (int i = 1; i < 4; ++i)
+            if (i < p.nseg && pr >= p.seg_pair0[i]) {
+                kb = p.seg_k0[i] + 2 * (pr - p.seg_pair0[i]);
+                kend = p.seg_k1[i];
+                sid = p.seg_stage[i];
+            }
+    }
+}
+
+template <bool SEG>
 __global__ void __launch_bounds__(PairN4::T, 1)
 modal_volume_pair_n4_kernel(ModalVolParams prm) {
     using W = PairN4;
@@ -190,7 +213,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
     }
 
     const double g = prm.g, ig = 1.0 / g, g2 = 2.0 * g;
-    const int npairs = (prm.K + 1) / 2;
+    const int npairs = SEG ? prm.seg_pairs : (prm.K + 1) / 2;
     const int gw = blockIdx.x * W::WARPS + warp, nw = gridDim.x * W::WARPS;
 
     const bool bulk_ok = ((reinterpret_cast<uintptr_t>(prm.gf) | reinterpret_cast<uintptr_t>(prm.bs) |
@@ -198,8 +221,10 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
     // the pair's u/gf/b: three bulk (TMA) copies of contiguous pair blocks by lane 0
     // (k0 even: every block is 16 B aligned), completion on the warp's mbarrier
     auto issue = [&](int pr) {
-        const int k0 = 2 * pr;
-        if (k0 + 1 < prm.K && bulk_ok) {
+        int k0, kend;
+        unsigned sid_;
+        pair_slot<SEG>(prm, pr, k0, kend, sid_);
+        if (k0 + 1 < kend && bulk_ok) {
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive_tx(mb, 8u * (90 + 320 + 80));
@@ -207,8 +232,8 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 bulk_g2s(stage + W::sG, prm.gf + (size_t)k0 * 4 * nh, 8u * 320, mb);
                 bulk_g2s(stage + W::sB, prm.bs + (size_t)k0 * nh, 8u * 80, mb);
             }
-        } else if (k0 < prm.K) {  // odd K (last element alone) or unaligned base pointers: plain loads
-            const int ne = k0 + 1 < prm.K ? 2 : 1;
+        } else if (k0 < kend) {  // odd K (last element alone) or unaligned base pointers: plain loads
+            const int ne = k0 + 1 < kend ? 2 : 1;
             for (int r = lane; r < 45 * ne; r += 32) stage[W::sU + r] = prm.u[(size_t)k0 * 45 + r];
             for (int r = lane; r < 160 * ne; r += 32) stage[W::sG + r] = prm.gf[(size_t)k0 * 160 + r];
             for (int r = lane; r < 40 * ne; r += 32) stage[W::sB + r] = prm.bs[(size_t)k0 * 40 + r];
@@ -220,8 +245,11 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
     if (gw < npairs) issue(gw);
     uint32_t phase = 0;
     for (int pr = gw; pr < npairs; pr += nw, phase ^= 1) {
-        const int k = 2 * pr + half;
-        const bool valid = k < prm.K;
+        int kb, kend;
+        unsigned sid;
+        pair_slot<SEG>(prm, pr, kb, kend, sid);
+        const int k = kb + half;
+        const bool valid = k < kend;
         // ---- park: staging -> work (u, b, g pairs), freeing the staging for the next pair
         {
             mbar_wait(mb, phase);
@@ -280,7 +308,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
             for (int q = 0; q < 2; ++q) {
                 const int i = q == 0 ? rA : rB;
                 if (i < nq) {
-                    if (valid && !(uq[q][0] > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
+                    if (valid && !(uq[q][0] > 0.0)) record_error(prm.err, sid, 0, prm.k_base + k);
                     const double inv = 1.0 / uq[q][0];
                     const double vx = uq[q][1] * inv, vy = uq[q][2] * inv;
                     work[W::wV + i] = g * (uq[q][0] + work[W::wBs + i]) - 0.5 * (vx * vx + vy * vy);
@@ -390,7 +418,7 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 r.g4 = d.y;
                 r.a0 = r.a1 = r.a2 = r.b1 = r.b2 = 0.0;
                 if (q < 2 || lp < 8) {
-                    if (valid && !(h > 0.0)) record_error(prm.err, prm.stage_id, 0, prm.k_base + k);
+                    if (valid && !(h > 0.0)) record_error(prm.err, sid, 0, prm.k_base + k);
                     reinterpret_cast<double2*>(work + W::wA)[row] = make_double2(r.U, r.V);
                     reinterpret_cast<double2*>(work + W::wB)[row] = make_double2(vt[q][1], vt[q][2]);
                     work[W::wH + row] = h;
@@ -552,8 +580,8 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int n = 2 * tig + q, e = n / 3;
-                const int ke = 2 * pr + e;
-                if (n < 6 && ke < prm.K) {
+                const int ke = kb + e;
+                if (n < 6 && ke < kend) {
                     double* out = prm.T1 + (size_t)ke * 3 * Np + (n % 3) * Np;
                     out[gid] = q ? d01 : d00;
                     if (8 + gid < Np) out[8 + gid] = q ? d11 : d10;

@@ -72,6 +72,7 @@ struct swedg_handle_s {
     double* u_alt = nullptr;  // SBP pair path: state buffers of the fused RK stages (u -> A -> B -> A -> B -> u)
     double* u_alt2 = nullptr;
     int diag_occ = 0;  // resident diag_kernel CTAs per SM (its staging size depends on the scheme)
+    bool merge_ticks = true;  // wavefront: one segmented volume launch per tick (SWEDG_WAVE_MERGE=0: per chunk)
     double* res = nullptr;   // LSRK register
     double* utmp = nullptr;  // host-API scratch state
     double* du = nullptr;    // host-API scratch rhs
@@ -300,6 +301,16 @@ void launch_pair(swedg_handle h, void (*kern)(ModalVolParams), const ModalVolPar
     launch_pdl(kern, std::max(grid, 1), Cfg::T, psm, h->stream, (h->pdl_mask & 1) != 0, vp);
 }
 
+// Volume kernels of several (stage, element range) pieces in one launch of the N = 4
+// FAST pair kernel (host-state wavefront: the pieces of one tick are independent).
+struct VolSeg {
+    int k0, k1;
+    unsigned stage_id;
+    double a = 0.0, b = 0.0;  // interface pieces: the stage's LSRK coefficients
+};
+int launch_volume_segments(swedg_handle h, const std::vector<VolSeg>& segs);
+int launch_surface_segments(swedg_handle h, const std::vector<VolSeg>& segs, double dt);
+
 // the SBP pair kernel bulk-copies (TMA) per-pair blocks: every source must be 16 B aligned
 // (true for the handle's own buffers; a caller's rhs_device pointer may not be)
 inline bool sbp_pair_aligned(const SbpParams& sp) {
@@ -357,7 +368,7 @@ int run_modal_stage(swedg_handle h, const StageArgs& sa) {
         if (h->mode == SWEDG_MODE_PARITY) {  // reference evaluation order, row per thread
             launch_vol(modal_volume_kernel<N, true>);
         } else if constexpr (N == 4) {  // pair kernel, operators in TMEM (modal_pair_n4.cuh)
-            launch_pair<PairN4>(h, modal_volume_pair_n4_kernel, vp);
+            launch_pair<PairN4>(h, modal_volume_pair_n4_kernel<false>, vp);
         } else if constexpr (N == 3) {  // modal_pair_n3.cuh
             launch_pair<PairN3>(h, modal_volume_pair_n3_kernel, vp);
         } else {  // N = 1, 2: two rows per thread (modal_fast.cuh)
@@ -735,6 +746,98 @@ int run_step(swedg_handle h, const unsigned* ids, double dt) {
     return SWEDG_OK;
 }
 
+int launch_volume_segments(swedg_handle h, const std::vector<VolSeg>& segs) {
+    ModalVolParams vp;
+    vp.K = h->K;
+    vp.g = h->g;
+    vp.ops = h->ops;
+    vp.u = h->u;
+    vp.gf = h->gf;
+    vp.bs = h->bs;
+    vp.src = h->src;
+    vp.trace = h->trace;
+    vp.accf = h->accf;
+    vp.T1 = h->T1;
+    vp.proj = nullptr;
+    vp.err = h->err;
+    vp.stage_id = segs[0].stage_id;
+    vp.early_exit = 1;
+    vp.k_base = 0;
+    vp.nseg = (int)segs.size();
+    int pairs = 0;
+    for (int i = 0; i < vp.nseg; ++i) {
+        vp.seg_k0[i] = segs[i].k0;
+        vp.seg_k1[i] = segs[i].k1;
+        vp.seg_stage[i] = segs[i].stage_id;
+        vp.seg_pair0[i] = pairs;
+        pairs += (segs[i].k1 - segs[i].k0 + 1) / 2;
+    }
+    vp.seg_pairs = pairs;
+    {
+        KTimer kt(h, 0);
+        auto kern = modal_volume_pair_n4_kernel<true>;
+        const size_t psm = PairN4::bytes();
+        const int occ = kernel_occupancy(reinterpret_cast<const void*>(kern), h->device, PairN4::T, psm);
+        const int grid = std::min((pairs + PairN4::WARPS - 1) / PairN4::WARPS, occ * h->nsm);
+        launch_pdl(kern, std::max(grid, 1), PairN4::T, psm, h->stream, (h->pdl_mask & 1) != 0, vp);
+    }
+    h->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
+// Interface/update kernels of several (stage, element range) pieces in one launch (N = 4
+// FAST, host-state wavefront).
+int launch_surface_segments(swedg_handle h, const std::vector<VolSeg>& segs, double dt) {
+    ModalSurfParams sp;
+    sp.K = h->K;
+    sp.g = h->g;
+    sp.lf = h->penalty == SWEDG_PENALTY_LF ? 1 : 0;
+    sp.ops = h->ops;
+    sp.trace = h->trace;
+    sp.accf = h->accf;
+    sp.T1 = h->T1;
+    sp.surf = h->surf;
+    sp.src = h->src;
+    sp.nbr = h->nbr;
+    sp.perm = h->perm;
+    sp.Minv = h->Minv;
+    sp.Mpk = h->Mpk;
+    sp.du = nullptr;
+    sp.u = h->u;
+    sp.res = h->res;
+    sp.rk_a = segs[0].a;
+    sp.rk_b = segs[0].b;
+    sp.dt = dt;
+    sp.rk_mode = 1;
+    sp.err = h->err;
+    sp.stage_id = segs[0].stage_id;
+    sp.early_exit = 1;
+    sp.k_begin = 0;
+    using SC = SurfCfg<4>;
+    sp.nseg = (int)segs.size();
+    int blocks = 0;
+    for (int i = 0; i < sp.nseg; ++i) {
+        sp.seg_k0[i] = segs[i].k0;
+        sp.seg_k1[i] = segs[i].k1;
+        sp.seg_a[i] = segs[i].a;
+        sp.seg_b[i] = segs[i].b;
+        sp.seg_stage[i] = segs[i].stage_id;
+        sp.seg_blk0[i] = blocks;
+        blocks += (segs[i].k1 - segs[i].k0 + SC::E - 1) / SC::E;
+    }
+    if (blocks <= 0) return SWEDG_OK;
+    {
+        KTimer kt(h, 1);
+        launch_pdl(modal_surface_kernel<4, false, true>, blocks, SC::T, 0, h->stream, (h->pdl_mask & 2) != 0, sp);
+    }
+    h->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, SWEDG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    return SWEDG_OK;
+}
+
 int run_stage(swedg_handle h, const StageArgs& sa) {
     if (h->scheme == SWEDG_SCHEME_SBP) {
         switch (h->N) {
@@ -993,6 +1096,7 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
     h->g = d->g;
     h->device = d->device;
     if (const char* v = std::getenv("SWEDG_PDL")) h->pdl_mask = std::atoi(v);
+    if (const char* v = std::getenv("SWEDG_WAVE_MERGE")) h->merge_ticks = std::atoi(v) != 0;
     cudaSetDevice(h->device);
     cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
     if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -2266,7 +2370,11 @@ int swedg_ratio_kernels(int device, int n, int nq, int K, const double* Q, const
 }
 
 namespace {
-// Element chunk c = [K c / C, K (c+1) / C).  The wavefront schedule needs every
+// first element of wavefront chunk c (c = C: K); even, so every pair of the segmented
+// volume launch starts on a 16 B-aligned state block
+int wave_lo(int K, int c, int C) { return c >= C ? K : (int)(((long)K * c / C) & ~1L); }
+
+// Element chunk c = [wave_lo(c), wave_lo(c + 1)).  The wavefront schedule needs every
 // neighbour of a chunk-c element in chunk c-1, c or c+1 (cyclically): true for the
 // row-ordered structured meshes of the native setup, checked once per chunk count.
 bool wave_adjacent(swedg_handle h, int C) {
@@ -2275,7 +2383,7 @@ bool wave_adjacent(swedg_handle h, int C) {
     if (cudaMemcpy(nbr.data(), h->nbr, nbr.size() * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return false;
     std::vector<int> chunk(h->K);
     for (int c = 0; c < C; ++c)
-        for (long e = (long)h->K * c / C; e < (long)h->K * (c + 1) / C; ++e) chunk[e] = c;
+        for (long e = wave_lo(h->K, c, C); e < wave_lo(h->K, c + 1, C); ++e) chunk[e] = c;
     bool ok = true;
     for (long e = 0; e < h->K && ok; ++e)
         for (int f = 0; f < 3; ++f) {
@@ -2326,7 +2434,7 @@ bool wave_halo_positions(swedg_handle h, int C, int* bmin, int* bmax) {
     *bmax = -1;
     for (const auto& r : h->bnd_ranges)
         for (int c = 0; c < C; ++c) {
-            const long a = (long)h->K * c / C, b = (long)h->K * (c + 1) / C;
+            const long a = wave_lo(h->K, c, C), b = wave_lo(h->K, c + 1, C);
             if (a < r.second && r.first < b) {
                 *bmin = std::min(*bmin, pos[c]);
                 *bmax = std::max(*bmax, pos[c]);
@@ -2337,7 +2445,7 @@ bool wave_halo_positions(swedg_handle h, int C, int* bmin, int* bmax) {
 
 int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, int C) {
     const size_t per = (size_t)3 * h->Np;
-    auto lo = [&](int c) { return (int)((long)h->K * c / C); };
+    auto lo = [&](int c) { return wave_lo(h->K, c, C); };
     const std::vector<int> A = wave_ring(C);
     const bool halo = halo_active(h);
     int bmin = C, bmax = -1;
@@ -2371,31 +2479,69 @@ int step_host_wavefront(swedg_handle h, double* u_host, double dt, int nsteps, i
         if (h2d(A[p])) return h->last_code;
     auto t0 = [](int g) { return 6 * g; };
     const int ticks = t0(G - 1) + C + 3;
+    // N = 4 FAST: the tick's volume pieces (independent: different chunks, and no piece
+    // reads what another writes) go out as one segmented launch of the pair kernel
+    const bool merge = h->N == 4 && h->mode == SWEDG_MODE_FAST && h->merge_ticks;
+    std::vector<VolSeg> segs;
+    std::vector<int> exch;
     for (int tau = 0; tau < ticks; ++tau) {
+        segs.clear();
+        exch.clear();
         for (int g = 0; g < G; ++g) {
             const int s = g % 5;
             const int pv = tau - t0(g);  // volume(g, pv)
             if (pv >= 0 && pv < C) {
                 const int c = A[pv];
                 if (s == 0) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
-                StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
-                             lo(c), lo(c + 1)};
-                if (run_stage(h, sa)) return h->last_code;
-                if (halo && pv == bmax) {  // every sent face's trace of stage g is written: exchange
-                    if (g > 0 && !h->p2p) CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_cons, 0));
-                    CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));
-                    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
-                    if (halo_exchange(h, s)) return h->last_code;
-                    CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+                if (merge) {
+                    segs.push_back({lo(c), lo(c + 1), ids[g]});
+                } else {
+                    StageArgs sa{h->u, 1, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
+                                 lo(c), lo(c + 1)};
+                    if (run_stage(h, sa)) return h->last_code;
                 }
+                if (halo && pv == bmax) exch.push_back(g);
             }
+        }
+        for (size_t i = 0; i < segs.size(); i += 4) {
+            const std::vector<VolSeg> part(segs.begin() + i, segs.begin() + std::min(segs.size(), i + 4));
+            if (launch_volume_segments(h, part)) return h->last_code;
+        }
+        for (int g : exch) {  // every sent face's trace of stage g is written: exchange
+            if (g > 0 && !h->p2p) CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_cons, 0));
+            CUDA_TRY(h, cudaEventRecord(h->ev_bnd, h->stream));
+            CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_bnd, 0));
+            if (halo_exchange(h, g % 5)) return h->last_code;
+            CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+        }
+        // the tick's interface pieces (independent as well): one segmented launch per <= 4
+        struct Piece {
+            int g, ps;
+        };
+        std::vector<Piece> pieces;
+        for (int g = 0; g < G; ++g) {
             const int ps = tau - t0(g) - 3;  // interface(g, ps)
-            if (ps >= 0 && ps < C) {
-                const int c = A[ps];
-                if (halo && ps == bmin) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+            if (ps >= 0 && ps < C) pieces.push_back({g, ps});
+        }
+        for (size_t i0 = 0; i0 < pieces.size(); i0 += merge ? 4 : 1) {
+            const size_t i1 = std::min(pieces.size(), i0 + (merge ? 4 : 1));
+            for (size_t i = i0; i < i1; ++i)
+                if (halo && pieces[i].ps == bmin) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+            if (merge) {
+                segs.clear();
+                for (size_t i = i0; i < i1; ++i) {
+                    const int g = pieces[i].g, s = g % 5, c = A[pieces[i].ps];
+                    segs.push_back({lo(c), lo(c + 1), ids[g], Lsrk45::a[s], Lsrk45::b[s]});
+                }
+                if (launch_surface_segments(h, segs, dt)) return h->last_code;
+            } else {
+                const int g = pieces[i0].g, s = g % 5, c = A[pieces[i0].ps];
                 StageArgs ss{h->u, 2, nullptr, true, Lsrk45::a[s], Lsrk45::b[s], dt, nullptr, ids[g], true,
                              lo(c), lo(c + 1)};
                 if (run_stage(h, ss)) return h->last_code;
+            }
+            for (size_t i = i0; i < i1; ++i) {
+                const int g = pieces[i].g, s = g % 5, ps = pieces[i].ps, c = A[ps];
                 if (halo && ps == bmax) {  // the stage's halo slots are consumed
                     if (halo_consumed(h, s, h->stream)) return h->last_code;
                     if (!h->p2p) CUDA_TRY(h, cudaEventRecord(h->ev_cons, h->stream));
@@ -2514,7 +2660,7 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
     if (halo) {  // multi-rank: the wavefront with the per-stage exchange, else range-chunked stages
         const int C = std::max(1, std::min(nchunks > 0 ? nchunks : 16, std::min(64, h->K)));
         int bmin, bmax;
-        if (!h->timers && C >= 3 && wave_adjacent(h, C) && wave_halo_positions(h, C, &bmin, &bmax)) {
+        if (!h->timers && C >= 3 && h->K >= 2 * C && wave_adjacent(h, C) && wave_halo_positions(h, C, &bmin, &bmax)) {
             if (!h->cp_in) {
                 CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_in, cudaStreamNonBlocking));
                 CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cp_out, cudaStreamNonBlocking));
@@ -2553,7 +2699,7 @@ int swedg_step_lsrk45_host(swedg_handle h, double* u_host, double dt, int nsteps
         h->ev_in.push_back(a);
         h->ev_out.push_back(b);
     }
-    if (nsteps > 0 && !h->timers && C >= 3 && wave_adjacent(h, C))
+    if (nsteps > 0 && !h->timers && C >= 3 && h->K >= 2 * C && wave_adjacent(h, C))
         return step_host_wavefront(h, u_host, dt, nsteps, C);
     auto lo = [&](int c) { return (int)((long)h->K * c / C); };
     // the copy streams start after everything already queued on the handle stream

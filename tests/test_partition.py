@@ -412,7 +412,7 @@ def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
             l0 = h.launches
             h.step_host(u0, 1e-3, 3, 4)
             out["u"] = u0
-            out["wavefront"] = h.launches - l0 == 5 * 3 * (2 * 4 + 1)
+            out["wavefront"] = h.launches - l0 == wave_launches(5 * 3, 4)
         else:  # run loop with invariant sampling: raw exact accumulators for the merge
             series, n = h.run(dt, 8 * dt, 4)  # the global mesh's dt
             out["raw"] = h.read_invariants_raw(len(series))
@@ -504,7 +504,8 @@ def test_multirank_host_state_wavefront_equal_global(P, C):
     rank's first and last rows in the ring's first chunks): the per-stage exchange is
     enqueued after the boundary chunks' volume kernels inside the wavefront, the boundary
     interface kernels wait for it.  Bitwise the global device-resident steps; the launch
-    count shows the wavefront ran (C volume + C interface launches + 1 pack per stage)."""
+    count shows the wavefront ran: per tick one segmented launch of the volume pieces and one
+    of the interface pieces (at most 4 per launch), 1 pack per stage."""
     ny, dt, nsteps = 16 * P, 1e-3, 3
 
     def mk(r):
@@ -523,5 +524,16 @@ def test_multirank_host_state_wavefront_equal_global(P, C):
     for r, (h, u) in enumerate(zip(hs, us)):
         j0, j1 = ny * r // P, ny * (r + 1) // P
         np.testing.assert_array_equal(u, ug[row * j0:row * j1])
-        assert h.launches - l0[r] == 5 * nsteps * (2 * C + 1)
+        assert h.launches - l0[r] == wave_launches(5 * nsteps, C)
         assert h.get_state()[2] == tg
+
+
+def wave_launches(G, C):
+    """Launches of the host-state wavefront over G stages with C chunks (N = 4 FAST):
+    volume pieces (g, p) go out at tick 6 g + p and interface pieces at 6 g + p + 3, merged
+    per tick in launches of <= 4 pieces; one pack per stage."""
+    ticks = {}
+    for g in range(G):
+        for p in range(C):
+            ticks[6 * g + p] = ticks.get(6 * g + p, 0) + 1
+    return 2 * sum((n + 3) // 4 for n in ticks.values()) + G
