@@ -158,6 +158,74 @@ __device__ __forceinline__ void warp_acc(long long* W, double x, int lane) {
     }
 }
 
+// Per-lane exact accumulation window (fewer warp-collective rounds): int64 limbs of
+// weight 2^(32 (J + i)), i < 5; a term's three signed digits land at offsets j - J ..
+// j - J + 2 (integer adds: exact).  The anchor J is set by the lane's first term of a
+// batch, one limb below it; a term outside the window goes through warp_acc at once,
+// and the window is flushed into the warp's limbs once per batch.
+struct LaneWin {
+    long long w[5];
+    int J;  // -1: empty
+};
+
+__device__ __forceinline__ void win_clear(LaneWin& a) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) a.w[i] = 0;
+    a.J = -1;
+}
+
+// false: x does not fit the window (the caller sends it through warp_acc)
+__device__ __forceinline__ bool win_add(LaneWin& a, double x) {
+    int j = 0;
+    int64_t d0 = 0, d1 = 0, d2 = 0;
+    if (!exact::split(x, j, d0, d1, d2)) return true;
+    if (a.J < 0) a.J = max(0, min(j - 1, exact::kLimbs - 6));
+    const int o = j - a.J;
+    if (o < 0 || o > 2) return false;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) a.w[i] += (i == o ? d0 : 0) + (i == o + 1 ? d1 : 0) + (i == o + 2 ? d2 : 0);
+    return true;
+}
+
+// Warp-collective: every lane's window into the warp's limbs W.  A window is normalised
+// to five digits in [0, 2^32) plus a signed top digit; lanes with equal anchors go in one
+// round (per digit: 16-bit halves summed with REDUX, exact in int32), lanes 0..5 add.
+__device__ __forceinline__ void win_flush(long long* W, LaneWin& a, int lane) {
+    int64_t D[6];
+    int64_t carry = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int64_t v = a.w[i] + carry;
+        carry = v >> 32;
+        D[i] = v - carry * 4294967296ll;
+    }
+    D[5] = carry;
+    unsigned pending = __ballot_sync(0xffffffffu, a.J >= 0);
+    while (pending) {
+        const bool mine_p = (pending >> lane) & 1u;
+        const int jr = __reduce_min_sync(0xffffffffu, mine_p ? a.J : 0x7fffffff);
+        const bool mine = mine_p && a.J == jr;
+        long long tot = 0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const int64_t v = mine ? D[q] : 0;
+            const uint64_t m = static_cast<uint64_t>(v < 0 ? -v : v);  // < 2^32
+            int lo = static_cast<int>(m & 0xffffu), hi = static_cast<int>(m >> 16);
+            if (v < 0) {
+                lo = -lo;
+                hi = -hi;
+            }
+            const int slo = __reduce_add_sync(0xffffffffu, lo);
+            const int shi = __reduce_add_sync(0xffffffffu, hi);
+            if (lane == q) tot = static_cast<long long>(shi) * 65536ll + slo;
+        }
+        if (lane < 6 && tot) W[jr + lane] += tot;
+        pending &= ~__ballot_sync(0xffffffffu, mine);
+        __syncwarp();
+    }
+    win_clear(a);
+}
+
 // vortex_exact (diagnostics.hpp:41-53).  exp is CUDA's (<= 1 ulp), not glibc's:
 // the exact-solution terms are within rounding of the reference's, not bitwise.
 __device__ __forceinline__ void vortex_exact_dev(const double* p, double x, double y, double t, double* ue) {
@@ -196,6 +264,9 @@ __global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
     const bool exact_sol = P.what == kDiagL2Vortex || P.what == kDiagL2Lake;
     unsigned long long kmin = order_key(1e300), kbad = ~0ull;
     unsigned nonfinite = 0;
+    LaneWin win[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) win_clear(win[q]);
     const long nbatch = ((long)P.K + kDiagBatch - 1) / kDiagBatch;
 
     for (long bt = (long)blockIdx.x * kDiagWarps + wid; bt < nbatch; bt += (long)gridDim.x * kDiagWarps) {
@@ -330,11 +401,16 @@ __global__ void __launch_bounds__(32 * kDiagWarps) diag_kernel(DiagParams P) {
                         tm[q] = 0.0;
                     }
             }
-            warp_acc(W[0], tm[0], lane);
-            warp_acc(W[1], tm[1], lane);
-            warp_acc(W[2], tm[2], lane);
-            if (inv) warp_acc(W[3], tm[3], lane);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < 3 || inv) {
+                    const bool ok = win_add(win[q], tm[q]);
+                    if (__any_sync(0xffffffffu, !ok)) warp_acc(W[q], ok ? 0.0 : tm[q], lane);
+                }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q < 3 || inv) win_flush(W[q], win[q], lane);
         __syncwarp();
     }
     // ---- merge: warp minima; warps' limbs -> block limbs -> record (integer adds: exact)
