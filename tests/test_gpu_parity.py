@@ -240,6 +240,41 @@ def test_host_state_stepping_equals_device_steps(mode, nchunks):
     assert ei.value.elem == 400 and abs(ei.value.t - 0.5) < 1e-12
 
 
+@pytest.mark.parametrize("nchunks", [6, 16])
+def test_host_state_wavefront_merged_launches_n4(nchunks, monkeypatch):
+    """N = 4 FAST host-state wavefront: each tick's volume pieces and interface pieces go
+    out as segmented launches (per-piece element range, stage id, LSRK coefficients);
+    bitwise the per-chunk launches (SWEDG_WAVE_MERGE=0) and the device-resident steps, and
+    a planted positivity failure reports the same element and stage time."""
+    c = capi.Case("smooth", N=4, nx=24, warp=0.1, seed=23)  # K = 1152
+    dt = c.dt
+    outs, errs = [], []
+    for merge in ("1", "0"):
+        monkeypatch.setenv("SWEDG_WAVE_MERGE", merge)
+        h = c.handle(mode=capi.MODE_FAST)
+        u = np.ascontiguousarray(c.u0())
+        h.set_state(u)
+        l0 = h.launches
+        h.step_host(u, dt, 3, nchunks)
+        outs.append((u, h.launches - l0))
+        bad = np.ascontiguousarray(c.u0())
+        bad[1000, 0, 3] = -1.0
+        h.set_state(bad, None, 0.5)
+        with pytest.raises(capi.PositivityError) as ei:
+            h.step_host(bad, dt, 2, nchunks)
+        errs.append((ei.value.elem, ei.value.t))
+        h.close()
+    hd = c.handle(mode=capi.MODE_FAST)
+    hd.set_state(c.u0())
+    hd.step(dt, 3)
+    ud = hd.get_state()[0]
+    np.testing.assert_array_equal(outs[0][0], ud)
+    np.testing.assert_array_equal(outs[1][0], ud)
+    # fewer launches when merged (with C <= 6 chunks no two pieces share a tick)
+    assert outs[0][1] < outs[1][1] if nchunks > 6 else outs[0][1] == outs[1][1]
+    assert errs[0] == errs[1] and errs[0][0] == 1000 and abs(errs[0][1] - 0.5) < 1e-12
+
+
 @pytest.mark.parametrize("N", [3, 4])
 def test_odd_element_count_imported_mesh(N):
     """Odd K (a pentagon fan of 5 triangles, wall boundary, imported through
