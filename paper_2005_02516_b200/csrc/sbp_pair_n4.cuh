@@ -245,12 +245,12 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         load_row(R0, r0);
         load_row(R1, r1);
         // ---- rows l', l'+16 x all 37 columns
-#pragma unroll 1
-        for (int j0 = 0; j0 < 36; j0 += 4) {
-            double2 qa[4], qb[4];
-            tmem_ld16x2(tbase + W::t0 + 4 * j0, tbase + W::t1 + 4 * j0, qa, qb);
+#pragma unroll 2
+        for (int j0 = 0; j0 < 36; j0 += 2) {  // two columns per TMEM load: 16 fewer live registers than four
+            double2 qa[2], qb[2];
+            tmem_ld8x2(tbase + W::t0 + 4 * j0, tbase + W::t1 + 4 * j0, qa, qb);
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
+            for (int p = 0; p < 2; ++p) {
                 const int j = j0 + p;
                 const double2 A = nA[j], B = nB[j], C = nC[j], D = nD[j];
                 const double hj = nH[j];

@@ -193,6 +193,25 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, uint32_t tb, double2 (&
     }
 }
 
+// Two x8 loads (2 (QA,QB) columns each) under one tcgen05.wait::ld.
+__device__ __forceinline__ void tmem_ld8x2(uint32_t ta, uint32_t tb, double2 (&qa)[2], double2 (&qb)[2]) {
+    uint32_t r[8], t[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta)
+                 : "memory");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7])
+                 : "r"(tb)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        qa[p] = make_double2(__hiloint2double(r[4 * p + 1], r[4 * p]), __hiloint2double(r[4 * p + 3], r[4 * p + 2]));
+        qb[p] = make_double2(__hiloint2double(t[4 * p + 1], t[4 * p]), __hiloint2double(t[4 * p + 3], t[4 * p + 2]));
+    }
+}
+
 __device__ __forceinline__ double2 tmem_ld4(uint32_t taddr) {
     uint32_t r0, r1, r2, r3;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
