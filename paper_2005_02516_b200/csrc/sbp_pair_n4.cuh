@@ -245,7 +245,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         load_row(R0, r0);
         load_row(R1, r1);
         // ---- rows l', l'+16 x all 37 columns
-#pragma unroll 2
+#pragma unroll 3
         for (int j0 = 0; j0 < 36; j0 += 2) {  // two columns per TMEM load: 16 fewer live registers than four
             double2 qa[2], qb[2];
             tmem_ld8x2(tbase + W::t0 + 4 * j0, tbase + W::t1 + 4 * j0, qa, qb);
