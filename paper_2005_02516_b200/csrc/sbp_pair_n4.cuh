@@ -6,7 +6,7 @@
 // live in TENSOR MEMORY (348 of 512 columns), so shared memory carries only the
 // node-j broadcasts (two addresses per warp, one per element), each feeding two
 // rows per lane; the next pair's state and geometric factors stream in with
-// cp.async during the flux loops.  Same arithmetic as sbp_rhs_kernel<4,false>
+// bulk (TMA) copies during the flux loops.  Same arithmetic as sbp_rhs_kernel<4,false>
 // (factored accumulation, reciprocal-form surface flux).  With prm.u_next set the
 // LSRK45 register update is fused (the state ping-pongs between two buffers, since
 // neighbours read the stage's input state).
@@ -38,14 +38,14 @@ struct SbpPairN4 {
     // device gf layout of SBP: volume rows of each column padded to sbp_gstride(37) = 38)
     static constexpr int sU = 0, sG = 222, gseg = sbp_gstride(37), slen = 526;
     // finish-phase inputs of a pair, bulk-copied as contiguous pair blocks (k0 even:
-    // 16 B aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15];
-    // nbr int[2][3] | perm int[2][15] by cp.async (8 B granules)
+    // 16 B aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15] |
+    // nbr int[2][3] + perm int[2][15] (one 144 B block of the handle's nbrperm array)
     static constexpr int rRes = 0, rSrc = 222, rMinv = 370, rSurf = 444, rNbr = 534, rPerm = 537, rlen = 552;
     static constexpr int per_warp = 2 * work_stride + slen + rlen;
     static constexpr size_t bytes() { return sizeof(double) * (size_t)WARPS * per_warp + 16; }
     // bytes per pair of each bulk group
     static constexpr uint32_t g1_bytes = 8u * (222 + 8 * gseg);
-    static constexpr uint32_t g2_bytes_nores = 8u * (148 + 74 + 90), g2_res = 8u * 222;
+    static constexpr uint32_t g2_bytes_nores = 8u * (148 + 74 + 90) + 144u, g2_res = 8u * 222;
 };
 
 __global__ void __launch_bounds__(SbpPairN4::T, 1)
@@ -155,7 +155,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             if (lane == 0) mbar_arrive(mb1);
         }
     };
-    // finish group: res/src/minv/surf pair blocks (bulk) and nbr/perm (cp.async)
+    // finish group: res/src/minv/surf and nbr/perm pair blocks (bulk copies on mb2)
     const bool with_res = prm.u_next != nullptr;
     auto issue_r = [&](int pr) {
         const int k0 = 2 * pr;
@@ -167,11 +167,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 bulk_g2s(rst + W::rSrc, prm.src + (size_t)k0 * 2 * nq, 8u * 148, mb2);
                 bulk_g2s(rst + W::rMinv, prm.minv + (size_t)k0 * nq, 8u * 74, mb2);
                 bulk_g2s(rst + W::rSurf, prm.surf + (size_t)k0 * 3 * nf, 8u * 90, mb2);
-            }
-            if (lane < 18) {  // nbr (3 granules) and perm (15 granules)
-                const int* src = lane < 3 ? prm.nbr + (size_t)k0 * 3 + 2 * lane : prm.perm + (size_t)k0 * nf + 2 * (lane - 3);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr_u32(rst + W::rNbr + lane)), "l"(src)
-                             : "memory");
+                bulk_g2s(rst + W::rNbr, prm.nbrperm + (size_t)pr * 36, 144u, mb2);  // nbr [2][3] | perm [2][15]
             }
         } else if (k0 < prm.K) {  // odd K: last element alone
             for (int x = lane; x < 3 * nq; x += 32)
@@ -185,7 +181,6 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             __syncwarp();
             if (lane == 0) mbar_arrive(mb2);
         }
-        cp_async_commit();
     };
 
     if (gw < npairs) {
@@ -266,7 +261,6 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         }
         // ---- the pair's finish-phase inputs (issued one flux loop ago)
         mbar_wait(mb2, phase);
-        cp_async_wait_all();
         __syncwarp();
         // ---- rows 32..36: columns ph, ph+3, ... (13 slots), three lanes per row (the row is
         //      loaded only now: it holds no registers through the main loop)
@@ -396,7 +390,6 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         __syncwarp();
         if (pr + nw < npairs) issue_r(pr + nw);
     }
-    cp_async_wait_all();
 
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();

@@ -65,6 +65,7 @@ struct swedg_handle_s {
     double* Mpk = nullptr;   // modal FAST: [K][Np(Np+1)/2] symmetrised packed M_h^{-1}
     int* nbr = nullptr;      // [K][3]
     int* perm = nullptr;     // [K][nf]
+    int* nbrperm = nullptr;  // SBP: per element pair nbr [2][3] | perm [2][nf] (36 ints, one bulk copy)
     int* fidx = nullptr;     // SBP face_index [nf]
     double* bs = nullptr;    // [K][nh] (modal)
     double* src = nullptr;   // [K][2][nh] (SBP: [K][2][nq])
@@ -452,6 +453,7 @@ int run_sbp_stage(swedg_handle h, const StageArgs& sa) {
     sp.minv = h->Minv + b * nq;
     sp.nbr = h->nbr + b * 3;
     sp.perm = h->perm + b * nf;
+    sp.nbrperm = h->nbrperm ? h->nbrperm + (b / 2) * 36 : nullptr;  // pair path: b even
     sp.du = sa.du_out ? sa.du_out + b * 3 * nq : nullptr;
     sp.uo = h->u;
     sp.res = h->res + b * 3 * nq;
@@ -1183,6 +1185,18 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
                 if (d->nbr[k * 3 + f] < 0)
                     for (int s = 0; s < npf; ++s) perm[k * nf + f * npf + s] = 0;
         if (dalloc(h, &h->perm, K * nf) || upload(h, h->perm, perm.data(), K * nf)) return bail(h->last_code);
+        if (h->scheme == SWEDG_SCHEME_SBP) {  // the SBP pair kernel's per-pair block: nbr [2][3] | perm [2][15]
+            const size_t np = (K + 1) / 2;
+            std::vector<int> blk(np * 36, -1);
+            for (size_t k = 0; k < K; ++k) {
+                int* b = blk.data() + (k / 2) * 36;
+                const int e = (int)(k & 1);
+                for (int f = 0; f < 3; ++f) b[3 * e + f] = d->nbr[k * 3 + f];
+                for (int x = 0; x < nf; ++x) b[6 + nf * e + x] = perm[k * nf + x];
+            }
+            if (dalloc(h, &h->nbrperm, blk.size()) || upload(h, h->nbrperm, blk.data(), blk.size()))
+                return bail(h->last_code);
+        }
     }
     if (h->scheme == SWEDG_SCHEME_HYBRIDIZED) {
         if (dalloc(h, &h->Minv, K * Np * Np) || upload(h, h->Minv, d->Mh_inv, K * Np * Np)) return bail(h->last_code);
@@ -1252,7 +1266,7 @@ int swedg_destroy(swedg_handle h) {
     if (h->comm) cudaStreamSynchronize(h->comm);
     p2p_detach(h);
     if (h->p2p_flags) cudaFree(h->p2p_flags);
-    void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->fidx,  h->bs,   h->src,
+    void* ptrs[] = {h->ops, h->gf,  h->surf, h->Minv, h->Mpk, h->nbr,  h->perm, h->nbrperm, h->fidx,  h->bs,   h->src,
                     h->u,   h->res, h->utmp, h->du,   h->proj, h->trace, h->accf, h->T1,  h->err,  h->fine,
                     h->dPq, h->map, h->bmod, h->uref, h->drec, h->series, h->wJ, h->u_alt, h->u_alt2,
                     h->pack_src, h->pack_dst, h->sendbuf};
