@@ -35,7 +35,7 @@ struct SbpParams {
     const double* minv;  // [K][nq]
     const int* nbr;      // [K][3]
     const int* perm;     // [K][nf]
-    const int* nbrperm;  // pair kernel (N = 4): per element pair nbr [2][3] | perm [2][15]
+    const int* nbrperm;  // pair kernel (N = 4): per element pair nbr [2][3] | face_index[perm] [2][15]
     double* du;          // rhs-mode output
     double* uo;          // RK-mode state (unused here)
     double* res;

@@ -39,7 +39,7 @@ struct SbpPairN4 {
     static constexpr int sU = 0, sG = 222, gseg = sbp_gstride(37), slen = 526;
     // finish-phase inputs of a pair, bulk-copied as contiguous pair blocks (k0 even:
     // 16 B aligned): res [2][3][37] | src [2][2][37] | minv [2][37] | surf [2][3][15] |
-    // nbr int[2][3] + perm int[2][15] (one 144 B block of the handle's nbrperm array)
+    // nbr int[2][3] + neighbour volume node int[2][15] (one 144 B block of the handle's nbrperm)
     static constexpr int rRes = 0, rSrc = 222, rMinv = 370, rSurf = 444, rNbr = 534, rPerm = 537, rlen = 552;
     static constexpr int per_warp = 2 * work_stride + slen + rlen;
     static constexpr size_t bytes() { return sizeof(double) * (size_t)WARPS * per_warp + 16; }
@@ -167,7 +167,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 bulk_g2s(rst + W::rSrc, prm.src + (size_t)k0 * 2 * nq, 8u * 148, mb2);
                 bulk_g2s(rst + W::rMinv, prm.minv + (size_t)k0 * nq, 8u * 74, mb2);
                 bulk_g2s(rst + W::rSurf, prm.surf + (size_t)k0 * 3 * nf, 8u * 90, mb2);
-                bulk_g2s(rst + W::rNbr, prm.nbrperm + (size_t)pr * 36, 144u, mb2);  // nbr [2][3] | perm [2][15]
+                bulk_g2s(rst + W::rNbr, prm.nbrperm + (size_t)pr * 36, 144u, mb2);  // nbr [2][3] | nodes [2][15]
             }
         } else if (k0 < prm.K) {  // odd K: last element alone
             for (int x = lane; x < 3 * nq; x += 32)
@@ -177,7 +177,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
             for (int x = lane; x < 3 * nf; x += 32) rst[W::rSurf + x] = prm.surf[(size_t)k0 * 3 * nf + x];
             int* ri = reinterpret_cast<int*>(rst + W::rNbr);
             for (int x = lane; x < 3; x += 32) ri[x] = prm.nbr[(size_t)k0 * 3 + x];
-            for (int x = lane; x < nf; x += 32) ri[6 + x] = prm.perm[(size_t)k0 * nf + x];
+            for (int x = lane; x < nf; x += 32) ri[6 + x] = prm.fidx[prm.perm[(size_t)k0 * nf + x]];
             __syncwarp();
             if (lane == 0) mbar_arrive(mb2);
         }
@@ -280,7 +280,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
         }
         // ---- the neighbour traces of the owned surface rows (after the rows 32..36 loop:
         //      measured 1 % faster than before it, the loop's registers being free by now)
-        const int* ri = reinterpret_cast<const int*>(rst + W::rNbr);  // nbr [2][3] | perm [2][15]
+        const int* ri = reinterpret_cast<const int*>(rst + W::rNbr);  // nbr [2][3] | neighbour nodes [2][15]
         double nb3[3][3];
         {
             const int slots[3] = {slot0, slot1, (xrow && ph == 0) ? slotX : -1};
@@ -295,7 +295,7 @@ sbp_rhs_pair_n4_kernel(SbpParams prm) {
                 if (valid && slot >= 0) {
                     const int nb = ri[half * 3 + slot / npf];
                     if (nb >= 0) {
-                        const double* un = prm.u_nb + (size_t)nb * 3 * nq + prm.fidx[ri[6 + half * nf + slot]];
+                        const double* un = prm.u_nb + (size_t)nb * 3 * nq + ri[6 + half * nf + slot];
                         nb3[q][0] = un[0];
                         nb3[q][1] = un[nq];
                         nb3[q][2] = un[2 * nq];

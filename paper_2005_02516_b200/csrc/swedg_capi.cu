@@ -65,7 +65,7 @@ struct swedg_handle_s {
     double* Mpk = nullptr;   // modal FAST: [K][Np(Np+1)/2] symmetrised packed M_h^{-1}
     int* nbr = nullptr;      // [K][3]
     int* perm = nullptr;     // [K][nf]
-    int* nbrperm = nullptr;  // SBP: per element pair nbr [2][3] | perm [2][nf] (36 ints, one bulk copy)
+    int* nbrperm = nullptr;  // SBP: per element pair nbr [2][3] | neighbour node [2][nf] (36 ints, one bulk copy)
     int* fidx = nullptr;     // SBP face_index [nf]
     double* bs = nullptr;    // [K][nh] (modal)
     double* src = nullptr;   // [K][2][nh] (SBP: [K][2][nq])
@@ -1185,14 +1185,16 @@ int swedg_create(const swedg_desc* d, swedg_handle* out) {
                 if (d->nbr[k * 3 + f] < 0)
                     for (int s = 0; s < npf; ++s) perm[k * nf + f * npf + s] = 0;
         if (dalloc(h, &h->perm, K * nf) || upload(h, h->perm, perm.data(), K * nf)) return bail(h->last_code);
-        if (h->scheme == SWEDG_SCHEME_SBP) {  // the SBP pair kernel's per-pair block: nbr [2][3] | perm [2][15]
+        if (h->scheme == SWEDG_SCHEME_SBP) {
+            // the SBP pair kernel's per-pair block: nbr [2][3] | the neighbour's volume node of
+            // each face slot [2][15] (face_index[perm], solver.hpp:405-407; 0 on walls)
             const size_t np = (K + 1) / 2;
             std::vector<int> blk(np * 36, -1);
             for (size_t k = 0; k < K; ++k) {
                 int* b = blk.data() + (k / 2) * 36;
                 const int e = (int)(k & 1);
                 for (int f = 0; f < 3; ++f) b[3 * e + f] = d->nbr[k * 3 + f];
-                for (int x = 0; x < nf; ++x) b[6 + nf * e + x] = perm[k * nf + x];
+                for (int x = 0; x < nf; ++x) b[6 + nf * e + x] = d->face_index[perm[k * nf + x]];
             }
             if (dalloc(h, &h->nbrperm, blk.size()) || upload(h, h->nbrperm, blk.data(), blk.size()))
                 return bail(h->last_code);
