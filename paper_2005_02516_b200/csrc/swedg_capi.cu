@@ -1521,10 +1521,13 @@ namespace {
 // Capture one LSRK45 step on the handle's stream into a CUDA graph (cached per
 // dt / stream / mode / penalty).  Stage ids baked into the graph are
 // graph_base..graph_base+4; record_error adds 5 x the device step counter.
+bool step_graph_ready(swedg_handle h, double dt) {
+    return h->graph_exec && h->graph_dt == dt && h->graph_stream == h->stream && h->graph_mode == h->mode &&
+           h->graph_penalty == h->penalty;
+}
+
 int capture_step_graph(swedg_handle h, double dt) {
-    if (h->graph_exec && h->graph_dt == dt && h->graph_stream == h->stream && h->graph_mode == h->mode &&
-        h->graph_penalty == h->penalty)
-        return SWEDG_OK;
+    if (step_graph_ready(h, dt)) return SWEDG_OK;
     if (h->graph_exec) {
         cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
@@ -1576,7 +1579,9 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync) {
                     "multi-rank handle: set a halo map and a transport (swedg_set_halo + swedg_set_nccl_comm / "
                     "swedg_set_exchange) or use the stage-level API");
     // a caller's exchange callback may not be capturable: individual launches then
-    const bool graphs = h->use_graphs && !h->timers && nsteps >= 2 && !(halo_active(h) && h->xfn);
+    // (a single step replays the graph too once it exists, e.g. in a run loop sampling every step)
+    const bool graphs = h->use_graphs && !h->timers && (nsteps >= 2 || (nsteps == 1 && step_graph_ready(h, dt))) &&
+                        !(halo_active(h) && h->xfn);
     if (graphs) {
         if (capture_step_graph(h, dt)) return h->last_code;
         // replay n, stage s reports id (first id of this call) + 5 n + s
@@ -2261,6 +2266,10 @@ int swedg_run(swedg_handle h, double dt, double tfinal, int sample_every, int ma
         return swedg_sample_invariants(h, ns++);
     };
     if (take()) return h->last_code;
+    // samples every step or every few steps: capture the step graph up front so that even
+    // one-step flushes replay it instead of launching the kernels one by one
+    if (cadence < 8 && nsteps >= 2 && h->use_graphs && !h->timers && !(halo_active(h) && h->xfn))
+        if (capture_step_graph(h, dt)) return h->last_code;
     int pending = 0;  // full-dt steps not yet enqueued
     auto flush = [&]() -> int {
         if (pending == 0) return SWEDG_OK;

@@ -184,9 +184,9 @@ def test_oracle_agrees_with_gpu_on_perturbed_state():
 
 
 def test_graph_replay_equals_individual_launches_and_reports_step():
-    """swedg_step_lsrk45 with nsteps >= 2 replays a captured one-step CUDA graph: bitwise
-    equal to individually launched steps; an error in a later step is attributed to the
-    right element and stage time."""
+    """swedg_step_lsrk45 with nsteps >= 2 replays a captured one-step CUDA graph (and a
+    one-step call replays it once it exists): bitwise equal to individually launched steps;
+    an error in a later step is attributed to the right element and stage time."""
     c = load_golden("c1_vortex")
     dt = float(c["dt"][0])
     h1 = make(c, capi.MODE_FAST)
@@ -197,11 +197,18 @@ def test_graph_replay_equals_individual_launches_and_reports_step():
     h2 = make(c, capi.MODE_FAST)
     h2.set_state(c["u"])
     h2.step(dt, 3)
-    h2.step(dt, 3)
+    h2.step(dt, 2)
+    h2.step(dt, 1)  # one step: the existing graph is replayed (run loops sampling every step)
     u2, r2, t2 = h2.get_state()
     np.testing.assert_array_equal(u1, u2)
     np.testing.assert_array_equal(r1, r2)
     assert t1 == t2
+    bad1 = np.array(c["u"], copy=True)
+    bad1[9, 0, 0] = -1.0
+    h2.set_state(bad1, None, 0.125)
+    with pytest.raises(capi.PositivityError) as ei:
+        h2.step(dt, 1)
+    assert ei.value.elem == 9 and abs(ei.value.t - 0.125) < 1e-12
     # positivity failure planted in element 7: reported with element id and a stage time
     bad = np.array(c["u"], copy=True)
     bad[7, 0, 0] = -1.0

@@ -263,6 +263,7 @@ def test_nccl_self_exchange_single_rank_graph():
             h.set_nccl_comm(comm)
             h.set_state(c.u0())
             h.step(dt, 3)  # graph capture + replay
+            h.set_graphs(False)
             h.step(dt, 1)  # individual launches
             u, _, t = h.get_state()
         finally:
@@ -370,6 +371,7 @@ def test_p2p_self_exchange_single_rank(scheme, N, mode):
     h.set_state(c.u0())
     attach_p2p_local([h])
     h.step(dt, 3)
+    h.set_graphs(False)
     h.step(dt, 1)
     u, _, t = h.get_state()
     np.testing.assert_array_equal(u, ug)
@@ -403,6 +405,7 @@ def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
         out = {}
         if job == "steps":
             h.step(1e-3, 3)  # captured step graph, replayed
+            h.set_graphs(False)
             h.step(1e-3, 1)  # individual launches
             out["u"] = h.get_state()[0]
         elif job == "host":
