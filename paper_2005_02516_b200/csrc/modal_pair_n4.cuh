@@ -396,12 +396,12 @@ modal_volume_pair_n4_kernel(ModalVolParams prm) {
                 }
             }
             {  // row rC (doubles 30..44)
-                double Vb[16], Vc[16];
-                tmem_ld32d(tbase + W::tV + 32, Vb);   // 16..31
-                tmem_ld32d(tbase + W::tV + 64, Vc);   // 32..47
+                double Vc[16];
+                const double2 v30 = tmem_ld4(tbase + W::tV + 60);  // doubles 30, 31
+                tmem_ld32d(tbase + W::tV + 64, Vc);              // 32..47
 #pragma unroll
                 for (int m = 0; m < Np; ++m) {
-                    const double c = (m + 30 < 32) ? Vb[m + 14] : Vc[m - 2];
+                    const double c = m == 0 ? v30.x : (m == 1 ? v30.y : Vc[m - 2]);
                     vt[2][0] = __fma_rn(c, work[W::wVh + m], vt[2][0]);
                     vt[2][1] = __fma_rn(c, work[W::wVh + Np + m], vt[2][1]);
                     vt[2][2] = __fma_rn(c, work[W::wVh + 2 * Np + m], vt[2][2]);
