@@ -432,6 +432,7 @@ def _p2p_rank_main(rank, P, scaling, scheme, mode, job, dt, port, q):
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("scaling,P,scheme,mode,job", [
     ("strong", 2, 0, "fast", "steps"), ("strong", 3, 0, "fast", "steps"), ("weak", 2, 0, "fast", "steps"),
+    ("weak", 2, 1, "fast", "steps"), ("weak", 3, 0, "parity", "steps"),
     ("strong", 3, 0, "parity", "steps"), ("strong", 2, 1, "fast", "steps"), ("strong", 3, 1, "fast", "steps"),
     ("strong", 3, 1, "parity", "steps"), ("strong", 3, 0, "fast", "host"), ("strong", 3, 0, "fast", "hostwave"),
     ("strong", 3, 0, "fast", "run"), ("strong", 3, 1, "fast", "run")])
