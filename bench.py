@@ -581,8 +581,8 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "steps": args.e2e_steps,
                 "path": "swedg_step_lsrk45_host: per step H2D of the state from pinned host memory + 5 "
-                        "stages + D2H of the result" + ("; 16 element chunks run through the stages as a "
-                                                         "wavefront so copies overlap compute" if world == 1 else
+                        "stages + D2H of the result" + ("; element chunks (24 at N=4 FAST) run through the "
+                                                         "stages as a wavefront so copies overlap compute" if world == 1 else
                                                          " (per rank; bytes are per rank)")},
         "gpu_launches": launches,
         "roofline": roofline,

@@ -173,7 +173,8 @@ int swedg_step_lsrk45(swedg_handle h, double dt, int nsteps, int sync);
 /* The same steps on a HOST-resident state u_host [K][3][Np] (the reference's
  * calling pattern: state.u lives on the host between steps).  Each step reads
  * its input from u_host and writes its result back; the transfers are
- * pipelined with the compute in `nchunks` element chunks (0 = 16).  When every
+ * pipelined with the compute in `nchunks` element chunks (0 = the default: 24 for the N = 4
+ * FAST path, whose wavefront merges each tick's launches, 16 otherwise).  When every
  * element's neighbours lie in its own or an adjacent chunk (row-ordered meshes),
  * the chunks run through the stages and steps as a wavefront, so a chunk's
  * D2H, its H2D for the next step and other chunks' kernels all overlap;
